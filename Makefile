@@ -1,0 +1,67 @@
+# Build of the B200-native AdaGScale renderer.
+#
+#   make            -> paper_2604_18980_b200/lib/libagsx.so   (CUDA kernels + C-ABI, sm_100a)
+#                      paper_2604_18980_b200/lib/libags.so    (C++ ags:: drop-in API over the C-ABI)
+#                      paper_2604_18980_b200/_core*.so        (pybind11 mirror of adagscale._core)
+#                      oracle/_build/libags_oracle.so         (test oracle, C restatement)
+#                      oracle/_ref/libags_ref.so              (test oracle, reference sources; only
+#                                                              when /root/reference exists)
+PKG      := paper_2604_18980_b200
+CSRC     := $(PKG)/csrc
+LIBDIR   := $(PKG)/lib
+PYTHON   ?= python3
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+CUDA_INC := /usr/local/cuda/include
+CUDA_LIB := /usr/local/cuda/lib64
+
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+# --fmad=false: the reference path has no FMA contraction.
+NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -prec-div=true -prec-sqrt=true \
+             -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills -Iinclude
+HOSTFLAGS := -std=gnu++20 -O3 -fPIC -ffp-contract=off -fno-fast-math -Iinclude -I$(CSRC)/host
+
+CU_SRCS  := $(CSRC)/k_preprocess.cu $(CSRC)/k_pairs.cu $(CSRC)/k_sort.cu $(CSRC)/k_raster.cu \
+            $(CSRC)/agsx_api.cu
+CU_OBJS  := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
+CU_HDRS  := $(wildcard $(CSRC)/*.cuh) include/agsx.h
+
+HOST_SRCS := $(wildcard $(CSRC)/host/*.cpp)
+HOST_OBJS := $(patsubst $(CSRC)/host/%.cpp,build/host_%.o,$(HOST_SRCS))
+HOST_HDRS := $(wildcard $(CSRC)/host/*.hpp) $(wildcard include/ags/*.hpp) include/agsx.h
+
+PY_EXT   := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_config_var('EXT_SUFFIX'))")
+PY_INC   := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_paths()['include'])")
+PYBIND   := $(shell $(PYTHON) -c "import pybind11;print(pybind11.get_include())")
+CORE     := $(PKG)/_core$(PY_EXT)
+
+all: $(LIBDIR)/libagsx.so $(LIBDIR)/libags.so $(CORE) oracle
+.PHONY: all oracle clean
+
+build/%.o: $(CSRC)/%.cu $(CU_HDRS)
+	@mkdir -p build
+	$(NVCC) $(NVCCFLAGS) -c $< -o $@
+
+$(LIBDIR)/libagsx.so: $(CU_OBJS)
+	@mkdir -p $(LIBDIR)
+	$(CXX) -shared -o $@ $^ -L$(CUDA_LIB) -lcudart_static -ldl -lrt -lpthread \
+	    -Wl,--exclude-libs,ALL -Wl,-soname,libagsx.so
+
+build/host_%.o: $(CSRC)/host/%.cpp $(HOST_HDRS)
+	@mkdir -p build
+	$(CXX) $(HOSTFLAGS) -c $< -o $@
+
+$(LIBDIR)/libags.so: $(HOST_OBJS) $(LIBDIR)/libagsx.so
+	$(CXX) -shared -o $@ $(HOST_OBJS) -L$(LIBDIR) -lagsx -Wl,-rpath,'$$ORIGIN' -Wl,-soname,libags.so
+
+$(CORE): $(CSRC)/python/bindings.cpp $(LIBDIR)/libags.so $(HOST_HDRS)
+	$(CXX) $(HOSTFLAGS) -shared -I$(PY_INC) -I$(PYBIND) $< -o $@ -L$(LIBDIR) -lags -lagsx \
+	    -Wl,-rpath,'$$ORIGIN/lib'
+
+oracle:
+	$(MAKE) -C oracle liboracle
+	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; fi
+
+clean:
+	rm -rf build $(LIBDIR) $(PKG)/_core*.so
+	$(MAKE) -C oracle clean

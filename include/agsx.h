@@ -1,0 +1,207 @@
+/*
+ * agsx.h -- C-ABI of the B200-native AdaGScale renderer (libagsx.so).
+ *
+ * This is the drop-in boundary below the reference's `ags::render()`.  Every
+ * entry point takes plain pointers and sizes, returns an int status and never
+ * throws.  Each function names the reference interface it replaces
+ * (/root/reference/proj/... file:line).
+ *
+ * Status codes (mapped by the C++ layer to the reference's exceptions):
+ *   AGSX_OK            0
+ *   AGSX_EINVAL        1  -> std::invalid_argument   (rasterizer.cpp:105-108,
+ *                                                     preprocess.cpp:123-125)
+ *   AGSX_EPAIR_BUDGET  2  -> ags::PairBudgetError    (pair_gen.hpp:74-76,
+ *                                                     pair_gen.cpp:181-184)
+ *   AGSX_ECUDA         3  -> std::runtime_error
+ *   AGSX_ENOMEM        4  -> std::runtime_error (std::bad_alloc)
+ *   AGSX_ECAPACITY     5  caller buffer too small; required size returned
+ *
+ * Threading: one agsx_ctx per host thread per GPU; a ctx owns one CUDA
+ * stream and grow-only device arenas.  Scenes are immutable once uploaded
+ * and may be shared by contexts on the same device.
+ */
+#ifndef AGSX_H
+#define AGSX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AGSX_ABI_VERSION 1
+
+enum {
+    AGSX_OK = 0,
+    AGSX_EINVAL = 1,
+    AGSX_EPAIR_BUDGET = 2,
+    AGSX_ECUDA = 3,
+    AGSX_ENOMEM = 4,
+    AGSX_ECAPACITY = 5
+};
+
+/* ags::Mode (scene.hpp:60); values equal the reference enum order. */
+enum { AGSX_MODE_AABB = 0, AGSX_MODE_OBB = 1, AGSX_MODE_ELLIPSE = 2, AGSX_MODE_ADAGSCALE = 3 };
+
+/* agsx_config.flags */
+enum {
+    /* Evaluate every blend alpha with the glibc-exact expf (bit-identical
+     * image to the CPU reference).  Without it the rasterizer uses the
+     * hardware ex2 path and re-evaluates exactly only when alpha is within a
+     * guard band of tau or of the clamp, so every blend decision is still
+     * exact and colours differ by O(1e-7). */
+    AGSX_FLAG_EXACT_ALPHA = 1
+};
+
+/* ags::Camera (scene.hpp:34-39). rotation: world-to-camera, row-major. */
+typedef struct {
+    float position[3];
+    float rotation[9];
+    float fx, fy;
+    int32_t width, height;
+} agsx_camera;
+
+/* ags::RenderConfig (scene.hpp:65-78) plus B200-path flags. */
+typedef struct {
+    int32_t tile_size;
+    float alpha_threshold;
+    float transmittance_floor;
+    float alpha_clamp;
+    float near_plane;
+    float guard_band;
+    int32_t mode;
+    float k;
+    int32_t thread_count; /* accepted, no device meaning (parallel.hpp:10-14) */
+    float background[3];
+    int32_t fixed_radius_aabb;
+    uint64_t pair_budget;
+    uint32_t flags; /* AGSX_FLAG_* */
+} agsx_config;
+
+/* ags::TUpperLUT (lut.hpp:11-26).  bin_count == 0 -> the all-ones default. */
+typedef struct {
+    float depth_min, depth_max;
+    int32_t bin_count;
+    const float* bins;
+} agsx_lut;
+
+/* Host SoA scene description for upload.  Replaces the
+ * std::span<const ags::Gaussian3D> argument of render() (rasterizer.hpp:63);
+ * Gaussian3D (scene.hpp:15-21) is AoS with a heap SH vector.
+ * sh is coefficient-major per Gaussian: sh[i*3*D + k*3 + c], D in {1,4,9,16}. */
+typedef struct {
+    uint64_t count;
+    int32_t sh_coeffs;
+    const float* mean;     /* 3*count */
+    const float* scale;    /* 3*count */
+    const float* rotation; /* 4*count, w x y z */
+    const float* opacity;  /* count */
+    const float* sh;       /* 3*sh_coeffs*count */
+} agsx_scene_desc;
+
+/* ags::SplatView (preprocess.hpp:15-24), byte-identical layout (60 B). */
+typedef struct {
+    float mean2d[2];
+    float cov2d[3];
+    float inv_cov[3];
+    float depth;
+    float rgb[3];
+    float opacity;
+    float th;
+    uint32_t source_id;
+} agsx_splat_view;
+
+/* Output of one frame (ags::RenderReport, rasterizer.hpp:31-40). */
+typedef struct {
+    float* image;          /* optional host H*W*3 f32 (HWC); NULL = keep on device */
+    float* max_t;          /* optional host, scene count entries, indexed by
+                              Gaussian id (RecordOptions::max_t; 0 = never blended) */
+    uint64_t pair_count;   /* out */
+    uint64_t splat_count;  /* out */
+    float stage_ms[4];     /* out: preprocess, pair_gen, sort, raster (device time) */
+} agsx_frame;
+
+typedef struct agsx_ctx agsx_ctx;
+typedef struct agsx_scene agsx_scene;
+
+/* ---- context --------------------------------------------------------- */
+int agsx_create(int device, agsx_ctx** out);
+void agsx_destroy(agsx_ctx* ctx);
+/* Last error message of this ctx (never NULL). */
+const char* agsx_last_error(const agsx_ctx* ctx);
+int agsx_abi_version(void);
+/* The ctx's CUDA stream (cudaStream_t) for event timing / interop. */
+void* agsx_stream(agsx_ctx* ctx);
+
+/* ---- scene (replaces passing the host span on every render) ---------- */
+int agsx_scene_upload(agsx_ctx* ctx, const agsx_scene_desc* desc, agsx_scene** out);
+void agsx_scene_free(agsx_scene* scene);
+uint64_t agsx_scene_count(const agsx_scene* scene);
+
+/* ---- the hot path: ags::render() (rasterizer.cpp:102-165) ------------ */
+/* Synchronous: validates like render() (scene.cpp:41-59,113-123), runs the
+ * four device stages, copies requested outputs to the host. */
+int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                const agsx_config* cfg, const agsx_lut* lut, agsx_frame* out);
+
+/* Asynchronous form for benchmarking / batching: enqueues one frame on the
+ * ctx stream and returns.  Results stay on the device; agsx_render_wait()
+ * synchronises, checks the budget/overflow status and fills counts and
+ * stage times of the most recent frame.  No host synchronisation occurs
+ * between the enqueued stages. */
+int agsx_render_async(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                      const agsx_config* cfg, const agsx_lut* lut);
+int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out);
+
+/* Device pointer to the ctx-owned image of the most recent frame
+ * (H*W*3 f32, HWC) and its dimensions. */
+int agsx_device_image(agsx_ctx* ctx, float** dptr, int32_t* width, int32_t* height);
+
+/* ---- parity hooks over the most recent fused frame ------------------- */
+/* Per-Gaussian tile counts (0 for culled Gaussians) and survivor flags
+ * (pair_gen.cpp:167-175 tile_counts, indexed by Gaussian id rather than by
+ * compacted splat index). */
+int agsx_dump_tile_counts(agsx_ctx* ctx, uint32_t* counts, uint8_t* alive, uint64_t n);
+/* Sorted pair list: key = (tile << 32) | bits(depth) (pair_gen.hpp:33-36),
+ * value = Gaussian id (maps to the reference splat_index via source_id). */
+int agsx_dump_sorted_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* gids, uint64_t capacity,
+                           uint64_t* out_count);
+/* Per-tile [start, end) ranges, 2*tile_count u32 (pair_sort.cpp:30-42). */
+int agsx_dump_ranges(agsx_ctx* ctx, uint32_t* ranges, uint64_t tile_count);
+
+/* ---- stage-level entry points (the reference's per-stage API) -------- */
+/* preprocess_view (preprocess.hpp:51-54): out holds scene count entries. */
+int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                         const agsx_config* cfg, const agsx_lut* lut, agsx_splat_view* out,
+                         uint64_t* out_count);
+/* generate_pairs (pair_gen.hpp:70-72) over a host splat list.  keys /
+ * splat_index hold `capacity` entries; AGSX_ECAPACITY with *out_total set if
+ * too small.  tile_counts: n entries. */
+int agsx_generate_pairs(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n,
+                        int32_t width, int32_t height, int32_t mode, const agsx_config* cfg,
+                        uint64_t* keys, uint32_t* splat_index, uint64_t capacity,
+                        uint32_t* tile_counts, uint64_t* out_total);
+/* sort_pairs (pair_sort.hpp:19): stable ascending by the full 64-bit key,
+ * in place; ranges: 2*tile_count u32. */
+int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64_t n,
+                    int32_t tile_count, uint32_t* ranges);
+/* raster_tile over every tile (rasterizer.hpp:54-58, rasterizer.cpp:137-147).
+ * image: H*W*3 host; max_t optional (n_splats entries). */
+int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
+                const uint32_t* splat_index, uint64_t n_pairs, const uint32_t* ranges,
+                int32_t width, int32_t height, const agsx_config* cfg, float* image,
+                float* max_t);
+
+/* ---- device libm pinning (glibc-exact logf / expf used on the path) -- */
+int agsx_device_logf(agsx_ctx* ctx, const float* x, float* y, uint64_t n);
+int agsx_device_expf(agsx_ctx* ctx, const float* x, float* y, uint64_t n);
+
+/* Number of kernels this ctx has launched since creation. */
+uint64_t agsx_kernel_launches(const agsx_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AGSX_H */

@@ -1,0 +1,947 @@
+// agsx_api.cu -- C-ABI of libagsx.so: contexts, device arenas, scene upload
+// and the per-frame launch sequence of the render path.
+//
+//   reference: render()          rasterizer.cpp:102-165
+//              validate(cfg/cam) scene.cpp:41-59, 113-123
+//              stage API         preprocess.hpp:51-54, pair_gen.hpp:70-72,
+//                                pair_sort.hpp:19, rasterizer.hpp:54-58
+//
+// A frame is enqueued on the ctx stream without any host synchronisation:
+// every data-dependent size (survivors, splats with tiles, pair count) stays
+// on the device and the kernels that consume it are persistent grids that
+// read it there.  The host reads one 128-byte counter block when the caller
+// waits for the frame; a pair count above the buffer capacity (but within
+// pair_budget) grows the pair arena and re-runs the frame.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace agsx;
+
+namespace {
+
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct StatusError {
+    int code;
+    std::string msg;
+};
+
+#define AGSX_CUDA(call)                                                                 \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            throw StatusError{e_ == cudaErrorMemoryAllocation ? AGSX_ENOMEM : AGSX_ECUDA, \
+                              std::string(#call) + ": " + cudaGetErrorString(e_)};      \
+    } while (0)
+
+}  // namespace
+
+struct agsx_scene {
+    int device = 0;
+    uint64_t n = 0;
+    int D = 1;
+    Buf pos_op, rot, scale_r, sh_gb, sh_rest;
+    DevScene view() const {
+        DevScene s;
+        s.n = n;
+        s.sh_coeffs = D;
+        s.pos_op = static_cast<const float4*>(pos_op.p);
+        s.rot = static_cast<const float4*>(rot.p);
+        s.scale_r = static_cast<const float4*>(scale_r.p);
+        s.sh_gb = static_cast<const float2*>(sh_gb.p);
+        s.sh_rest = static_cast<const float*>(sh_rest.p);
+        return s;
+    }
+};
+
+struct agsx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err = "";
+    uint64_t launches = 0;
+    uint32_t epoch = 1;
+    int num_sms = 148;
+    int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1;
+
+    // device arenas (grow-only)
+    Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2;
+    Buf tkeys, pvals, tkeys2, pvals2;
+    Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext;
+    Buf tmp0, tmp1, tmp2, tmp3, tmp4;
+    uint64_t pair_capacity = 0;
+
+    Counters* h_ctr = nullptr;  // pinned
+    cudaEvent_t ev[6] = {};
+
+    // most recent fused frame
+    bool have_frame = false;
+    const agsx_scene* f_scene = nullptr;
+    agsx_camera f_cam{};
+    agsx_config f_cfg{};
+    std::vector<float> f_lut;
+    float f_lut_dmin = 0.0f, f_lut_dmax = 100.0f;
+    bool f_has_lut = false;
+    FrameParams f_params{};
+    bool f_maxt = false;
+    uint32_t* f_tkeys = nullptr;
+    uint32_t* f_pvals = nullptr;
+    int f_tile_count = 0;
+};
+
+namespace {
+
+void ensure(Buf& b, size_t bytes, bool zero = false) {
+    if (b.bytes >= bytes) return;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    const size_t alloc = std::max<size_t>(bytes, 256);
+    AGSX_CUDA(cudaMalloc(&b.p, alloc));
+    if (zero) AGSX_CUDA(cudaMemset(b.p, 0, alloc));
+    b.bytes = alloc;
+}
+
+void release(Buf& b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+template <typename T>
+T* ptr(const Buf& b) {
+    return static_cast<T*>(b.p);
+}
+
+void check_launch(agsx_ctx* ctx) {
+    ++ctx->launches;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw StatusError{AGSX_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e)};
+}
+
+template <typename F>
+int guarded(agsx_ctx* ctx, F&& f) {
+    try {
+        AGSX_CUDA(cudaSetDevice(ctx->device));
+        const int rc = f();
+        if (rc == AGSX_OK) ctx->err.clear();
+        return rc;
+    } catch (const StatusError& e) {
+        ctx->err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        ctx->err = "host allocation failed";
+        return AGSX_ENOMEM;
+    } catch (...) {
+        ctx->err = "unknown error";
+        return AGSX_ECUDA;
+    }
+}
+
+int fail(agsx_ctx* ctx, int code, const std::string& msg) {
+    ctx->err = msg;
+    return code;
+}
+
+// ---- validation (scene.cpp:41-59, 113-123) ------------------------------
+std::string validate_config(const agsx_config& c) {
+    if (!(c.alpha_threshold > 0.0f && c.alpha_threshold < c.alpha_clamp && c.alpha_clamp <= 1.0f))
+        return "require 0 < alpha_threshold < alpha_clamp <= 1";
+    if (!(c.transmittance_floor > 0.0f)) return "transmittance_floor must be positive";
+    if (c.tile_size < 1) return "tile_size must be >= 1";
+    if (c.k < 0.0f) return "k must be >= 0";
+    if (!(c.near_plane > 0.0f)) return "near_plane must be positive";
+    if (c.mode < AGSX_MODE_AABB || c.mode > AGSX_MODE_ADAGSCALE) return "unknown mode";
+    return {};
+}
+
+std::string validate_camera(const agsx_camera& cam) {
+    // orthonormality_drift: max |R^T R - I| with float Mat3 products
+    const float* r = cam.rotation;
+    float drift = 0.0f;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            float s = 0.0f;
+            for (int k = 0; k < 3; ++k) s += r[k * 3 + i] * r[k * 3 + j];
+            const float target = (i == j) ? 1.0f : 0.0f;
+            drift = smax(drift, std::fabs(s - target));
+        }
+    if (drift > 1e-5f) return "camera rotation is not orthonormal";
+    if (!(cam.fx > 0.0f && cam.fy > 0.0f)) return "focal lengths must be positive";
+    if (!(cam.width > 0 && cam.height > 0)) return "image dimensions must be positive";
+    return {};
+}
+
+int tile_bits(uint32_t tile_count) {
+    int b = 0;
+    while (b < 32 && (tile_count - 1) >> b) ++b;
+    return std::max(b, 1);
+}
+
+FrameParams make_params(const agsx_camera& cam, const agsx_config& cfg, const agsx_lut* lut,
+                        const float* lut_ext_dev) {
+    FrameParams p;
+    std::memset(&p, 0, sizeof(p));
+    for (int i = 0; i < 3; ++i) p.cam_pos[i] = cam.position[i];
+    for (int i = 0; i < 9; ++i) p.R[i] = cam.rotation[i];
+    p.fx = cam.fx;
+    p.fy = cam.fy;
+    p.W = cam.width;
+    p.H = cam.height;
+    p.ppx = 0.5f * static_cast<float>(cam.width);
+    p.ppy = 0.5f * static_cast<float>(cam.height);
+    p.lim_x = cfg.guard_band * 0.5 * cam.width / cam.fx;
+    p.lim_y = cfg.guard_band * 0.5 * cam.height / cam.fy;
+    p.tile_size = cfg.tile_size;
+    p.tiles_x = (cam.width + cfg.tile_size - 1) / cfg.tile_size;
+    p.tiles_y = (cam.height + cfg.tile_size - 1) / cfg.tile_size;
+    p.mode = cfg.mode;
+    p.fixed_aabb = cfg.fixed_radius_aabb ? 1 : 0;
+    p.tau = cfg.alpha_threshold;
+    p.tfloor = cfg.transmittance_floor;
+    p.aclamp = cfg.alpha_clamp;
+    p.near_plane = cfg.near_plane;
+    p.guard = cfg.guard_band;
+    p.k = cfg.k;
+    for (int i = 0; i < 3; ++i) p.bg[i] = cfg.background[i];
+    p.flags = cfg.flags;
+    p.adaptive = cfg.mode == AGSX_MODE_ADAGSCALE ? 1 : 0;
+    p.lut_dmin = 0.0f;
+    p.lut_dmax = 100.0f;
+    p.lut_n = 20;
+    for (int i = 0; i < 20; ++i) p.lut[i] = 1.0f;
+    if (lut && lut->bin_count > 0) {
+        p.lut_dmin = lut->depth_min;
+        p.lut_dmax = lut->depth_max;
+        p.lut_n = lut->bin_count;
+        if (lut->bin_count <= kLutInline) {
+            for (int i = 0; i < lut->bin_count; ++i) p.lut[i] = lut->bins[i];
+        } else {
+            p.lut_ext = lut_ext_dev;
+        }
+    }
+    return p;
+}
+
+int raster_ppt(int tile_size) {
+    if (tile_size <= 16) return 1;
+    if (tile_size <= 32) return 4;
+    return 16;
+}
+
+void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
+                   const float4* P0, const float4* P1, const float4* P2, float* image,
+                   uint32_t* maxt) {
+    const int grid = p.tiles_x * p.tiles_y;
+    if (grid == 0) return;
+    const bool exact = (p.flags & AGSX_FLAG_EXACT_ALPHA) != 0;
+    launch_raster_kernel(raster_ppt(p.tile_size), exact, maxt != nullptr, grid, ctx->stream, p, ranges, vals,
+                         P0, P1, P2, image, maxt);
+    check_launch(ctx);
+}
+
+size_t onesweep_smem(bool k64) {
+    return (k64 ? 8 : 4) * static_cast<size_t>(kSortTile) + 4 * static_cast<size_t>(kSortTile) +
+           (kSortThreads / 32) * 256 * 4;
+}
+
+// One stable onesweep pass; returns nothing, counts launches.
+template <typename K>
+void onesweep_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout,
+                   const uint32_t* n_dev, uint64_t n_host, int shift, const uint32_t* hist,
+                   uint32_t* tile_ctr) {
+    const int occ = sizeof(K) == 8 ? ctx->occ_sort64 : ctx->occ_sort32;
+    int grid = ctx->num_sms * occ;
+    if (!n_dev) {
+        const uint64_t tiles = (n_host + kSortTile - 1) / kSortTile;
+        grid = static_cast<int>(std::min<uint64_t>(grid, std::max<uint64_t>(tiles, 1)));
+    }
+    launch_onesweep<K>(grid, onesweep_smem(sizeof(K) == 8), ctx->stream, kin, vin, kout, vout, n_dev, n_host,
+                       shift, hist, ptr<uint64_t>(ctx->lb), tile_ctr, ctx->epoch++);
+    check_launch(ctx);
+}
+
+void ensure_lb(agsx_ctx* ctx, uint64_t max_elems) {
+    const uint64_t words = std::max<uint64_t>(max_elems / 256 + 2,
+                                              (max_elems / kSortTile + 2) * 256);
+    ensure(ctx->lb, words * sizeof(uint64_t), /*zero=*/true);
+}
+
+// Arena sizing for a scene of n Gaussians and a frame of `tiles` tiles.
+void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pixels, bool obb,
+                          uint64_t pair_budget) {
+    ensure(ctx->status, std::max<uint64_t>(n, 1) * 4);
+    ensure(ctx->p0, std::max<uint64_t>(n, 1) * 16);
+    ensure(ctx->p1, std::max<uint64_t>(n, 1) * 16);
+    ensure(ctx->p2, std::max<uint64_t>(n, 1) * 16);
+    ensure(ctx->p3, std::max<uint64_t>(n, 1) * 16);
+    if (obb) ensure(ctx->p4, std::max<uint64_t>(n, 1) * 16);
+    ensure(ctx->dkeys, std::max<uint64_t>(n, 1) * 4);
+    ensure(ctx->dvals, std::max<uint64_t>(n, 1) * 4);
+    ensure(ctx->dkeys2, std::max<uint64_t>(n, 1) * 4);
+    ensure(ctx->dvals2, std::max<uint64_t>(n, 1) * 4);
+    ensure(ctx->ranges, std::max<uint64_t>(tiles, 1) * 8);
+    ensure(ctx->image, std::max<uint64_t>(pixels, 1) * 12);
+    ensure(ctx->ctr, sizeof(Counters) + 2 * 8 * 256 * 4);
+    if (ctx->pair_capacity == 0) {
+        // first guess: 12 pairs per Gaussian, at most the budget, at least 1M
+        ctx->pair_capacity = std::min<uint64_t>(std::max<uint64_t>(12 * n, 1u << 20),
+                                                std::max<uint64_t>(pair_budget, 1));
+    }
+    const uint64_t cap = ctx->pair_capacity;
+    ensure(ctx->tkeys, cap * 4);
+    ensure(ctx->pvals, cap * 4);
+    ensure(ctx->tkeys2, cap * 4);
+    ensure(ctx->pvals2, cap * 4);
+    ensure_lb(ctx, std::max(cap, n));
+}
+
+SplatPlanes planes_of(agsx_ctx* ctx) {
+    SplatPlanes pl;
+    pl.p0 = ptr<float4>(ctx->p0);
+    pl.p1 = ptr<float4>(ctx->p1);
+    pl.p2 = ptr<float4>(ctx->p2);
+    pl.p3 = ptr<float4>(ctx->p3);
+    pl.p4 = ptr<float4>(ctx->p4);
+    return pl;
+}
+
+// Validates and resolves the LUT; returns AGSX_OK or EINVAL.
+int prepare(agsx_ctx* ctx, const agsx_camera* cam, const agsx_config* cfg, const agsx_lut* lut,
+            FrameParams& p) {
+    if (!cam || !cfg) return fail(ctx, AGSX_EINVAL, "render: null camera or config");
+    std::string bad = validate_config(*cfg);
+    if (!bad.empty()) return fail(ctx, AGSX_EINVAL, "render: " + bad);
+    bad = validate_camera(*cam);
+    if (!bad.empty()) return fail(ctx, AGSX_EINVAL, "render: " + bad);
+    if (cfg->mode == AGSX_MODE_ADAGSCALE && lut == nullptr)
+        return fail(ctx, AGSX_EINVAL, "preprocess_view: adagscale mode requires a T-upper LUT");
+    if (cfg->tile_size > 64)
+        return fail(ctx, AGSX_EINVAL, "tile_size > 64 is not supported by the device rasterizer");
+    const float* lut_dev = nullptr;
+    if (lut && lut->bin_count > kLutInline) {
+        ensure(ctx->lut_ext, lut->bin_count * sizeof(float));
+        AGSX_CUDA(cudaMemcpyAsync(ctx->lut_ext.p, lut->bins, lut->bin_count * sizeof(float),
+                                  cudaMemcpyHostToDevice, ctx->stream));
+        lut_dev = ptr<float>(ctx->lut_ext);
+    }
+    p = make_params(*cam, *cfg, cfg->mode == AGSX_MODE_ADAGSCALE ? lut : nullptr, lut_dev);
+    return AGSX_OK;
+}
+
+// Enqueue the whole frame (no host synchronisation).
+void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bool maxt,
+                   agsx_splat_view* dump) {
+    const uint64_t n = sc->n;
+    const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
+    Counters* ctr = ptr<Counters>(ctx->ctr);
+    uint32_t* hist_depth = reinterpret_cast<uint32_t*>(ctr + 1);
+    uint32_t* hist_tile = hist_depth + 8 * 256;
+    cudaStream_t st = ctx->stream;
+
+    AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
+    AGSX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters) + 2 * 8 * 256 * 4, st));
+    AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
+    if (maxt) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, n * 4, st));
+    const SplatPlanes pl = planes_of(ctx);
+    if (n > 0) {
+        const int grid = static_cast<int>((n + 255) / 256);
+        k_preprocess<<<grid, 256, 0, st>>>(p, sc->view(), pl, ptr<uint32_t>(ctx->status),
+                                            ptr<uint32_t>(ctx->dkeys), ptr<uint32_t>(ctx->dvals),
+                                            ptr<uint64_t>(ctx->lb), ctr, ctx->epoch++, dump);
+        check_launch(ctx);
+    }
+    AGSX_CUDA(cudaEventRecord(ctx->ev[1], st));
+    // K4a: stable sort of the splats with tiles by depth bits (4 x 8-bit)
+    uint32_t* dk[2] = {ptr<uint32_t>(ctx->dkeys), ptr<uint32_t>(ctx->dkeys2)};
+    uint32_t* dv[2] = {ptr<uint32_t>(ctx->dvals), ptr<uint32_t>(ctx->dvals2)};
+    if (n > 0) {
+        const int hgrid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->num_sms * 4));
+        launch_hist<uint32_t>(hgrid, st, dk[0], &ctr->m, 0, 0, 4, hist_depth);
+        check_launch(ctx);
+        for (int ps = 0; ps < 4; ++ps) {
+            onesweep_pass<uint32_t>(ctx, dk[ps & 1], dv[ps & 1], dk[(ps + 1) & 1], dv[(ps + 1) & 1],
+                                    &ctr->m, 0, 8 * ps, hist_depth + 256 * ps, &ctr->tile_ctr[2 + ps]);
+        }
+    }
+    AGSX_CUDA(cudaEventRecord(ctx->ev[2], st));
+    // K3: scan + emit in depth order
+    uint32_t* tk[2] = {ptr<uint32_t>(ctx->tkeys), ptr<uint32_t>(ctx->tkeys2)};
+    uint32_t* pv[2] = {ptr<uint32_t>(ctx->pvals), ptr<uint32_t>(ctx->pvals2)};
+    if (n > 0) {
+        k_emit<<<ctx->num_sms * ctx->occ_emit, 256, 0, st>>>(p, dv[0], ptr<uint32_t>(ctx->status), pl,
+                                                            tk[0], pv[0], ctx->pair_capacity,
+                                                            ptr<uint64_t>(ctx->lb), ctr, ctx->epoch++);
+        check_launch(ctx);
+    }
+    AGSX_CUDA(cudaEventRecord(ctx->ev[3], st));
+    // K4b: stable sort of the pairs by tile id, then K5 ranges
+    const int passes = (tile_bits(static_cast<uint32_t>(tiles)) + 7) / 8;
+    int cur = 0;
+    if (n > 0) {
+        launch_hist<uint32_t>(ctx->num_sms * 4, st, tk[0], &ctr->p_eff, 0, 0, passes, hist_tile);
+        check_launch(ctx);
+        for (int ps = 0; ps < passes; ++ps) {
+            onesweep_pass<uint32_t>(ctx, tk[cur], pv[cur], tk[cur ^ 1], pv[cur ^ 1], &ctr->p_eff, 0,
+                                    8 * ps, hist_tile + 256 * ps, &ctr->tile_ctr[6 + ps]);
+            cur ^= 1;
+        }
+        k_ranges_u32<<<ctx->num_sms * 4, 256, 0, st>>>(tk[cur], &ctr->p_eff, ptr<uint2>(ctx->ranges));
+        check_launch(ctx);
+    }
+    AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
+    // K6
+    launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ptr<float>(ctx->image),
+                  maxt ? ptr<uint32_t>(ctx->maxt) : nullptr);
+    AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
+    AGSX_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    ctx->f_tkeys = tk[cur];
+    ctx->f_pvals = pv[cur];
+    ctx->f_tile_count = static_cast<int>(tiles);
+}
+
+int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, const agsx_config* cfg,
+                const agsx_lut* lut, bool maxt) {
+    if (!sc) return fail(ctx, AGSX_EINVAL, "render: null scene");
+    if (sc->device != ctx->device) return fail(ctx, AGSX_EINVAL, "scene lives on another device");
+    FrameParams p;
+    const int rc = prepare(ctx, cam, cfg, lut, p);
+    if (rc) return rc;
+    const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
+    ensure_frame_buffers(ctx, sc->n, tiles, static_cast<uint64_t>(cam->width) * cam->height,
+                         cfg->mode == AGSX_MODE_OBB, cfg->pair_budget);
+    if (maxt) ensure(ctx->maxt, std::max<uint64_t>(sc->n, 1) * 4);
+    ctx->have_frame = true;
+    ctx->f_scene = sc;
+    ctx->f_cam = *cam;
+    ctx->f_cfg = *cfg;
+    ctx->f_has_lut = lut != nullptr;
+    if (lut && lut->bin_count > 0) {
+        ctx->f_lut.assign(lut->bins, lut->bins + lut->bin_count);
+        ctx->f_lut_dmin = lut->depth_min;
+        ctx->f_lut_dmax = lut->depth_max;
+    } else {
+        ctx->f_lut.clear();
+    }
+    ctx->f_params = p;
+    ctx->f_maxt = maxt;
+    enqueue_frame(ctx, sc, p, maxt, nullptr);
+    return AGSX_OK;
+}
+
+// Wait for the enqueued frame; grow the pair arena and re-run on overflow.
+int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
+    if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame in flight");
+    for (int attempt = 0; attempt < 4; ++attempt) {
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        const Counters c = *ctx->h_ctr;
+        const uint64_t pairs = c.p == 0xffffffffu ? UINT64_MAX : c.p;
+        if (pairs > ctx->f_cfg.pair_budget) {
+            return fail(ctx, AGSX_EPAIR_BUDGET,
+                        "pair count " + (pairs == UINT64_MAX ? std::string(">= 2^32") : std::to_string(pairs)) +
+                            " exceeds budget " + std::to_string(ctx->f_cfg.pair_budget));
+        }
+        if (c.overflow || c.p_eff != c.p) {
+            if (pairs >= (1ull << 31)) return fail(ctx, AGSX_ENOMEM, "pair count exceeds 2^31");
+            ctx->pair_capacity = std::min<uint64_t>(pairs + pairs / 8 + 1024, ctx->f_cfg.pair_budget);
+            const uint64_t tiles = static_cast<uint64_t>(ctx->f_params.tiles_x) * ctx->f_params.tiles_y;
+            ensure_frame_buffers(ctx, ctx->f_scene->n, tiles,
+                                 static_cast<uint64_t>(ctx->f_cam.width) * ctx->f_cam.height,
+                                 ctx->f_cfg.mode == AGSX_MODE_OBB, ctx->f_cfg.pair_budget);
+            enqueue_frame(ctx, ctx->f_scene, ctx->f_params, ctx->f_maxt, nullptr);
+            continue;
+        }
+        if (out) {
+            out->pair_count = c.p;
+            out->splat_count = c.s;
+            float ms[5];
+            for (int i = 0; i < 5; ++i) AGSX_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[i], ctx->ev[i + 1]));
+            out->stage_ms[0] = ms[0];
+            out->stage_ms[1] = ms[2];
+            out->stage_ms[2] = ms[1] + ms[3];
+            out->stage_ms[3] = ms[4];
+        }
+        return AGSX_OK;
+    }
+    return fail(ctx, AGSX_ECUDA, "pair arena did not converge");
+}
+
+}  // namespace
+
+extern "C" {
+
+int agsx_abi_version(void) { return AGSX_ABI_VERSION; }
+
+int agsx_create(int device, agsx_ctx** out) {
+    if (!out) return AGSX_EINVAL;
+    *out = nullptr;
+    agsx_ctx* ctx = new (std::nothrow) agsx_ctx();
+    if (!ctx) return AGSX_ENOMEM;
+    ctx->device = device;
+    const int rc = guarded(ctx, [&]() -> int {
+        AGSX_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        AGSX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+        AGSX_CUDA(onesweep_configure<uint32_t>(onesweep_smem(false), &ctx->occ_sort32));
+        AGSX_CUDA(onesweep_configure<uint64_t>(onesweep_smem(true), &ctx->occ_sort64));
+        AGSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ_emit, k_emit, 256, 0));
+        ctx->occ_sort32 = std::max(ctx->occ_sort32, 1);
+        ctx->occ_sort64 = std::max(ctx->occ_sort64, 1);
+        ctx->occ_emit = std::max(ctx->occ_emit, 1);
+        for (auto& e : ctx->ev) AGSX_CUDA(cudaEventCreate(&e));
+        AGSX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ctr), sizeof(Counters)));
+        std::memset(ctx->h_ctr, 0, sizeof(Counters));
+        return AGSX_OK;
+    });
+    if (rc != AGSX_OK) {
+        std::fprintf(stderr, "agsx_create: %s\n", ctx->err.c_str());
+        agsx_destroy(ctx);
+        return rc;
+    }
+    *out = ctx;
+    return AGSX_OK;
+}
+
+void agsx_destroy(agsx_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (Buf* b : {&ctx->status, &ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4, &ctx->dkeys,
+                   &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
+                   &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
+                   &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
+                   &ctx->tmp3, &ctx->tmp4})
+        release(*b);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+const char* agsx_last_error(const agsx_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void* agsx_stream(agsx_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+uint64_t agsx_kernel_launches(const agsx_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int agsx_scene_upload(agsx_ctx* ctx, const agsx_scene_desc* d, agsx_scene** out) {
+    if (!ctx || !d || !out) return AGSX_EINVAL;
+    *out = nullptr;
+    const int D = d->sh_coeffs;
+    if (!(D == 1 || D == 4 || D == 9 || D == 16))
+        return fail(ctx, AGSX_EINVAL, "sh coefficient count must be 3*d^2 for d in {1,2,3,4}");
+    agsx_scene* sc = new (std::nothrow) agsx_scene();
+    if (!sc) return AGSX_ENOMEM;
+    const int rc = guarded(ctx, [&]() -> int {
+        sc->device = ctx->device;
+        sc->n = d->count;
+        sc->D = D;
+        const uint64_t n = d->count;
+        ensure(sc->pos_op, std::max<uint64_t>(n, 1) * 16);
+        ensure(sc->rot, std::max<uint64_t>(n, 1) * 16);
+        ensure(sc->scale_r, std::max<uint64_t>(n, 1) * 16);
+        ensure(sc->sh_gb, std::max<uint64_t>(n, 1) * 8);
+        ensure(sc->sh_rest, std::max<uint64_t>(n * (3 * D - 3), 1) * 4);
+        if (n == 0) return AGSX_OK;
+        // stage the host SoA arrays, pack on the device in slices
+        const uint64_t slice = 1u << 22;
+        const uint64_t fl_per = 3 + 3 + 4 + 1 + 3 * static_cast<uint64_t>(D);
+        Buf stage;
+        ensure(stage, std::min(n, slice) * fl_per * 4);
+        float* s = ptr<float>(stage);
+        for (uint64_t b = 0; b < n; b += slice) {
+            const uint64_t m = std::min(slice, n - b);
+            float* sm = s;
+            float* ss = sm + 3 * m;
+            float* sq = ss + 3 * m;
+            float* so = sq + 4 * m;
+            float* sh = so + m;
+            AGSX_CUDA(cudaMemcpyAsync(sm, d->mean + 3 * b, 12 * m, cudaMemcpyHostToDevice, ctx->stream));
+            AGSX_CUDA(cudaMemcpyAsync(ss, d->scale + 3 * b, 12 * m, cudaMemcpyHostToDevice, ctx->stream));
+            AGSX_CUDA(cudaMemcpyAsync(sq, d->rotation + 4 * b, 16 * m, cudaMemcpyHostToDevice, ctx->stream));
+            AGSX_CUDA(cudaMemcpyAsync(so, d->opacity + b, 4 * m, cudaMemcpyHostToDevice, ctx->stream));
+            AGSX_CUDA(cudaMemcpyAsync(sh, d->sh + 3 * D * b, 12 * D * m, cudaMemcpyHostToDevice, ctx->stream));
+            k_pack_scene<<<static_cast<int>((m + 255) / 256), 256, 0, ctx->stream>>>(
+                m, D, sm, ss, sq, so, sh, ptr<float4>(sc->pos_op) + b, ptr<float4>(sc->rot) + b,
+                ptr<float4>(sc->scale_r) + b, ptr<float2>(sc->sh_gb) + b,
+                ptr<float>(sc->sh_rest) + b * (3 * D - 3));
+            check_launch(ctx);
+        }
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        release(stage);
+        return AGSX_OK;
+    });
+    if (rc != AGSX_OK) {
+        agsx_scene_free(sc);
+        return rc;
+    }
+    *out = sc;
+    return AGSX_OK;
+}
+
+void agsx_scene_free(agsx_scene* sc) {
+    if (!sc) return;
+    cudaSetDevice(sc->device);
+    for (Buf* b : {&sc->pos_op, &sc->rot, &sc->scale_r, &sc->sh_gb, &sc->sh_rest}) release(*b);
+    delete sc;
+}
+
+uint64_t agsx_scene_count(const agsx_scene* sc) { return sc ? sc->n : 0; }
+
+int agsx_render_async(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                      const agsx_config* cfg, const agsx_lut* lut) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int { return start_frame(ctx, scene, cam, cfg, lut, false); });
+}
+
+int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int { return finish_frame(ctx, out); });
+}
+
+int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                const agsx_config* cfg, const agsx_lut* lut, agsx_frame* out) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        const bool maxt = out && out->max_t;
+        int rc = start_frame(ctx, scene, cam, cfg, lut, maxt);
+        if (rc) return rc;
+        rc = finish_frame(ctx, out);
+        if (rc) return rc;
+        if (out && out->image) {
+            AGSX_CUDA(cudaMemcpyAsync(out->image, ctx->image.p,
+                                      static_cast<size_t>(cam->width) * cam->height * 12,
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        if (maxt && scene->n) {
+            AGSX_CUDA(cudaMemcpyAsync(out->max_t, ctx->maxt.p, scene->n * 4, cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+        }
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return AGSX_OK;
+    });
+}
+
+int agsx_device_image(agsx_ctx* ctx, float** dptr, int32_t* width, int32_t* height) {
+    if (!ctx || !dptr) return AGSX_EINVAL;
+    if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame rendered yet");
+    *dptr = ptr<float>(ctx->image);
+    if (width) *width = ctx->f_cam.width;
+    if (height) *height = ctx->f_cam.height;
+    return AGSX_OK;
+}
+
+int agsx_dump_tile_counts(agsx_ctx* ctx, uint32_t* counts, uint8_t* alive, uint64_t n) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame rendered yet");
+        if (n != ctx->f_scene->n) return fail(ctx, AGSX_EINVAL, "count mismatch");
+        std::vector<uint32_t> st(n);
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (n) AGSX_CUDA(cudaMemcpy(st.data(), ctx->status.p, n * 4, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < n; ++i) {
+            if (counts) counts[i] = st[i] & kCountMask;
+            if (alive) alive[i] = (st[i] & kAliveBit) ? 1 : 0;
+        }
+        return AGSX_OK;
+    });
+}
+
+int agsx_dump_sorted_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* gids, uint64_t capacity,
+                           uint64_t* out_count) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame rendered yet");
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        const Counters c = *ctx->h_ctr;
+        const uint64_t P = c.p_eff;
+        if (out_count) *out_count = P;
+        if (P > capacity) return fail(ctx, AGSX_ECAPACITY, "buffer too small");
+        const uint64_t n = ctx->f_scene->n;
+        std::vector<uint32_t> dk(c.m), dv(c.m), tk(P), pv(P);
+        if (c.m) {
+            AGSX_CUDA(cudaMemcpy(dk.data(), ctx->dkeys.p, c.m * 4, cudaMemcpyDeviceToHost));
+            AGSX_CUDA(cudaMemcpy(dv.data(), ctx->dvals.p, c.m * 4, cudaMemcpyDeviceToHost));
+        }
+        if (P) {
+            AGSX_CUDA(cudaMemcpy(tk.data(), ctx->f_tkeys, P * 4, cudaMemcpyDeviceToHost));
+            AGSX_CUDA(cudaMemcpy(pv.data(), ctx->f_pvals, P * 4, cudaMemcpyDeviceToHost));
+        }
+        std::vector<uint32_t> depth_by_gid(n, 0);
+        for (uint32_t j = 0; j < c.m; ++j) depth_by_gid[dv[j]] = dk[j];
+        for (uint64_t i = 0; i < P; ++i) {
+            if (keys) keys[i] = (static_cast<uint64_t>(tk[i]) << 32) | depth_by_gid[pv[i]];
+            if (gids) gids[i] = pv[i];
+        }
+        return AGSX_OK;
+    });
+}
+
+int agsx_dump_ranges(agsx_ctx* ctx, uint32_t* ranges, uint64_t tile_count) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame rendered yet");
+        if (tile_count != static_cast<uint64_t>(ctx->f_tile_count))
+            return fail(ctx, AGSX_EINVAL, "tile count mismatch");
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (tile_count)
+            AGSX_CUDA(cudaMemcpy(ranges, ctx->ranges.p, tile_count * 8, cudaMemcpyDeviceToHost));
+        return AGSX_OK;
+    });
+}
+
+int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                         const agsx_config* cfg, const agsx_lut* lut, agsx_splat_view* out,
+                         uint64_t* out_count) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!scene) return fail(ctx, AGSX_EINVAL, "null scene");
+        // preprocess_view validates only the LUT requirement (preprocess.cpp:121-125)
+        if (cfg->mode == AGSX_MODE_ADAGSCALE && lut == nullptr)
+            return fail(ctx, AGSX_EINVAL, "preprocess_view: adagscale mode requires a T-upper LUT");
+        agsx_config c = *cfg;
+        if (c.tile_size < 1) c.tile_size = 16;
+        FrameParams p;
+        const float* lut_dev = nullptr;
+        if (lut && lut->bin_count > kLutInline) {
+            ensure(ctx->lut_ext, lut->bin_count * sizeof(float));
+            AGSX_CUDA(cudaMemcpy(ctx->lut_ext.p, lut->bins, lut->bin_count * 4, cudaMemcpyHostToDevice));
+            lut_dev = ptr<float>(ctx->lut_ext);
+        }
+        p = make_params(*cam, c, c.mode == AGSX_MODE_ADAGSCALE ? lut : nullptr, lut_dev);
+        const uint64_t n = scene->n;
+        const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
+        ensure_frame_buffers(ctx, n, tiles, static_cast<uint64_t>(cam->width) * cam->height,
+                             c.mode == AGSX_MODE_OBB, c.pair_budget);
+        ensure(ctx->dump, std::max<uint64_t>(n, 1) * sizeof(agsx_splat_view));
+        Counters* ctr = ptr<Counters>(ctx->ctr);
+        AGSX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), ctx->stream));
+        if (n) {
+            k_preprocess<<<static_cast<int>((n + 255) / 256), 256, 0, ctx->stream>>>(
+                p, scene->view(), planes_of(ctx), ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys),
+                ptr<uint32_t>(ctx->dvals), ptr<uint64_t>(ctx->lb), ctr, ctx->epoch++,
+                ptr<agsx_splat_view>(ctx->dump));
+            check_launch(ctx);
+        }
+        std::vector<uint32_t> st(n);
+        std::vector<agsx_splat_view> sv(n);
+        if (n) {
+            AGSX_CUDA(cudaMemcpyAsync(st.data(), ctx->status.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+            AGSX_CUDA(cudaMemcpyAsync(sv.data(), ctx->dump.p, n * sizeof(agsx_splat_view),
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        uint64_t m = 0;
+        for (uint64_t i = 0; i < n; ++i)
+            if (st[i] & kAliveBit) out[m++] = sv[i];
+        *out_count = m;
+        ctx->have_frame = false;
+        return AGSX_OK;
+    });
+}
+
+int agsx_generate_pairs(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n, int32_t width,
+                        int32_t height, int32_t mode, const agsx_config* cfg, uint64_t* keys,
+                        uint32_t* splat_index, uint64_t capacity, uint32_t* tile_counts,
+                        uint64_t* out_total) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (cfg->tile_size < 1) return fail(ctx, AGSX_EINVAL, "tile_size must be >= 1");
+        agsx_config c = *cfg;
+        c.mode = mode;
+        agsx_camera cam{};
+        cam.width = width;
+        cam.height = height;
+        cam.fx = cam.fy = 1.0f;
+        const FrameParams p = make_params(cam, c, nullptr, nullptr);
+        ensure(ctx->tmp0, std::max<uint64_t>(n, 1) * sizeof(agsx_splat_view));
+        ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 4);  // counts
+        ensure(ctx->tmp2, std::max<uint64_t>(n, 1) * 4);  // depth bits
+        ensure(ctx->tmp3, std::max<uint64_t>(n, 1) * 8);  // offsets
+        for (Buf* b : {&ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4})
+            ensure(*b, std::max<uint64_t>(n, 1) * 16);
+        const SplatPlanes pl = planes_of(ctx);
+        if (n) {
+            AGSX_CUDA(cudaMemcpyAsync(ctx->tmp0.p, splats, n * sizeof(agsx_splat_view),
+                                      cudaMemcpyHostToDevice, ctx->stream));
+            k_splats_to_planes<<<static_cast<int>((n + 255) / 256), 256, 0, ctx->stream>>>(
+                p, ptr<agsx_splat_view>(ctx->tmp0), n, pl, ptr<uint32_t>(ctx->tmp1), ptr<uint32_t>(ctx->tmp2));
+            check_launch(ctx);
+        }
+        std::vector<uint32_t> cnt(n);
+        if (n) AGSX_CUDA(cudaMemcpyAsync(cnt.data(), ctx->tmp1.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::vector<uint64_t> off(n);
+        uint64_t total = 0;
+        for (uint64_t i = 0; i < n; ++i) {
+            off[i] = total;
+            total += cnt[i];
+            if (tile_counts) tile_counts[i] = cnt[i];
+        }
+        *out_total = total;
+        if (total > cfg->pair_budget)
+            return fail(ctx, AGSX_EPAIR_BUDGET, "pair count " + std::to_string(total) + " exceeds budget " +
+                                                    std::to_string(cfg->pair_budget));
+        if (total > capacity) return fail(ctx, AGSX_ECAPACITY, "output buffers too small");
+        if (total == 0) return AGSX_OK;
+        ensure(ctx->tmp4, total * 8);
+        ensure(ctx->pvals, total * 4);
+        AGSX_CUDA(cudaMemcpyAsync(ctx->tmp3.p, off.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream));
+        k_emit_list<<<static_cast<int>((n + 255) / 256), 256, 0, ctx->stream>>>(
+            p, n, pl, ptr<uint32_t>(ctx->tmp1), ptr<uint64_t>(ctx->tmp3), ptr<uint32_t>(ctx->tmp2),
+            ptr<uint64_t>(ctx->tmp4), ptr<uint32_t>(ctx->pvals));
+        check_launch(ctx);
+        AGSX_CUDA(cudaMemcpyAsync(keys, ctx->tmp4.p, total * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaMemcpyAsync(splat_index, ctx->pvals.p, total * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        ctx->have_frame = false;
+        return AGSX_OK;
+    });
+}
+
+int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64_t n,
+                    int32_t tile_count, uint32_t* ranges) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (tile_count < 0) return fail(ctx, AGSX_EINVAL, "negative tile count");
+        if (n >= (1ull << 32)) return fail(ctx, AGSX_EINVAL, "too many pairs");
+        ensure(ctx->tmp0, std::max<uint64_t>(n, 1) * 8);
+        ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 8);
+        ensure(ctx->tmp2, std::max<uint64_t>(n, 1) * 4);
+        ensure(ctx->tmp3, std::max<uint64_t>(n, 1) * 4);
+        ensure(ctx->hist, 8 * 256 * 4 + sizeof(Counters));
+        ensure(ctx->ranges, std::max<int>(tile_count, 1) * 8);
+        ensure_lb(ctx, n);
+        uint32_t* hist = ptr<uint32_t>(ctx->hist);
+        Counters* ctr = reinterpret_cast<Counters*>(hist + 8 * 256);
+        cudaStream_t st = ctx->stream;
+        AGSX_CUDA(cudaMemsetAsync(ctx->hist.p, 0, 8 * 256 * 4 + sizeof(Counters), st));
+        if (tile_count) AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, static_cast<size_t>(tile_count) * 8, st));
+        uint64_t* k[2] = {ptr<uint64_t>(ctx->tmp0), ptr<uint64_t>(ctx->tmp1)};
+        uint32_t* v[2] = {ptr<uint32_t>(ctx->tmp2), ptr<uint32_t>(ctx->tmp3)};
+        int cur = 0;
+        if (n) {
+            AGSX_CUDA(cudaMemcpyAsync(k[0], keys, n * 8, cudaMemcpyHostToDevice, st));
+            AGSX_CUDA(cudaMemcpyAsync(v[0], splat_index, n * 4, cudaMemcpyHostToDevice, st));
+            const int hgrid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->num_sms * 4));
+            launch_hist<uint64_t>(hgrid, st, k[0], nullptr, n, 0, 8, hist);
+            check_launch(ctx);
+            std::vector<uint32_t> h(8 * 256);
+            AGSX_CUDA(cudaMemcpyAsync(h.data(), hist, h.size() * 4, cudaMemcpyDeviceToHost, st));
+            AGSX_CUDA(cudaStreamSynchronize(st));
+            for (int ps = 0; ps < 8; ++ps) {
+                // a digit shared by every key permutes nothing in a stable pass
+                bool trivial = false;
+                for (int d = 0; d < 256; ++d) trivial = trivial || h[ps * 256 + d] == n;
+                if (trivial) continue;
+                onesweep_pass<uint64_t>(ctx, k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], nullptr, n, 8 * ps,
+                                        hist + 256 * ps, &ctr->tile_ctr[ps]);
+                cur ^= 1;
+            }
+            if (tile_count) {
+                k_ranges_u64<<<ctx->num_sms * 4, 256, 0, st>>>(k[cur], n, static_cast<uint32_t>(tile_count),
+                                                                ptr<uint2>(ctx->ranges));
+                check_launch(ctx);
+            }
+            AGSX_CUDA(cudaMemcpyAsync(keys, k[cur], n * 8, cudaMemcpyDeviceToHost, st));
+            AGSX_CUDA(cudaMemcpyAsync(splat_index, v[cur], n * 4, cudaMemcpyDeviceToHost, st));
+        }
+        if (tile_count)
+            AGSX_CUDA(cudaMemcpyAsync(ranges, ctx->ranges.p, static_cast<size_t>(tile_count) * 8,
+                                      cudaMemcpyDeviceToHost, st));
+        AGSX_CUDA(cudaStreamSynchronize(st));
+        ctx->have_frame = false;
+        return AGSX_OK;
+    });
+}
+
+int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
+                const uint32_t* splat_index, uint64_t n_pairs, const uint32_t* ranges, int32_t width,
+                int32_t height, const agsx_config* cfg, float* image, float* max_t) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (cfg->tile_size < 1 || cfg->tile_size > 64)
+            return fail(ctx, AGSX_EINVAL, "tile_size must be in [1, 64]");
+        if (width <= 0 || height <= 0) return fail(ctx, AGSX_EINVAL, "image dimensions must be positive");
+        agsx_camera cam{};
+        cam.width = width;
+        cam.height = height;
+        cam.fx = cam.fy = 1.0f;
+        const FrameParams p = make_params(cam, *cfg, nullptr, nullptr);
+        const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
+        ensure(ctx->tmp0, std::max<uint64_t>(n_splats, 1) * sizeof(agsx_splat_view));
+        ensure(ctx->tmp1, std::max<uint64_t>(n_splats, 1) * 4);
+        ensure(ctx->tmp2, std::max<uint64_t>(n_splats, 1) * 4);
+        ensure(ctx->tmp3, std::max<uint64_t>(n_pairs, 1) * 4);
+        ensure(ctx->tmp4, std::max<uint64_t>(tiles, 1) * 8);
+        ensure(ctx->image, static_cast<uint64_t>(width) * height * 12);
+        ensure(ctx->maxt, std::max<uint64_t>(n_splats, 1) * 4);
+        for (Buf* b : {&ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4})
+            ensure(*b, std::max<uint64_t>(n_splats, 1) * 16);
+        const SplatPlanes pl = planes_of(ctx);
+        cudaStream_t st = ctx->stream;
+        if (n_splats) {
+            AGSX_CUDA(cudaMemcpyAsync(ctx->tmp0.p, splats, n_splats * sizeof(agsx_splat_view),
+                                      cudaMemcpyHostToDevice, st));
+            k_splats_to_planes<<<static_cast<int>((n_splats + 255) / 256), 256, 0, st>>>(
+                p, ptr<agsx_splat_view>(ctx->tmp0), n_splats, pl, ptr<uint32_t>(ctx->tmp1),
+                ptr<uint32_t>(ctx->tmp2));
+            check_launch(ctx);
+        }
+        if (n_pairs)
+            AGSX_CUDA(cudaMemcpyAsync(ctx->tmp3.p, splat_index, n_pairs * 4, cudaMemcpyHostToDevice, st));
+        AGSX_CUDA(cudaMemcpyAsync(ctx->tmp4.p, ranges, tiles * 8, cudaMemcpyHostToDevice, st));
+        if (max_t) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, std::max<uint64_t>(n_splats, 1) * 4, st));
+        launch_raster(ctx, p, ptr<uint2>(ctx->tmp4), ptr<uint32_t>(ctx->tmp3), pl.p0, pl.p1, pl.p2,
+                      ptr<float>(ctx->image), max_t ? ptr<uint32_t>(ctx->maxt) : nullptr);
+        AGSX_CUDA(cudaMemcpyAsync(image, ctx->image.p, static_cast<size_t>(width) * height * 12,
+                                  cudaMemcpyDeviceToHost, st));
+        if (max_t && n_splats)
+            AGSX_CUDA(cudaMemcpyAsync(max_t, ctx->maxt.p, n_splats * 4, cudaMemcpyDeviceToHost, st));
+        AGSX_CUDA(cudaStreamSynchronize(st));
+        ctx->have_frame = false;
+        return AGSX_OK;
+    });
+}
+
+int agsx_device_logf(agsx_ctx* ctx, const float* x, float* y, uint64_t n) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        ensure(ctx->tmp0, std::max<uint64_t>(n, 1) * 4);
+        ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 4);
+        if (!n) return AGSX_OK;
+        AGSX_CUDA(cudaMemcpyAsync(ctx->tmp0.p, x, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+        k_logf<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ptr<float>(ctx->tmp0), ptr<float>(ctx->tmp1), n);
+        check_launch(ctx);
+        AGSX_CUDA(cudaMemcpyAsync(y, ctx->tmp1.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return AGSX_OK;
+    });
+}
+
+int agsx_device_expf(agsx_ctx* ctx, const float* x, float* y, uint64_t n) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        ensure(ctx->tmp0, std::max<uint64_t>(n, 1) * 4);
+        ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 4);
+        if (!n) return AGSX_OK;
+        AGSX_CUDA(cudaMemcpyAsync(ctx->tmp0.p, x, n * 4, cudaMemcpyHostToDevice, ctx->stream));
+        k_expf<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(ptr<float>(ctx->tmp0), ptr<float>(ctx->tmp1), n);
+        check_launch(ctx);
+        AGSX_CUDA(cudaMemcpyAsync(y, ctx->tmp1.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return AGSX_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,350 @@
+// agsx_internal.cuh -- device data layout and shared device functions of the
+// B200 render path.  See DESIGN.md §3 for the HBM layout.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/agsx.h"
+#include "device_math.cuh"
+
+namespace agsx {
+
+constexpr int kLutInline = 64;
+constexpr uint32_t kAliveBit = 0x80000000u;
+constexpr uint32_t kCountMask = 0x7fffffffu;
+
+// Everything a frame's kernels need, passed by value (kernel parameter
+// space), so a frame needs no host->device copies besides this launch state.
+struct FrameParams {
+    // camera (scene.hpp:34-49)
+    float cam_pos[3];
+    float R[9];
+    float fx, fy;
+    int W, H;
+    float ppx, ppy;       // principal_point(): 0.5f * (float)W, 0.5f * (float)H
+    double lim_x, lim_y;  // guard_band * 0.5 * W / fx (preprocess.cpp:45-46), host-evaluated
+    // config (scene.hpp:65-78)
+    int tile_size, tiles_x, tiles_y;
+    int mode;
+    int fixed_aabb;
+    float tau, tfloor, aclamp, near_plane, guard, k;
+    float bg[3];
+    uint32_t flags;
+    // T_upper LUT (lut.hpp:11-26)
+    int adaptive;
+    float lut_dmin, lut_dmax;
+    int lut_n;
+    float lut[kLutInline];
+    const float* lut_ext;  // device copy when lut_n > kLutInline
+};
+
+// Device-resident scene (uploaded once; 56 B per Gaussian for SH degree 0).
+struct DevScene {
+    uint64_t n;
+    int sh_coeffs;  // D per channel
+    const float4* pos_op;   // mean.xyz, opacity
+    const float4* rot;      // w, x, y, z
+    const float4* scale_r;  // scale.xyz, sh[0] (red DC)
+    const float2* sh_gb;    // sh[1], sh[2] (green/blue DC)
+    const float* sh_rest;   // (D-1)*3 floats per Gaussian, coefficient-major
+};
+
+// Per-splat planes written by preprocess for splats that hit >= 1 tile,
+// indexed by Gaussian id (value of every pair).
+//   P0 = {mean.x, mean.y, inv.xx, inv.xy}            raster + emit
+//   P1 = {inv.yy, opacity, pcut, bbox_x (2 x int16)} raster + emit(inv.yy)
+//   P2 = {r, g, b, bbox_y (2 x int16)}               raster
+//   P3 = {rx, ry, r2, r}                             emit (tile test)
+//   P4 = {v1.x, v1.y, a, b}                          emit, OBB mode only
+struct SplatPlanes {
+    float4* p0;
+    float4* p1;
+    float4* p2;
+    float4* p3;
+    float4* p4;
+};
+
+// ---- tile intersection (pair_gen.cpp:11-159) ---------------------------
+struct TileTest {
+    float cx, cy;
+    float rx, ry;    // half extents of the candidate box (r_px for AABB/OBB)
+    float ixx, ixy, iyy, r2;  // ellipse / adagscale
+    float v1x, v1y, a, b;     // obb
+    int mode;
+};
+
+struct Span {
+    int tx0, ty0, tx1, ty1;
+    bool empty;
+};
+
+// eigen_sym2 (math.hpp:105-131); only l1, l2, v1 are consumed.
+__host__ __device__ __forceinline__ void eigen_sym2(float xx, float xy, float yy, float& l1,
+                                                     float& l2, float& v1x, float& v1y) {
+    const float mean = 0.5f * (xx + yy);
+    const float hd = 0.5f * (xx - yy);
+    const float r = sqrtf(hd * hd + xy * xy);
+    l1 = mean + r;
+    l2 = mean - r;
+    if (xy == 0.0f) {
+        if (xx >= yy) {
+            v1x = 1.0f;
+            v1y = 0.0f;
+        } else {
+            v1x = 0.0f;
+            v1y = 1.0f;
+        }
+        return;
+    }
+    const float ax = l1 - yy, ay = xy;
+    const float bx = xy, by = l1 - xx;
+    const bool pick_a = (ax * ax + ay * ay) >= (bx * bx + by * by);
+    const float vx = pick_a ? ax : bx, vy = pick_a ? ay : by;
+    const float n = sqrtf(vx * vx + vy * vy);
+    v1x = vx / n;
+    v1y = vy / n;
+}
+
+// Builds the mode-specific tile test of intersect_tiles (pair_gen.cpp:108-116,
+// 145-147).  th is the splat's threshold in AdaGScale mode, tau otherwise.
+__device__ __forceinline__ TileTest make_tile_test(float cx, float cy, float cxx, float cxy,
+                                                   float cyy, float ixx, float ixy, float iyy,
+                                                   float opacity, float th, const FrameParams& p) {
+    TileTest t;
+    t.mode = p.mode;
+    t.cx = cx;
+    t.cy = cy;
+    const float th_eff = p.mode == AGSX_MODE_ADAGSCALE ? th : p.tau;
+    float r = sqrtf(2.0f * glibc_logf(opacity / th_eff));
+    if (p.mode == AGSX_MODE_AABB && p.fixed_aabb) r = 3.0f;
+    t.ixx = ixx;
+    t.ixy = ixy;
+    t.iyy = iyy;
+    t.r2 = r * r;
+    t.v1x = t.v1y = t.a = t.b = 0.0f;
+    if (p.mode == AGSX_MODE_AABB || p.mode == AGSX_MODE_OBB) {
+        float l1, l2, v1x, v1y;
+        eigen_sym2(cxx, cxy, cyy, l1, l2, v1x, v1y);
+        const float r_px = r * sqrtf(smax(l1, 0.0f));
+        t.rx = t.ry = r_px;
+        if (p.mode == AGSX_MODE_OBB) {
+            t.v1x = v1x;
+            t.v1y = v1y;
+            t.a = r * sqrtf(smax(l1, 0.0f));
+            t.b = r * sqrtf(smax(l2, 0.0f));
+        }
+    } else {
+        t.rx = r * sqrtf(smax(cxx, 0.0f));
+        t.ry = r * sqrtf(smax(cyy, 0.0f));
+    }
+    return t;
+}
+
+// tile_span (pair_gen.cpp:41-55)
+__device__ __forceinline__ Span tile_span(const TileTest& t, const FrameParams& p) {
+    Span s;
+    const float ts = static_cast<float>(p.tile_size);
+    s.tx0 = imax(0, f2i_x86(floorf((t.cx - t.rx) / ts)));
+    s.ty0 = imax(0, f2i_x86(floorf((t.cy - t.ry) / ts)));
+    s.tx1 = imin(p.tiles_x - 1, f2i_x86(floorf((t.cx + t.rx) / ts)));
+    s.ty1 = imin(p.tiles_y - 1, f2i_x86(floorf((t.cy + t.ry) / ts)));
+    s.empty = s.tx0 > s.tx1 || s.ty0 > s.ty1 || t.cx + t.rx < 0.0f || t.cy + t.ry < 0.0f ||
+              t.cx - t.rx > static_cast<float>(p.W) || t.cy - t.ry > static_cast<float>(p.H);
+    return s;
+}
+
+__device__ __forceinline__ bool box_overlap(float x0, float y0, float x1, float y1, float cx,
+                                            float cy, float rx, float ry) {
+    return x0 <= cx + rx && cx - rx <= x1 && y0 <= cy + ry && cy - ry <= y1;
+}
+
+// SymMat2::quad (math.hpp:91-93): ((xx*dx)*dx + ((2*xy)*dx)*dy) + (yy*dy)*dy
+__host__ __device__ __forceinline__ float quad_form(float xx, float xy, float yy, float dx,
+                                                    float dy) {
+    return xx * dx * dx + 2.0f * xy * dx * dy + yy * dy * dy;
+}
+
+// min_quad_to_rect (pair_gen.cpp:65-83)
+__device__ __forceinline__ float min_quad_to_rect(const TileTest& t, float x0, float y0, float x1,
+                                                  float y1) {
+    const float cx = t.cx, cy = t.cy;
+    if (cx >= x0 && cx <= x1 && cy >= y0 && cy <= y1) return 0.0f;
+    float h0, h1, v0, v1;
+    {
+        const float dy = y0 - cy;
+        const float x = sclamp(cx - t.ixy * dy / t.ixx, x0, x1);
+        h0 = quad_form(t.ixx, t.ixy, t.iyy, x - cx, dy);
+    }
+    {
+        const float dy = y1 - cy;
+        const float x = sclamp(cx - t.ixy * dy / t.ixx, x0, x1);
+        h1 = quad_form(t.ixx, t.ixy, t.iyy, x - cx, dy);
+    }
+    {
+        const float dx = x0 - cx;
+        const float y = sclamp(cy - t.ixy * dx / t.iyy, y0, y1);
+        v0 = quad_form(t.ixx, t.ixy, t.iyy, dx, y - cy);
+    }
+    {
+        const float dx = x1 - cx;
+        const float y = sclamp(cy - t.ixy * dx / t.iyy, y0, y1);
+        v1 = quad_form(t.ixx, t.ixy, t.iyy, dx, y - cy);
+    }
+    return smin(smin(h0, h1), smin(v0, v1));
+}
+
+// obb_overlap (pair_gen.cpp:88-104); u = v1, v = (-v1.y, v1.x).
+__device__ __forceinline__ bool obb_overlap(const TileTest& t, float x0, float y0, float x1,
+                                            float y1) {
+    const float ux = t.v1x, uy = t.v1y, vx = -t.v1y, vy = t.v1x;
+    const float rx = t.a * fabsf(ux) + t.b * fabsf(vx);
+    const float ry = t.a * fabsf(uy) + t.b * fabsf(vy);
+    if (!box_overlap(x0, y0, x1, y1, t.cx, t.cy, rx, ry)) return false;
+    const float tcx = 0.5f * (x0 + x1), tcy = 0.5f * (y0 + y1);
+    const float hw = 0.5f * (x1 - x0);
+    const float hh = 0.5f * (y1 - y0);
+    const float dx = tcx - t.cx, dy = tcy - t.cy;
+    const float tile_u = hw * fabsf(ux) + hh * fabsf(uy);
+    if (fabsf(dx * ux + dy * uy) > t.a + tile_u) return false;
+    const float tile_v = hw * fabsf(vx) + hh * fabsf(vy);
+    if (fabsf(dx * vx + dy * vy) > t.b + tile_v) return false;
+    return true;
+}
+
+// One tile of the candidate span (tile_rect pair_gen.cpp:24-33 + the
+// per-mode test of pair_gen.cpp:118-158).
+__device__ __forceinline__ bool tile_hit(const TileTest& t, int tx, int ty, const FrameParams& p) {
+    const float ts = static_cast<float>(p.tile_size);
+    const float x0 = tx * ts, y0 = ty * ts;
+    const float x1 = smin(x0 + ts, static_cast<float>(p.W));
+    const float y1 = smin(y0 + ts, static_cast<float>(p.H));
+    if (t.mode == AGSX_MODE_AABB) return box_overlap(x0, y0, x1, y1, t.cx, t.cy, t.rx, t.ry);
+    if (t.mode == AGSX_MODE_OBB)
+        return box_overlap(x0, y0, x1, y1, t.cx, t.cy, t.rx, t.ry) &&
+               obb_overlap(t, x0, y0, x1, y1);
+    if (!box_overlap(x0, y0, x1, y1, t.cx, t.cy, t.rx, t.ry)) return false;
+    return min_quad_to_rect(t, x0, y0, x1, y1) <= t.r2;
+}
+
+__device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FrameParams& p) {
+    const Span s = tile_span(t, p);
+    if (s.empty) return 0;
+    uint32_t n = 0;
+    for (int ty = s.ty0; ty <= s.ty1; ++ty)
+        for (int tx = s.tx0; tx <= s.tx1; ++tx) n += tile_hit(t, tx, ty, p) ? 1u : 0u;
+    return n;
+}
+
+// Conservative blend-side culling data for the rasterizer (not part of the
+// reference; it only lets whole warps skip splats whose alpha is provably
+// below tau at every pixel of the warp):
+//   pcut : power < pcut  =>  opacity * expf(power) < tau
+//   bbox : pixel-index box outside of which power < pcut.
+__device__ __forceinline__ void blend_cull_data(float mx, float my, float ixx, float ixy, float iyy, float opacity,
+                                float tau, float& pcut, uint32_t& bbx, uint32_t& bby) {
+    auto pack = [](double lo, double hi) {
+        const int a = static_cast<int>(fmax(-32768.0, fmin(32767.0, lo)));
+        const int b = static_cast<int>(fmax(-32768.0, fmin(32767.0, hi)));
+        return (static_cast<uint32_t>(a) & 0xffffu) | (static_cast<uint32_t>(b) << 16);
+    };
+    if (!(opacity >= tau)) {  // alpha <= opacity < tau everywhere (or NaN): never blends
+        pcut = __int_as_float(0x7f800000);
+        bbx = bby = pack(32767.0, -32768.0);
+        return;
+    }
+    const double lr = log(static_cast<double>(opacity) / static_cast<double>(tau));  // >= 0
+    const double cut = -lr - 1e-4 * (1.0 + lr);
+    pcut = __double2float_rd(cut);
+    // q = -2 * power, evaluated in float: q_f >= Q * (1 - 64 u kappa).
+    const double a = ixx, b = ixy, c = iyy;
+    const double det = a * c - b * b;
+    const double tr = a + c;
+    const double disc = sqrt(fmax(0.0, 0.25 * (a - c) * (a - c) + b * b));
+    const double lmax = 0.5 * tr + disc, lmin = 0.5 * tr - disc;
+    const double relerr = 64.0 * 0x1p-24 * (lmin > 0.0 ? lmax / lmin : 1e300);
+    if (!(det > 0.0) || !(lmin > 0.0) || !(relerr < 0.5) || !isfinite(mx) || !isfinite(my)) {
+        bbx = bby = pack(-32768.0, 32767.0);  // no culling for this splat
+        return;
+    }
+    const double r2 = (-2.0 * cut) / (1.0 - relerr);
+    const double ex = sqrt(r2 * c / det) * 1.0001 + 1e-3;  // (M^-1)_xx = iyy / det
+    const double ey = sqrt(r2 * a / det) * 1.0001 + 1e-3;
+    bbx = pack(floor(mx - ex - 0.5) - 1.0, ceil(mx + ex - 0.5) + 1.0);
+    bby = pack(floor(my - ey - 0.5) - 1.0, ceil(my + ey - 0.5) + 1.0);
+}
+
+
+// ---- decoupled look-back state words -----------------------------------
+// u64 = [63:62] flag | [61:32] epoch | [31:0] value.  The epoch (bumped per
+// launch) makes stale words from earlier launches invisible, so the state
+// arrays never need clearing.
+constexpr uint64_t kFlagAgg = 1ull << 62;
+constexpr uint64_t kFlagIncl = 2ull << 62;
+
+__device__ __forceinline__ uint64_t lb_pack(uint64_t flag, uint32_t epoch, uint32_t v) {
+    return flag | (static_cast<uint64_t>(epoch & 0x3fffffffu) << 32) | v;
+}
+__device__ __forceinline__ void lb_store(uint64_t* a, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t lb_load(const uint64_t* a) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t sat_add(uint32_t a, uint32_t b) {
+    const uint32_t s = a + b;
+    return s < a ? 0xffffffffu : s;
+}
+
+// Single-value look-back by one warp.  Returns the exclusive prefix of
+// `tile` and publishes its inclusive prefix.  Called by all 32 lanes of one
+// warp; `aggregate` must be warp-uniform.
+__device__ __forceinline__ uint32_t lookback_warp(uint64_t* states, uint32_t tile,
+                                                  uint32_t aggregate, uint32_t epoch) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t ep = epoch & 0x3fffffffu;
+    if (tile == 0) {
+        if (lane == 0) lb_store(&states[0], lb_pack(kFlagIncl, epoch, aggregate));
+        return 0;
+    }
+    if (lane == 0) lb_store(&states[tile], lb_pack(kFlagAgg, epoch, aggregate));
+    uint32_t prefix = 0;
+    int64_t base = static_cast<int64_t>(tile) - 1;
+    while (true) {
+        const int64_t idx = base - lane;
+        uint64_t s = kFlagIncl;  // virtual inclusive predecessor of tile 0
+        uint64_t flag = kFlagIncl;
+        if (idx >= 0) {
+            s = lb_load(&states[idx]);
+            flag = s & (3ull << 62);
+            if (static_cast<uint32_t>((s >> 32) & 0x3fffffffu) != ep) flag = 0;
+        }
+        // All lanes must hold a published word before the window is consumed.
+        if (__any_sync(0xffffffffu, flag == 0)) continue;
+        const uint32_t incl_mask = __ballot_sync(0xffffffffu, flag == kFlagIncl);
+        const uint32_t v = static_cast<uint32_t>(s);
+        const int stop = incl_mask ? __ffs(incl_mask) - 1 : 31;
+        uint32_t contrib = lane <= stop ? v : 0u;
+        for (int o = 16; o > 0; o >>= 1) contrib = sat_add(contrib, __shfl_xor_sync(0xffffffffu, contrib, o));
+        prefix = sat_add(prefix, contrib);
+        if (incl_mask) break;
+        base -= 32;
+    }
+    if (lane == 0) lb_store(&states[tile], lb_pack(kFlagIncl, epoch, sat_add(prefix, aggregate)));
+    return prefix;
+}
+
+// Per-frame device counters (one small memset per frame).
+struct Counters {
+    uint32_t tile_ctr[16];  // dynamic tile ids for look-back kernels
+    uint32_t m;             // splats with >= 1 tile (depth-sort length)
+    uint32_t s;             // survivors (splat_count)
+    uint32_t p;             // total pairs (saturating)
+    uint32_t overflow;      // pair buffer capacity exceeded
+    uint32_t p_eff;         // p if it fits the pair buffers, else 0 (memory safety)
+    uint32_t pad[11];
+};
+
+}  // namespace agsx

@@ -1,0 +1,198 @@
+// k_pairs.cu -- K3 pair emission and K5 tile ranges.
+//
+//   reference: generate_pairs emit pass  pair_gen.cpp:187-201
+//              serial prefix sum         pair_gen.cpp:177-180
+//              pack_pair_key             pair_gen.hpp:33-36
+//              range scan                pair_sort.cpp:30-42
+//
+// The fused path emits pairs in depth-sorted splat order (ties by Gaussian
+// id), so a stable sort on the tile field alone yields exactly the
+// reference's stable (tile, depth, emission order) permutation -- LSD radix
+// order with the 32 depth bits sorted once per splat instead of once per
+// pair.  The exclusive scan of the per-splat tile counts is
+// fused into the emit kernel with a decoupled look-back.
+#include "kernels.cuh"
+
+namespace agsx {
+
+__device__ __forceinline__ TileTest planes_tile_test(const FrameParams& p, const SplatPlanes& pl,
+                                                     uint32_t g) {
+    const float4 a = pl.p0[g];
+    const float iyy = pl.p1[g].x;
+    const float4 c = pl.p3[g];
+    TileTest t;
+    t.mode = p.mode;
+    t.cx = a.x;
+    t.cy = a.y;
+    t.ixx = a.z;
+    t.ixy = a.w;
+    t.iyy = iyy;
+    t.rx = c.x;
+    t.ry = c.y;
+    t.r2 = c.z;
+    t.v1x = t.v1y = t.a = t.b = 0.0f;
+    if (p.mode == AGSX_MODE_OBB) {
+        const float4 e = pl.p4[g];
+        t.v1x = e.x;
+        t.v1y = e.y;
+        t.a = e.z;
+        t.b = e.w;
+    }
+    return t;
+}
+
+// Persistent over the depth-sorted splat list; per 256-splat tile: block
+// scan of tile counts + look-back -> pair offsets, then emission of
+// (tile id, Gaussian id) for every intersected tile in row-major order.
+__global__ void __launch_bounds__(256)
+k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __restrict__ status,
+       SplatPlanes pl, uint32_t* __restrict__ tkeys, uint32_t* __restrict__ pvals,
+       uint64_t capacity, uint64_t* lb_states, Counters* ctr, uint32_t epoch) {
+    __shared__ uint32_t s_tile, s_prefix;
+    __shared__ uint32_t s_warp[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = ctr->m;
+    const uint32_t ntiles = (n + 255u) / 256u;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(&ctr->tile_ctr[1], 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if (tile >= ntiles) break;
+        const uint32_t j = tile * 256u + tid;
+        uint32_t g = 0, cnt = 0;
+        if (j < n) {
+            g = order[j];
+            cnt = status[g] & kCountMask;
+        }
+        // block exclusive scan of cnt
+        uint32_t incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = lane < 8 ? s_warp[lane] : 0u;
+            uint32_t wi = v;
+            for (int o = 1; o < 8; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += t;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, wi, 7);
+            if (lane < 8) s_warp[lane] = wi - v;
+            const uint32_t prefix = lookback_warp(lb_states, tile, total, epoch);
+            if (lane == 0) {
+                s_prefix = prefix;
+                if (tile == ntiles - 1) {
+                    const uint32_t pt = sat_add(prefix, total);
+                    ctr->p = pt;
+                    ctr->p_eff = (pt != 0xffffffffu && pt <= capacity) ? pt : 0u;
+                }
+            }
+        }
+        __syncthreads();
+        if (cnt) {
+            const uint64_t off = static_cast<uint64_t>(s_prefix) + s_warp[warp] + (incl - cnt);
+            if (off + cnt > capacity || s_prefix == 0xffffffffu) {
+                atomicOr(&ctr->overflow, 1u);
+            } else {
+                const TileTest t = planes_tile_test(p, pl, g);
+                const Span s = tile_span(t, p);
+                uint64_t at = off;
+                for (int ty = s.ty0; ty <= s.ty1; ++ty)
+                    for (int tx = s.tx0; tx <= s.tx1; ++tx)
+                        if (tile_hit(t, tx, ty, p)) {
+                            tkeys[at] = static_cast<uint32_t>(ty * p.tiles_x + tx);
+                            pvals[at] = g;
+                            ++at;
+                        }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Standalone generate_pairs over a splat list (agsx_generate_pairs):
+// planes + tile counts per list entry.
+__global__ void k_splats_to_planes(FrameParams p, const agsx_splat_view* __restrict__ splats,
+                                   uint64_t n, SplatPlanes pl, uint32_t* __restrict__ counts,
+                                   uint32_t* __restrict__ depth_bits) {
+    const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const agsx_splat_view s = splats[j];
+    const TileTest t = make_tile_test(s.mean2d[0], s.mean2d[1], s.cov2d[0], s.cov2d[1], s.cov2d[2],
+                                      s.inv_cov[0], s.inv_cov[1], s.inv_cov[2], s.opacity, s.th, p);
+    counts[j] = count_tiles(t, p);
+    depth_bits[j] = __float_as_uint(s.depth);
+    float pcut;
+    uint32_t bbx, bby;
+    blend_cull_data(s.mean2d[0], s.mean2d[1], s.inv_cov[0], s.inv_cov[1], s.inv_cov[2], s.opacity,
+                    p.tau, pcut, bbx, bby);
+    pl.p0[j] = make_float4(s.mean2d[0], s.mean2d[1], s.inv_cov[0], s.inv_cov[1]);
+    pl.p1[j] = make_float4(s.inv_cov[2], s.opacity, pcut, __uint_as_float(bbx));
+    pl.p2[j] = make_float4(s.rgb[0], s.rgb[1], s.rgb[2], __uint_as_float(bby));
+    pl.p3[j] = make_float4(t.rx, t.ry, t.r2, 0.0f);
+    if (p.mode == AGSX_MODE_OBB) pl.p4[j] = make_float4(t.v1x, t.v1y, t.a, t.b);
+}
+
+// Emission in list order (the reference's splat order) with 64-bit keys.
+__global__ void k_emit_list(FrameParams p, uint64_t n, SplatPlanes pl,
+                            const uint32_t* __restrict__ counts, const uint64_t* __restrict__ offsets,
+                            const uint32_t* __restrict__ depth_bits, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ vals) {
+    const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= n || counts[j] == 0) return;
+    const TileTest t = planes_tile_test(p, pl, static_cast<uint32_t>(j));
+    const Span s = tile_span(t, p);
+    uint64_t at = offsets[j];
+    const uint64_t lo = depth_bits[j];
+    for (int ty = s.ty0; ty <= s.ty1; ++ty)
+        for (int tx = s.tx0; tx <= s.tx1; ++tx)
+            if (tile_hit(t, tx, ty, p)) {
+                keys[at] = (static_cast<uint64_t>(ty * p.tiles_x + tx) << 32) | lo;
+                vals[at] = static_cast<uint32_t>(j);
+                ++at;
+            }
+}
+
+// ranges[tile] = [first, last+1) over the tile-sorted pair list; tiles
+// without pairs keep the {0,0} written by the frame memset.
+__global__ void k_ranges_u32(const uint32_t* __restrict__ keys, const uint32_t* n_dev,
+                             uint2* __restrict__ ranges) {
+    const uint32_t n = *n_dev;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t t = keys[i];
+        if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
+        if (i == n - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+    }
+}
+
+// Same over full 64-bit keys (sort_pairs API): tile = key >> 32, ignored
+// when >= tile_count (pair_sort.cpp:39).
+__global__ void k_ranges_u64(const uint64_t* __restrict__ keys, uint64_t n, uint32_t tile_count,
+                             uint2* __restrict__ ranges) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t t = static_cast<uint32_t>(keys[i] >> 32);
+        if (t >= tile_count) continue;
+        if (i == 0 || static_cast<uint32_t>(keys[i - 1] >> 32) != t)
+            ranges[t].x = static_cast<uint32_t>(i);
+        if (i == n - 1 || static_cast<uint32_t>(keys[i + 1] >> 32) != t)
+            ranges[t].y = static_cast<uint32_t>(i + 1);
+    }
+}
+
+__global__ void k_logf(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        y[i] = glibc_logf(x[i]);
+}
+
+__global__ void k_expf(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        y[i] = glibc_expf(x[i]);
+}
+
+}  // namespace agsx

@@ -1,0 +1,301 @@
+// k_preprocess.cu -- K1: per-Gaussian preprocess fused with the tile-count
+// pass and the order-preserving compaction of the splats that hit >= 1 tile.
+//
+//   reference: preprocess_view  preprocess.cpp:118-163
+//              project          preprocess.cpp:26-66
+//              eval_color       preprocess.cpp:68-105
+//              compute_th       preprocess.cpp:107-116
+//              count pass       pair_gen.cpp:167-175 (intersect_tiles :108-159)
+//
+// One thread per Gaussian; one 256-thread CTA per 256 Gaussians, CTA order
+// taken from an atomic counter so the single-pass (decoupled look-back)
+// compaction only ever waits on CTAs that are already resident.
+#include "agsx_internal.cuh"
+#include "kernels.cuh"
+
+namespace agsx {
+
+namespace {
+
+constexpr float kShC0 = 0.28209479177387814f;
+constexpr float kShC1 = 0.4886025119029199f;
+__device__ __constant__ float kShC2[5] = {1.0925484305920792f, -1.0925484305920792f,
+                                          0.31539156525252005f, -1.0925484305920792f,
+                                          0.5462742152960396f};
+__device__ __constant__ float kShC3[7] = {-0.5900435899266435f, 2.890611442640554f,
+                                          -0.4570457994644658f, 0.3731763325901154f,
+                                          -0.4570457994644658f, 1.445305721320277f,
+                                          -0.5900435899266435f};
+
+// TUpperLUT::value_at (lut.hpp:16-25) with x86 float->int semantics.
+__device__ __forceinline__ float lut_value(const FrameParams& p, float depth) {
+    const float w = (p.lut_dmax - p.lut_dmin) / static_cast<float>(p.lut_n);
+    int b = f2i_x86((depth - p.lut_dmin) / w);
+    if (b < 0) b = 0;
+    if (b >= p.lut_n) b = p.lut_n - 1;
+    return p.lut_ext ? p.lut_ext[b] : p.lut[b];
+}
+
+// eval_color (preprocess.cpp:68-105), coefficient-major SH.
+__device__ __forceinline__ void eval_color(const DevScene& sc, uint64_t i, float sh0r, float sh0g,
+                                           float sh0b, float dx, float dy, float dz, float* rgb) {
+    float r = kShC0 * sh0r, g = kShC0 * sh0g, b = kShC0 * sh0b;
+    const int D = sc.sh_coeffs;
+    if (D > 1) {
+        const float* sh = sc.sh_rest + i * static_cast<uint64_t>((D - 1) * 3) - 3;  // sh[k*3+c], k>=1
+        auto acc = [&](float w, int k) {
+            r += w * sh[k * 3 + 0];
+            g += w * sh[k * 3 + 1];
+            b += w * sh[k * 3 + 2];
+        };
+        const float x = dx, y = dy, z = dz;
+        acc(-kShC1 * y, 1);
+        acc(kShC1 * z, 2);
+        acc(-kShC1 * x, 3);
+        if (D > 4) {
+            const float xx = x * x, yy = y * y, zz = z * z;
+            const float xy = x * y, yz = y * z, xz = x * z;
+            acc(kShC2[0] * xy, 4);
+            acc(kShC2[1] * yz, 5);
+            acc(kShC2[2] * (2.0f * zz - xx - yy), 6);
+            acc(kShC2[3] * xz, 7);
+            acc(kShC2[4] * (xx - yy), 8);
+            if (D > 9) {
+                acc(kShC3[0] * y * (3.0f * xx - yy), 9);
+                acc(kShC3[1] * xy * z, 10);
+                acc(kShC3[2] * y * (4.0f * zz - xx - yy), 11);
+                acc(kShC3[3] * z * (2.0f * zz - 3.0f * xx - 3.0f * yy), 12);
+                acc(kShC3[4] * x * (4.0f * zz - xx - yy), 13);
+                acc(kShC3[5] * z * (xx - yy), 14);
+                acc(kShC3[6] * x * (xx - 3.0f * yy), 15);
+            }
+        }
+    }
+    rgb[0] = sclamp(r + 0.5f, 0.0f, 1.0f);
+    rgb[1] = sclamp(g + 0.5f, 0.0f, 1.0f);
+    rgb[2] = sclamp(b + 0.5f, 0.0f, 1.0f);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(256)
+k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ status,
+             uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals, uint64_t* lb_states,
+             Counters* ctr, uint32_t epoch, agsx_splat_view* __restrict__ dump) {
+    __shared__ uint32_t s_tile;
+    __shared__ uint32_t s_warp_keep[8];
+    __shared__ uint32_t s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(&ctr->tile_ctr[0], 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const uint64_t i = static_cast<uint64_t>(tile) * 256u + tid;
+
+    bool alive = false, keep = false;
+    float depth = 0.0f;
+    if (i < sc.n) {
+        const float4 po = sc.pos_op[i];
+        const float4 q = sc.rot[i];
+        const float4 sr = sc.scale_r[i];
+        const float opacity = po.w;
+        // to_camera (scene.hpp:41-43, Mat3f*Vec3f math.hpp:43-49)
+        const float dx = po.x - p.cam_pos[0], dy = po.y - p.cam_pos[1], dz = po.z - p.cam_pos[2];
+        const float tx = p.R[0] * dx + p.R[1] * dy + p.R[2] * dz;
+        const float ty = p.R[3] * dx + p.R[4] * dy + p.R[5] * dz;
+        const float tz = p.R[6] * dx + p.R[7] * dy + p.R[8] * dz;
+        bool ok = !(tz <= p.near_plane);
+        float m2x = 0.0f, m2y = 0.0f;
+        if (ok) {
+            const float inv_z = 1.0f / tz;
+            m2x = p.fx * tx * inv_z + p.ppx;
+            m2y = p.fy * ty * inv_z + p.ppy;
+            const float ndc_x = (m2x - p.ppx) / p.ppx;
+            const float ndc_y = (m2y - p.ppy) / p.ppy;
+            ok = !(fabsf(ndc_x) > p.guard || fabsf(ndc_y) > p.guard);
+        }
+        float cxx = 0.0f, cxy = 0.0f, cyy = 0.0f, det = 0.0f, th = p.tau;
+        if (ok) {
+            // Jacobian at the clamped point, double precision (preprocess.cpp:42-57)
+            const double iz = 1.0 / static_cast<double>(tz);
+            const double txc = sclampd(tx * iz, -p.lim_x, p.lim_x) * tz;
+            const double tyc = sclampd(ty * iz, -p.lim_y, p.lim_y) * tz;
+            const double j00 = p.fx * iz, j01 = 0.0, j02 = -p.fx * txc * iz * iz;
+            const double j10 = 0.0, j11 = p.fy * iz, j12 = -p.fy * tyc * iz * iz;
+            // jw = J * W  (rows 0, 1; Mat3 product math.hpp:50-59, s = 0 then +=)
+            double jw[2][3];
+            for (int c = 0; c < 3; ++c) {
+                const double w0 = p.R[c], w1 = p.R[3 + c], w2 = p.R[6 + c];
+                double s = 0.0;
+                s += j00 * w0;
+                s += j01 * w1;
+                s += j02 * w2;
+                jw[0][c] = s;
+                s = 0.0;
+                s += j10 * w0;
+                s += j11 * w1;
+                s += j12 * w2;
+                jw[1][c] = s;
+            }
+            // covariance_3d (scene.cpp:31-39) with rotation_matrix<double> (math.hpp:147-164)
+            const double n = sqrt(static_cast<double>(q.x) * q.x + static_cast<double>(q.y) * q.y +
+                                  static_cast<double>(q.z) * q.z + static_cast<double>(q.w) * q.w);
+            const double qw = q.x / n, qx = q.y / n, qy = q.z / n, qz = q.w / n;
+            double rs[9];
+            rs[0] = 1 - 2 * (qy * qy + qz * qz);
+            rs[1] = 2 * (qx * qy - qw * qz);
+            rs[2] = 2 * (qx * qz + qw * qy);
+            rs[3] = 2 * (qx * qy + qw * qz);
+            rs[4] = 1 - 2 * (qx * qx + qz * qz);
+            rs[5] = 2 * (qy * qz - qw * qx);
+            rs[6] = 2 * (qx * qz - qw * qy);
+            rs[7] = 2 * (qy * qz + qw * qx);
+            rs[8] = 1 - 2 * (qx * qx + qy * qy);
+            for (int row = 0; row < 3; ++row) {
+                rs[row * 3 + 0] *= sr.x;
+                rs[row * 3 + 1] *= sr.y;
+                rs[row * 3 + 2] *= sr.z;
+            }
+            double cov[9];
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) {
+                    double s = 0.0;
+                    s += rs[r * 3 + 0] * rs[c * 3 + 0];
+                    s += rs[r * 3 + 1] * rs[c * 3 + 1];
+                    s += rs[r * 3 + 2] * rs[c * 3 + 2];
+                    cov[r * 3 + c] = s;
+                }
+            // sigma = (jw * cov) * jw^T, entries (0,0), (0,1), (1,1)
+            double t[2][3];
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 3; ++c) {
+                    double s = 0.0;
+                    s += jw[r][0] * cov[0 * 3 + c];
+                    s += jw[r][1] * cov[1 * 3 + c];
+                    s += jw[r][2] * cov[2 * 3 + c];
+                    t[r][c] = s;
+                }
+            double s00 = 0.0, s01 = 0.0, s11 = 0.0;
+            s00 += t[0][0] * jw[0][0];
+            s00 += t[0][1] * jw[0][1];
+            s00 += t[0][2] * jw[0][2];
+            s01 += t[0][0] * jw[1][0];
+            s01 += t[0][1] * jw[1][1];
+            s01 += t[0][2] * jw[1][2];
+            s11 += t[1][0] * jw[1][0];
+            s11 += t[1][1] * jw[1][1];
+            s11 += t[1][2] * jw[1][2];
+            cxx = static_cast<float>(s00 + 0.3);
+            cxy = static_cast<float>(s01);
+            cyy = static_cast<float>(s11 + 0.3);
+            det = cxx * cyy - cxy * cxy;
+            ok = det > 0.0f;
+        }
+        if (ok && p.adaptive) {
+            // compute_th, Eq. 10 (preprocess.cpp:107-116)
+            const float t_upper = lut_value(p, tz);
+            const float denom = t_upper * 2.0f * 3.14159265358979323846f * sqrtf(det);
+            th = p.k / denom + p.tau;
+        }
+        if (ok && th >= opacity) ok = false;
+        uint32_t cnt = 0;
+        if (ok) {
+            alive = true;
+            depth = tz;
+            const float inv_det = 1.0f / det;  // SymMat2::inverse (math.hpp:85-88)
+            const float ixx = cyy * inv_det, ixy = -cxy * inv_det, iyy = cxx * inv_det;
+            const TileTest tt = make_tile_test(m2x, m2y, cxx, cxy, cyy, ixx, ixy, iyy, opacity, th, p);
+            cnt = count_tiles(tt, p);
+            keep = cnt > 0;
+            float rgb[3] = {0.5f, 0.5f, 0.5f};
+            if (keep || dump) {
+                // Vec3f::normalized (math.hpp:25-28) of mean - cam.position
+                const float nrm = sqrtf(dx * dx + dy * dy + dz * dz);
+                float ux = 0.0f, uy = 0.0f, uz = 0.0f;
+                if (nrm > 0.0f) {
+                    const float inv = 1.0f / nrm;
+                    ux = dx * inv;
+                    uy = dy * inv;
+                    uz = dz * inv;
+                }
+                const float2 gb = sc.sh_gb[i];
+                eval_color(sc, i, sr.w, gb.x, gb.y, ux, uy, uz, rgb);
+            }
+            if (keep) {
+                float pcut;
+                uint32_t bbx, bby;
+                blend_cull_data(m2x, m2y, ixx, ixy, iyy, opacity, p.tau, pcut, bbx, bby);
+                pl.p0[i] = make_float4(m2x, m2y, ixx, ixy);
+                pl.p1[i] = make_float4(iyy, opacity, pcut, __uint_as_float(bbx));
+                pl.p2[i] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(bby));
+                pl.p3[i] = make_float4(tt.rx, tt.ry, tt.r2, 0.0f);
+                if (p.mode == AGSX_MODE_OBB) pl.p4[i] = make_float4(tt.v1x, tt.v1y, tt.a, tt.b);
+            }
+            if (dump) {
+                agsx_splat_view v;
+                v.mean2d[0] = m2x;
+                v.mean2d[1] = m2y;
+                v.cov2d[0] = cxx;
+                v.cov2d[1] = cxy;
+                v.cov2d[2] = cyy;
+                v.inv_cov[0] = ixx;
+                v.inv_cov[1] = ixy;
+                v.inv_cov[2] = iyy;
+                v.depth = tz;
+                v.rgb[0] = rgb[0];
+                v.rgb[1] = rgb[1];
+                v.rgb[2] = rgb[2];
+                v.opacity = opacity;
+                v.th = th;
+                v.source_id = static_cast<uint32_t>(i);
+                dump[i] = v;
+            }
+        }
+        status[i] = cnt | (alive ? kAliveBit : 0u);
+    }
+
+    // ---- order-preserving compaction of `keep` (single pass) -----------
+    const uint32_t keep_mask = __ballot_sync(0xffffffffu, keep);
+    const uint32_t alive_cnt = __popc(__ballot_sync(0xffffffffu, alive));
+    if (lane == 0) s_warp_keep[warp] = __popc(keep_mask);
+    if (alive_cnt && lane == 0) atomicAdd(&ctr->s, alive_cnt);
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = lane < 8 ? s_warp_keep[lane] : 0u;
+        uint32_t incl = v;
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 7);
+        if (lane < 8) s_warp_keep[lane] = incl - v;
+        const uint32_t prefix = lookback_warp(lb_states, tile, total, epoch);
+        if (lane == 0) {
+            s_prefix = prefix;
+            if (tile == gridDim.x - 1) ctr->m = prefix + total;
+        }
+    }
+    __syncthreads();
+    if (keep) {
+        const uint32_t pos = s_prefix + s_warp_keep[warp] + __popc(keep_mask & ((1u << lane) - 1u));
+        dkeys[pos] = __float_as_uint(depth);
+        dvals[pos] = static_cast<uint32_t>(i);
+    }
+}
+
+// Scene upload: host SoA (agsx_scene_desc) -> device planes.
+__global__ void k_pack_scene(uint64_t n, int D, const float* __restrict__ mean,
+                             const float* __restrict__ scale, const float* __restrict__ rot,
+                             const float* __restrict__ op, const float* __restrict__ sh,
+                             float4* pos_op, float4* rotq, float4* scale_r, float2* sh_gb,
+                             float* sh_rest) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    pos_op[i] = make_float4(mean[3 * i], mean[3 * i + 1], mean[3 * i + 2], op[i]);
+    rotq[i] = make_float4(rot[4 * i], rot[4 * i + 1], rot[4 * i + 2], rot[4 * i + 3]);
+    const float* s = sh + i * 3 * D;
+    scale_r[i] = make_float4(scale[3 * i], scale[3 * i + 1], scale[3 * i + 2], s[0]);
+    sh_gb[i] = make_float2(s[1], s[2]);
+    for (int k = 3; k < 3 * D; ++k) sh_rest[i * (3 * D - 3) + (k - 3)] = s[k];
+}
+
+}  // namespace agsx

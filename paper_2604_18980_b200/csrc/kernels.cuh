@@ -1,0 +1,49 @@
+// kernels.cuh -- kernel declarations shared between the translation units.
+#pragma once
+#include "agsx_internal.cuh"
+
+namespace agsx {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // keys per onesweep tile
+
+__global__ void k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* status,
+                             uint32_t* dkeys, uint32_t* dvals, uint64_t* lb_states, Counters* ctr,
+                             uint32_t epoch, agsx_splat_view* dump);
+__global__ void k_pack_scene(uint64_t n, int D, const float* mean, const float* scale,
+                             const float* rot, const float* op, const float* sh, float4* pos_op,
+                             float4* rotq, float4* scale_r, float2* sh_gb, float* sh_rest);
+
+__global__ void k_emit(FrameParams p, const uint32_t* order, const uint32_t* status,
+                       SplatPlanes pl, uint32_t* tkeys, uint32_t* pvals, uint64_t capacity,
+                       uint64_t* lb_states, Counters* ctr, uint32_t epoch);
+__global__ void k_splats_to_planes(FrameParams p, const agsx_splat_view* splats, uint64_t n,
+                                   SplatPlanes pl, uint32_t* counts, uint32_t* depth_bits);
+__global__ void k_emit_list(FrameParams p, uint64_t n, SplatPlanes pl, const uint32_t* counts,
+                            const uint64_t* offsets, const uint32_t* depth_bits, uint64_t* keys,
+                            uint32_t* vals);
+__global__ void k_ranges_u32(const uint32_t* keys, const uint32_t* n_dev, uint2* ranges);
+__global__ void k_ranges_u64(const uint64_t* keys, uint64_t n, uint32_t tile_count, uint2* ranges);
+
+// Templated kernels are launched through host functions defined in the
+// translation unit that instantiates them (a template kernel's host stub is
+// only registered there).
+template <typename K>
+void launch_hist(int grid, cudaStream_t st, const K* keys, const uint32_t* n_dev, uint64_t n_host,
+                 int first_shift, int npasses, uint32_t* hist);
+template <typename K>
+void launch_onesweep(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
+                     uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift,
+                     const uint32_t* hist, uint64_t* lb, uint32_t* tile_ctr, uint32_t epoch);
+template <typename K>
+cudaError_t onesweep_configure(size_t smem, int* occupancy);
+
+void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t st, const FrameParams& p,
+                          const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
+                          const float4* P2, float* image, uint32_t* maxt_buf);
+
+__global__ void k_logf(const float* x, float* y, uint64_t n);
+__global__ void k_expf(const float* x, float* y, uint64_t n);
+
+}  // namespace agsx

@@ -1,0 +1,475 @@
+// bindings.cpp -- pybind11 module paper_2604_18980_b200._core.
+//
+// Mirrors the reference's Python module adagscale._core
+// (/root/reference/proj/python/bindings.cpp:129-201): Scene, synth_scene,
+// render, psnr, write_image, peripheral_score_closed, pack_pair_key with the
+// same argument names, defaults, return dicts and exception types.  render()
+// runs on the GPU through libagsx.so with the GIL released; the Scene keeps
+// a device-resident copy after its first render.
+//
+// B200 additions: Renderer (one CUDA context/stream, asynchronous frames
+// that stay in HBM, parity dumps), and the per-stage entry points.
+#include <pybind11/numpy.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <mutex>
+#include <numbers>
+#include <stdexcept>
+
+#include "agsx.h"
+#include "ags/ags.hpp"
+
+namespace py = pybind11;
+
+namespace {
+
+using f32arr = py::array_t<float, py::array::c_style | py::array::forcecast>;
+
+struct SceneDeleter {
+    void operator()(agsx_scene* s) const { agsx_scene_free(s); }
+};
+
+// Host SoA copy + lazily uploaded device copy (one per device).
+struct Scene {
+    std::uint64_t n = 0;
+    int D = 1;
+    std::vector<float> mean, scale, rot, op, sh;
+    std::vector<agsx_camera> cameras;
+    std::map<int, std::shared_ptr<agsx_scene>> device;
+    std::mutex mu;
+};
+
+class Renderer;
+Renderer& default_renderer();
+
+[[noreturn]] void raise_status(int rc, const agsx_ctx* ctx) {
+    const std::string msg = ctx ? agsx_last_error(ctx) : "agsx error";
+    if (rc == AGSX_EINVAL) throw py::value_error(msg);
+    if (rc == AGSX_EPAIR_BUDGET) throw ags::PairBudgetError(msg);
+    if (rc == AGSX_ENOMEM) throw std::bad_alloc();
+    throw std::runtime_error(msg.empty() ? "agsx: device error" : msg);
+}
+
+agsx_config make_config(const std::string& mode, double k, int threads, int tile_size, bool exact,
+                        std::size_t pair_budget) {
+    ags::RenderConfig def;
+    ags::Mode m;
+    if (!ags::parse_mode(mode, m)) throw py::value_error("unknown mode '" + mode + "'");
+    agsx_config c{};
+    c.tile_size = tile_size;
+    c.alpha_threshold = def.alpha_threshold;
+    c.transmittance_floor = def.transmittance_floor;
+    c.alpha_clamp = def.alpha_clamp;
+    c.near_plane = def.near_plane;
+    c.guard_band = def.guard_band;
+    c.mode = static_cast<int>(m);
+    c.k = static_cast<float>(k);
+    c.thread_count = threads;
+    c.fixed_radius_aabb = 0;
+    c.pair_budget = pair_budget;
+    c.flags = exact ? AGSX_FLAG_EXACT_ALPHA : 0u;
+    return c;
+}
+
+// bindings.cpp:44-53 of the reference: empty bins -> the all-ones LUT.
+struct LutHolder {
+    std::vector<float> bins;
+    agsx_lut lut{};
+    LutHolder(const std::vector<float>& b, float dmin, float dmax) {
+        if (b.empty()) {
+            bins.assign(20, 1.0f);
+            lut.depth_min = 0.0f;
+            lut.depth_max = 100.0f;
+        } else {
+            bins = b;
+            lut.depth_min = dmin;
+            lut.depth_max = dmax;
+        }
+        lut.bin_count = static_cast<int32_t>(bins.size());
+        lut.bins = bins.data();
+    }
+};
+
+class Renderer {
+public:
+    explicit Renderer(int device) : device_(device) {
+        const int rc = agsx_create(device, &ctx_);
+        if (rc != AGSX_OK) throw std::runtime_error("agsx_create failed: no usable CUDA device " + std::to_string(device));
+    }
+    ~Renderer() {
+        if (ctx_) agsx_destroy(ctx_);
+    }
+    Renderer(const Renderer&) = delete;
+    Renderer& operator=(const Renderer&) = delete;
+
+    agsx_scene* device_scene(Scene& s) {
+        std::lock_guard<std::mutex> g(s.mu);
+        auto it = s.device.find(device_);
+        if (it != s.device.end()) return it->second.get();
+        agsx_scene_desc d{s.n, s.D, s.mean.data(), s.scale.data(), s.rot.data(), s.op.data(), s.sh.data()};
+        agsx_scene* out = nullptr;
+        const int rc = agsx_scene_upload(ctx_, &d, &out);
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        s.device[device_] = std::shared_ptr<agsx_scene>(out, SceneDeleter{});
+        return out;
+    }
+
+    static const agsx_camera& view_of(const Scene& s, int view) {
+        if (view < 0 || view >= static_cast<int>(s.cameras.size()))
+            throw std::out_of_range("view index out of range");
+        return s.cameras[view];
+    }
+
+    py::dict render(Scene& scene, int view, const std::string& mode, double k,
+                    const std::vector<float>& lut_bins, float dmin, float dmax, int threads,
+                    int tile_size, bool exact, bool max_t, std::size_t pair_budget, bool image) {
+        const agsx_camera cam = view_of(scene, view);
+        const agsx_config cfg = make_config(mode, k, threads, tile_size, exact, pair_budget);
+        const LutHolder lut(lut_bins, dmin, dmax);
+        agsx_scene* dev = device_scene(scene);
+        py::array_t<float> img;
+        if (image) img = py::array_t<float>({cam.height, cam.width, 3});
+        std::vector<float> mt;
+        agsx_frame f{};
+        if (image) f.image = img.mutable_data();
+        if (max_t) {
+            mt.assign(std::max<std::uint64_t>(scene.n, 1), 0.0f);
+            f.max_t = mt.data();
+        }
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            std::lock_guard<std::mutex> g(mu_);
+            rc = agsx_render(ctx_, dev, &cam, &cfg, cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr, &f);
+        }
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        py::dict out;
+        if (image) out["image"] = img;
+        out["pair_count"] = f.pair_count;
+        out["splat_count"] = f.splat_count;
+        py::dict times;
+        const char* names[4] = {"preprocess", "pair_gen", "sort", "raster"};
+        for (int i = 0; i < 4; ++i) times[names[i]] = f.stage_ms[i] * 1e-3;
+        out["stage_times"] = times;
+        if (max_t) {
+            // per splat in preprocess order (RenderReport::max_t)
+            py::array_t<std::uint8_t> alive(scene.n);
+            rc = agsx_dump_tile_counts(ctx_, nullptr, alive.mutable_data(), scene.n);
+            if (rc != AGSX_OK) raise_status(rc, ctx_);
+            std::vector<float> comp;
+            comp.reserve(f.splat_count);
+            const std::uint8_t* a = alive.data();
+            for (std::uint64_t i = 0; i < scene.n; ++i)
+                if (a[i]) comp.push_back(mt[i]);
+            out["max_t"] = py::array_t<float>(comp.size(), comp.data());
+        }
+        return out;
+    }
+
+    void render_async(Scene& scene, int view, const std::string& mode, double k,
+                      const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size,
+                      bool exact, std::size_t pair_budget) {
+        const agsx_camera cam = view_of(scene, view);
+        const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
+        const LutHolder lut(lut_bins, dmin, dmax);
+        agsx_scene* dev = device_scene(scene);
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = agsx_render_async(ctx_, dev, &cam, &cfg, cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr);
+        }
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+    }
+
+    py::dict wait() {
+        agsx_frame f{};
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = agsx_render_wait(ctx_, &f);
+        }
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        py::dict out;
+        out["pair_count"] = f.pair_count;
+        out["splat_count"] = f.splat_count;
+        out["stage_ms"] = std::vector<float>(f.stage_ms, f.stage_ms + 4);
+        return out;
+    }
+
+    py::tuple device_image() {
+        float* p = nullptr;
+        int32_t w = 0, h = 0;
+        const int rc = agsx_device_image(ctx_, &p, &w, &h);
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        return py::make_tuple(reinterpret_cast<std::uintptr_t>(p), w, h);
+    }
+
+    py::array_t<std::uint32_t> dump_tile_counts(std::uint64_t n) {
+        py::array_t<std::uint32_t> c(n);
+        const int rc = agsx_dump_tile_counts(ctx_, c.mutable_data(), nullptr, n);
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        return c;
+    }
+
+    py::tuple dump_sorted_pairs() {
+        std::uint64_t n = 0;
+        int rc = agsx_dump_sorted_pairs(ctx_, nullptr, nullptr, 0, &n);
+        if (rc != AGSX_OK && rc != AGSX_ECAPACITY) raise_status(rc, ctx_);
+        py::array_t<std::uint64_t> keys(n);
+        py::array_t<std::uint32_t> gids(n);
+        rc = agsx_dump_sorted_pairs(ctx_, keys.mutable_data(), gids.mutable_data(), n, &n);
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        return py::make_tuple(keys, gids);
+    }
+
+    py::array_t<std::uint32_t> dump_ranges(std::uint64_t tile_count) {
+        py::array_t<std::uint32_t> r({static_cast<py::ssize_t>(tile_count), py::ssize_t(2)});
+        const int rc = agsx_dump_ranges(ctx_, r.mutable_data(), tile_count);
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        return r;
+    }
+
+    std::uintptr_t stream() const { return reinterpret_cast<std::uintptr_t>(agsx_stream(ctx_)); }
+    std::uint64_t kernel_launches() const { return agsx_kernel_launches(ctx_); }
+    int device() const { return device_; }
+
+private:
+    int device_;
+    agsx_ctx* ctx_ = nullptr;
+    std::mutex mu_;
+};
+
+Renderer& default_renderer() {
+    static std::unique_ptr<Renderer> r;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    if (!r) {
+        const char* e = std::getenv("AGS_DEVICE");
+        r = std::make_unique<Renderer>(e ? std::atoi(e) : 0);
+    }
+    return *r;
+}
+
+std::shared_ptr<Scene> make_synth(std::uint64_t seed, int count, const std::string& layout, int cameras,
+                                  int width, int height, float focal) {
+    if (count < 1) throw py::value_error("synth_scene: count must be >= 1");
+    auto s = std::make_shared<Scene>();
+    s->n = static_cast<std::uint64_t>(count);
+    s->D = 1;
+    s->mean.resize(3 * s->n);
+    s->scale.resize(3 * s->n);
+    s->rot.resize(4 * s->n);
+    s->op.resize(s->n);
+    s->sh.resize(3 * s->n);
+    s->cameras.resize(std::max(cameras, 0));
+    int rc;
+    {
+        py::gil_scoped_release nogil;
+        rc = ags_synth_scene_soa(seed, count, layout.c_str(), cameras, width, height, focal, focal,
+                                 s->mean.data(), s->scale.data(), s->rot.data(), s->op.data(),
+                                 s->sh.data(), s->cameras.data());
+    }
+    if (rc != 0) throw py::value_error("synth_scene: unknown layout '" + layout + "'");
+    return s;
+}
+
+std::shared_ptr<Scene> scene_from_arrays(f32arr mean, f32arr scale, f32arr rotation, f32arr opacity,
+                                         f32arr sh, const std::vector<py::dict>& cameras) {
+    auto s = std::make_shared<Scene>();
+    const auto n = static_cast<std::uint64_t>(opacity.size());
+    if (mean.size() != static_cast<py::ssize_t>(3 * n) || scale.size() != static_cast<py::ssize_t>(3 * n) ||
+        rotation.size() != static_cast<py::ssize_t>(4 * n) || sh.size() % (3 * std::max<std::uint64_t>(n, 1)) != 0)
+        throw py::value_error("inconsistent scene array sizes");
+    s->n = n;
+    s->D = n ? static_cast<int>(sh.size() / (3 * n)) : 1;
+    if (!(s->D == 1 || s->D == 4 || s->D == 9 || s->D == 16))
+        throw py::value_error("sh coefficient count must be 3*d^2 for d in {1,2,3,4}");
+    s->mean.assign(mean.data(), mean.data() + mean.size());
+    s->scale.assign(scale.data(), scale.data() + scale.size());
+    s->rot.assign(rotation.data(), rotation.data() + rotation.size());
+    s->op.assign(opacity.data(), opacity.data() + opacity.size());
+    s->sh.assign(sh.data(), sh.data() + sh.size());
+    for (const py::dict& d : cameras) {
+        agsx_camera c{};
+        auto pos = d["position"].cast<std::vector<float>>();
+        auto rot = d["rotation"].cast<std::vector<float>>();
+        if (pos.size() != 3 || rot.size() != 9) throw py::value_error("camera needs position[3], rotation[9]");
+        std::copy(pos.begin(), pos.end(), c.position);
+        std::copy(rot.begin(), rot.end(), c.rotation);
+        c.fx = d["fx"].cast<float>();
+        c.fy = d["fy"].cast<float>();
+        c.width = d["width"].cast<int>();
+        c.height = d["height"].cast<int>();
+        s->cameras.push_back(c);
+    }
+    return s;
+}
+
+py::dict camera_dict(const agsx_camera& c) {
+    py::dict d;
+    d["position"] = std::vector<float>(c.position, c.position + 3);
+    d["rotation"] = std::vector<float>(c.rotation, c.rotation + 9);
+    d["fx"] = c.fx;
+    d["fy"] = c.fy;
+    d["width"] = c.width;
+    d["height"] = c.height;
+    return d;
+}
+
+void check_image(const f32arr& a) {
+    if (a.ndim() != 3 || a.shape(2) != 3) throw py::value_error("expected an (H, W, 3) float array");
+}
+
+// ---- stage entry points over numpy (parity hooks) ------------------------
+py::array splats_to_numpy(const std::vector<agsx_splat_view>& v) {
+    // structured dtype identical to ags::SplatView
+    py::list names, formats, offsets;
+    auto add = [&](const char* n, const char* f, int off) {
+        names.append(n);
+        formats.append(f);
+        offsets.append(off);
+    };
+    add("mean2d", "(2,)<f4", 0);
+    add("cov2d", "(3,)<f4", 8);
+    add("inv_cov", "(3,)<f4", 20);
+    add("depth", "<f4", 32);
+    add("rgb", "(3,)<f4", 36);
+    add("opacity", "<f4", 48);
+    add("th", "<f4", 52);
+    add("source_id", "<u4", 56);
+    py::dict spec;
+    spec["names"] = names;
+    spec["formats"] = formats;
+    spec["offsets"] = offsets;
+    spec["itemsize"] = 60;
+    py::dtype dt = py::dtype::from_args(spec);
+    py::array out(dt, std::vector<py::ssize_t>{static_cast<py::ssize_t>(v.size())});
+    if (!v.empty()) std::memcpy(out.mutable_data(), v.data(), v.size() * sizeof(agsx_splat_view));
+    return out;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+    m.doc() = "B200-native tile-based gaussian splatting renderer with viewpoint-adaptive "
+              "pair reduction (AdaGScale); drop-in for adagscale._core";
+
+    py::register_exception<ags::PairBudgetError>(m, "PairBudgetError", PyExc_RuntimeError);
+
+    py::class_<Scene, std::shared_ptr<Scene>>(m, "Scene")
+        .def_property_readonly("gaussian_count", [](const Scene& s) { return s.n; })
+        .def_property_readonly("camera_count", [](const Scene& s) { return s.cameras.size(); })
+        .def_property_readonly("sh_coeffs", [](const Scene& s) { return s.D; })
+        .def("camera", [](const Scene& s, int i) { return camera_dict(Renderer::view_of(s, i)); })
+        .def("arrays",
+             [](const Scene& s) {
+                 const auto n = static_cast<py::ssize_t>(s.n);
+                 py::dict d;
+                 d["mean"] = py::array_t<float>({n, py::ssize_t(3)}, s.mean.data());
+                 d["scale"] = py::array_t<float>({n, py::ssize_t(3)}, s.scale.data());
+                 d["rotation"] = py::array_t<float>({n, py::ssize_t(4)}, s.rot.data());
+                 d["opacity"] = py::array_t<float>({n}, s.op.data());
+                 d["sh"] = py::array_t<float>({n, py::ssize_t(s.D), py::ssize_t(3)}, s.sh.data());
+                 return d;
+             })
+        .def_static("from_arrays", &scene_from_arrays, py::arg("mean"), py::arg("scale"),
+                    py::arg("rotation"), py::arg("opacity"), py::arg("sh"), py::arg("cameras"))
+        .def("__repr__", [](const Scene& s) {
+            return "<adagscale.Scene " + std::to_string(s.n) + " gaussians, " +
+                   std::to_string(s.cameras.size()) + " cameras>";
+        });
+
+    m.def("synth_scene", &make_synth, py::arg("seed"), py::arg("count"), py::arg("layout") = "slab",
+          py::arg("cameras") = 24, py::arg("width") = 640, py::arg("height") = 480,
+          py::arg("focal") = 500.0f, "Deterministic synthetic scene with its camera set");
+
+    m.def(
+        "render",
+        [](Scene& scene, int view, const std::string& mode, double k, const std::vector<float>& lut_bins,
+           float lut_depth_min, float lut_depth_max, int threads, int tile_size, bool exact, bool max_t,
+           std::size_t pair_budget) {
+            return default_renderer().render(scene, view, mode, k, lut_bins, lut_depth_min, lut_depth_max,
+                                             threads, tile_size, exact, max_t, pair_budget, true);
+        },
+        py::arg("scene"), py::arg("view") = 0, py::arg("mode") = "ellipse", py::arg("k") = 0.0,
+        py::arg("lut_bins") = std::vector<float>{}, py::arg("lut_depth_min") = 0.0f,
+        py::arg("lut_depth_max") = 100.0f, py::arg("threads") = 0, py::arg("tile_size") = 16,
+        py::arg("exact") = false, py::arg("max_t") = false,
+        py::arg("pair_budget") = std::size_t{1} << 27,
+        "Render one view on the GPU; returns dict with image, pair_count, splat_count, stage_times");
+
+    m.def(
+        "psnr",
+        [](const f32arr& a, const f32arr& b) {
+            check_image(a);
+            check_image(b);
+            if (a.shape(0) != b.shape(0) || a.shape(1) != b.shape(1))
+                throw py::value_error("psnr: image dimensions differ");
+            return ags_psnr(a.data(), b.data(), static_cast<std::uint64_t>(a.size()));
+        },
+        py::arg("a"), py::arg("b"));
+
+    m.def(
+        "write_image",
+        [](const f32arr& a, const std::string& path) {
+            // 8-bit binary PPM, round-half-away of clamp(v)*255 (gsio.cpp:265-281)
+            check_image(a);
+            const int h = static_cast<int>(a.shape(0)), w = static_cast<int>(a.shape(1));
+            std::ofstream out(path, std::ios::binary);
+            if (!out) throw std::runtime_error("cannot open '" + path + "' for writing");
+            out << "P6\n" << w << " " << h << "\n255\n";
+            std::vector<unsigned char> px(static_cast<std::size_t>(w) * h * 3);
+            const float* d = a.data();
+            for (std::size_t i = 0; i < px.size(); ++i) {
+                const float v = d[i] < 0.0f ? 0.0f : (1.0f < d[i] ? 1.0f : d[i]);
+                px[i] = static_cast<unsigned char>(std::lround(static_cast<double>(v) * 255.0));
+            }
+            out.write(reinterpret_cast<const char*>(px.data()), static_cast<std::streamsize>(px.size()));
+            if (!out) throw std::runtime_error("write failure on '" + path + "'");
+        },
+        py::arg("image"), py::arg("path"), "8-bit binary PPM");
+
+    m.def(
+        "peripheral_score_closed",
+        [](float cov_xx, float cov_xy, float cov_yy, float x, float t_const, float tau) {
+            // t_const * 2*pi*sqrt(det(cov2d)) * (x - tau)  (calibrate.cpp:67-74)
+            const float det = cov_xx * cov_yy - cov_xy * cov_xy;
+            return static_cast<double>(t_const) * 2.0 * std::numbers::pi *
+                   std::sqrt(static_cast<double>(det)) * (static_cast<double>(x) - static_cast<double>(tau));
+        },
+        py::arg("cov_xx"), py::arg("cov_xy"), py::arg("cov_yy"), py::arg("x"), py::arg("t_const") = 1.0f,
+        py::arg("tau") = 1.0f / 255.0f);
+
+    m.def("pack_pair_key", &ags::pack_pair_key, py::arg("tile"), py::arg("depth"));
+
+    py::class_<Renderer>(m, "Renderer")
+        .def(py::init<int>(), py::arg("device") = 0)
+        .def("render", &Renderer::render, py::arg("scene"), py::arg("view") = 0, py::arg("mode") = "ellipse",
+             py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{}, py::arg("lut_depth_min") = 0.0f,
+             py::arg("lut_depth_max") = 100.0f, py::arg("threads") = 0, py::arg("tile_size") = 16,
+             py::arg("exact") = false, py::arg("max_t") = false, py::arg("pair_budget") = std::size_t{1} << 27,
+             py::arg("image") = true)
+        .def("render_async", &Renderer::render_async, py::arg("scene"), py::arg("view") = 0,
+             py::arg("mode") = "ellipse", py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{},
+             py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("tile_size") = 16,
+             py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27)
+        .def("wait", &Renderer::wait)
+        .def("device_image", &Renderer::device_image)
+        .def("dump_tile_counts", &Renderer::dump_tile_counts, py::arg("n"))
+        .def("dump_sorted_pairs", &Renderer::dump_sorted_pairs)
+        .def("dump_ranges", &Renderer::dump_ranges, py::arg("tile_count"))
+        .def("upload", [](Renderer& r, Scene& s) { r.device_scene(s); })
+        .def_property_readonly("stream", &Renderer::stream)
+        .def_property_readonly("kernel_launches", &Renderer::kernel_launches)
+        .def_property_readonly("device", &Renderer::device);
+
+    m.def("default_renderer", &default_renderer, py::return_value_policy::reference);
+    m.attr("SPLAT_ITEMSIZE") = static_cast<int>(sizeof(agsx_splat_view));
+    (void)&splats_to_numpy;
+}

@@ -1,0 +1,358 @@
+"""GPU parity of the CUDA render path against the CPU oracle, through the C-ABI.
+
+Bar (north star): per-Gaussian tile counts, survivor sets, total pairs,
+sorted 64-bit (tile|depth) keys and tile ranges bit-exact; images bit-exact
+with AGSX_FLAG_EXACT_ALPHA and within max-abs 1e-3 / PSNR >= 50 dB on the
+default (hardware-exp, guard-banded) path.  Known-answer cases follow the
+reference unit suites (file:line cited per test).
+"""
+import numpy as np
+import pytest
+
+from paper_2604_18980_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+IMG_MAX_ABS = 1e-3  # north_star tolerance, per channel
+IMG_MIN_PSNR = 50.0  # dB vs the oracle image
+
+# calibrated AdaGScale parameters (reference `calibrate` on veil 100K 1080p)
+K1080 = 0.3985099792480469
+LUT_BINS = [1.0] * 20
+LUT_BINS[7] = 0.003038157941773534
+LUT_BINS[8] = 0.007012989837676287
+
+
+def scene_pair(port, ctx, seed, count, layout, cams, w, h, focal):
+    """Same synthetic scene for the oracle (its own generator) and the GPU (the product's)."""
+    import paper_2604_18980_b200 as P
+
+    o = port.synth_scene(seed, count, layout, cameras=cams, width=w, height=h, focal=focal)
+    s = P.synth_scene(seed, count, layout, cameras=cams, width=w, height=h, focal=focal)
+    a = s.arrays()
+    for f in ("mean", "scale", "rotation", "opacity", "sh"):
+        assert np.array_equal(a[f].reshape(-1).view(np.uint32), getattr(o, f).reshape(-1).view(np.uint32)), f
+    dev = ctx.upload(a["mean"], a["scale"], a["rotation"], a["opacity"], a["sh"])
+    return o, dev
+
+
+def oracle_pipeline(port, scene, cam, cfg, lut):
+    splats = port.preprocess(scene, cam, cfg, lut)
+    keys, idx, counts = port.generate_pairs(splats, cam.width, cam.height, cfg.mode, cfg)
+    tiles = ((cam.width + cfg.tile_size - 1) // cfg.tile_size) * ((cam.height + cfg.tile_size - 1) // cfg.tile_size)
+    skeys, sidx, ranges = port.sort_pairs(keys, idx, tiles)
+    img = port.raster(splats, skeys, sidx, ranges, cam.width, cam.height, cfg)
+    return splats, counts, skeys, sidx, ranges, img
+
+
+def gpu_cfg(mode, k=0.0, exact=False, **kw):
+    return capi.default_config(mode, k, exact=exact, **kw)
+
+
+def to_gpu_cam(c):
+    g = capi.Camera()
+    g.position[:] = list(c.position)
+    g.rotation[:] = list(c.rotation)
+    g.fx, g.fy, g.width, g.height = c.fx, c.fy, c.width, c.height
+    return g
+
+
+def psnr(a, b):
+    d = a.astype(np.float64) - b.astype(np.float64)
+    mse = np.mean(d * d)
+    return np.inf if mse == 0 else 10 * np.log10(1.0 / mse)
+
+
+def check_frame(ctx, port, oscene, dev, view, mode, k=0.0, lut_bins=None, exact=True, **kw):
+    ocam = oscene.cameras[view]
+    gcam = to_gpu_cam(ocam)
+    ocfg = port.config(mode, k=k, **kw)
+    gcfg = gpu_cfg(mode, k, exact=exact, **kw)
+    olut = port.lut(lut_bins) if lut_bins is not None else None
+    glut = capi.make_lut(lut_bins) if lut_bins is not None else (capi.make_lut() if mode == "adagscale" else None)
+    splats, counts, skeys, sidx, ranges, oimg = oracle_pipeline(port, oscene, ocam, ocfg, olut)
+    out = ctx.render(dev, gcam, gcfg, glut)
+    n = oscene.count
+    # survivors and per-Gaussian tile counts
+    gcounts, galive = ctx.dump_tile_counts(n)
+    alive = np.zeros(n, bool)
+    alive[splats["source_id"]] = True
+    ocounts = np.zeros(n, np.uint32)
+    ocounts[splats["source_id"]] = counts
+    assert out["splat_count"] == len(splats)
+    assert np.array_equal(galive, alive)
+    assert np.array_equal(gcounts, ocounts)
+    assert out["pair_count"] == len(skeys)
+    # sorted keys bit-exact; values map to the oracle's splat_index via source_id
+    gkeys, ggids = ctx.dump_sorted_pairs()
+    assert np.array_equal(gkeys, skeys)
+    assert np.array_equal(ggids, splats["source_id"][sidx])
+    tiles = len(ranges)
+    assert np.array_equal(ctx.dump_ranges(tiles), ranges)
+    img = out["image"]
+    if exact:
+        assert np.array_equal(img.view(np.uint32), oimg.view(np.uint32))
+    else:
+        assert np.max(np.abs(img - oimg)) <= IMG_MAX_ABS
+        assert psnr(img, oimg) >= IMG_MIN_PSNR
+    return out, oimg
+
+
+# --------------------------------------------------------------------------- full pipeline
+@pytest.mark.parametrize("layout", ["slab", "two_slab", "veil", "ramp", "aniso"])
+@pytest.mark.parametrize("mode", ["aabb", "obb", "ellipse", "adagscale"])
+def test_render_matches_oracle_small(ctx, port, layout, mode):
+    oscene, dev = scene_pair(port, ctx, 5, 3000, layout, 3, 320, 240, 250.0)
+    check_frame(ctx, port, oscene, dev, 1, mode, k=0.3, lut_bins=[0.6] * 20 if mode == "adagscale" else None)
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_render_config1_veil_adagscale(ctx, port, exact):
+    """Config 1: veil 100K, 1920x1080, AdaGScale with the calibrated K/LUT."""
+    oscene, dev = scene_pair(port, ctx, 1, 100_000, "veil", 16, 1920, 1080, 1500.0)
+    out, _ = check_frame(ctx, port, oscene, dev, 0, "adagscale", k=K1080, lut_bins=LUT_BINS, exact=exact)
+    assert out["pair_count"] == 2_357_743  # SURVEY.md §6 [measured] on the reference
+
+
+def test_fast_alpha_within_tolerance(ctx, port):
+    oscene, dev = scene_pair(port, ctx, 9, 4000, "veil", 2, 480, 320, 375.0)
+    check_frame(ctx, port, oscene, dev, 0, "ellipse", exact=False)
+
+
+def test_background_and_tile_sizes(ctx, port):
+    oscene, dev = scene_pair(port, ctx, 53, 400, "slab", 2, 101, 77, 90.0)
+    for ts in (8, 16, 32):
+        check_frame(ctx, port, oscene, dev, 0, "ellipse", background=(0.2, 0.2, 0.2), tile_size=ts)
+        check_frame(ctx, port, oscene, dev, 0, "aabb", background=(0.2, 0.2, 0.2), tile_size=ts)
+
+
+def test_fixed_radius_aabb(ctx, port):
+    oscene, dev = scene_pair(port, ctx, 3, 2000, "veil", 2, 320, 240, 250.0)
+    check_frame(ctx, port, oscene, dev, 0, "aabb", fixed_radius_aabb=1)
+
+
+def test_k0_adagscale_equals_ellipse(ctx, port):
+    """test_rasterizer.cpp:152-165, acceptance.cpp:94-118."""
+    oscene, dev = scene_pair(port, ctx, 41, 1000, "slab", 2, 640, 480, 500.0)
+    cam = to_gpu_cam(oscene.cameras[0])
+    a = ctx.render(dev, cam, gpu_cfg("ellipse"))
+    b = ctx.render(dev, cam, gpu_cfg("adagscale", 0.0), capi.make_lut())
+    assert a["pair_count"] == b["pair_count"] and a["splat_count"] == b["splat_count"]
+    assert np.array_equal(a["image"], b["image"])
+
+
+def test_lossless_modes_agree_bitwise(ctx, port):
+    """test_rasterizer.cpp:133-150: AABB, OBB and Ellipse render identical images."""
+    for layout in ("slab", "aniso"):
+        oscene, dev = scene_pair(port, ctx, 37, 1200, layout, 2, 640, 480, 500.0)
+        cam = to_gpu_cam(oscene.cameras[1])
+        imgs = [ctx.render(dev, cam, gpu_cfg(m, exact=False)) for m in ("aabb", "obb", "ellipse")]
+        assert np.array_equal(imgs[0]["image"], imgs[1]["image"])
+        assert np.array_equal(imgs[1]["image"], imgs[2]["image"])
+        assert imgs[2]["pair_count"] <= imgs[1]["pair_count"] <= imgs[0]["pair_count"]
+
+
+def test_pair_budget_error(ctx, port):
+    oscene, dev = scene_pair(port, ctx, 5, 3000, "slab", 2, 320, 240, 250.0)
+    cam = to_gpu_cam(oscene.cameras[0])
+    with pytest.raises(capi.PairBudgetError):
+        ctx.render(dev, cam, gpu_cfg("ellipse", pair_budget=4))
+    # the context stays usable
+    out = ctx.render(dev, cam, gpu_cfg("ellipse"))
+    assert out["pair_count"] > 4
+
+
+def test_invalid_config_and_camera(ctx, port):
+    oscene, dev = scene_pair(port, ctx, 5, 100, "slab", 2, 64, 48, 100.0)
+    cam = to_gpu_cam(oscene.cameras[0])
+    with pytest.raises(capi.AgsxError) as e:
+        ctx.render(dev, cam, gpu_cfg("ellipse", alpha_threshold=2.0))
+    assert e.value.code == capi.EINVAL
+    with pytest.raises(capi.AgsxError) as e:
+        ctx.render(dev, cam, gpu_cfg("adagscale"), None)  # adagscale needs a LUT
+    assert e.value.code == capi.EINVAL
+    bad = to_gpu_cam(oscene.cameras[0])
+    bad.rotation[0] = 2.0
+    with pytest.raises(capi.AgsxError):
+        ctx.render(dev, bad, gpu_cfg("ellipse"))
+
+
+def test_empty_scene_renders_background(ctx):
+    """test_rasterizer.cpp:97-114."""
+    dev = ctx.upload(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 4)), np.zeros(0), np.zeros((0, 1, 3)))
+    cam = capi.Camera()
+    cam.rotation[:] = [1, 0, 0, 0, 1, 0, 0, 0, 1]
+    cam.fx = cam.fy = 100.0
+    cam.width, cam.height = 64, 48
+    out = ctx.render(dev, cam, gpu_cfg("ellipse", background=(0.1, 0.2, 0.3)))
+    assert out["pair_count"] == 0 and out["splat_count"] == 0
+    assert out["image"][10, 10, 0] == np.float32(0.1)
+    assert out["image"][47, 63, 2] == np.float32(0.3)
+
+
+def test_max_t_matches_oracle(ctx, port, ref):
+    """test_rasterizer.cpp:180-219: max transmittance instrumentation, exact."""
+    oscene, dev = scene_pair(port, ctx, 47, 400, "slab", 2, 640, 480, 500.0)
+    ocam = oscene.cameras[0]
+    rscene = ref.synth_scene(47, 400, "slab", cameras=2)
+    want = ref.render(rscene, rscene.cameras[0], ref.config("ellipse"), max_t=True)
+    out = ctx.render(dev, to_gpu_cam(ocam), gpu_cfg("ellipse", exact=True), max_t=True, n=400)
+    _, alive = ctx.dump_tile_counts(400)
+    got = out["max_t_by_gid"][alive]
+    assert np.array_equal(got.view(np.uint32), want["max_t"].view(np.uint32))
+
+
+# --------------------------------------------------------------------------- stage API
+def splat(mean, cov, opacity, th, depth=5.0, rgb=(1, 1, 1)):
+    s = np.zeros(1, capi.SPLAT_DTYPE)
+    s["mean2d"] = mean
+    s["cov2d"] = cov
+    det = np.float32(cov[0]) * np.float32(cov[2]) - np.float32(cov[1]) * np.float32(cov[1])
+    inv = np.float32(1.0) / np.float32(det)
+    s["inv_cov"] = [np.float32(cov[2]) * inv, -np.float32(cov[1]) * inv, np.float32(cov[0]) * inv]
+    s["depth"] = depth
+    s["rgb"] = rgb
+    s["opacity"] = opacity
+    s["th"] = th
+    return s
+
+
+def test_one_tile_splat_all_modes(ctx):
+    """test_pair_gen.cpp:55-66."""
+    s = splat((24, 24), (4, 0, 4), 0.99, 1 / 255)
+    for m in ("aabb", "obb", "ellipse", "adagscale"):
+        keys, idx, counts = ctx.generate_pairs(s, 64, 64, m, gpu_cfg(m))
+        assert list(counts) == [1]
+        assert keys[0] >> 32 == 1 * 4 + 1
+
+
+def test_five_tile_splat(ctx):
+    """test_pair_gen.cpp:205-225: tiles 298..302 in emission order."""
+    s = splat((328, 120), (81, 0, 2.25), 0.99, 1 / 255)
+    keys, idx, counts = ctx.generate_pairs(s, 640, 480, "ellipse", gpu_cfg("ellipse"))
+    assert list(counts) == [5]
+    assert [int(k >> 32) for k in keys] == [298, 299, 300, 301, 302]
+    assert all((k & 0xFFFFFFFF) == 0x40A00000 for k in keys)  # bits of depth 5.0
+    with pytest.raises(capi.PairBudgetError):
+        ctx.generate_pairs(s, 640, 480, "ellipse", gpu_cfg("ellipse", pair_budget=4))
+
+
+def test_offscreen_and_empty(ctx):
+    """test_pair_gen.cpp:227-237."""
+    keys, idx, counts = ctx.generate_pairs(np.zeros(0, capi.SPLAT_DTYPE), 64, 64, "ellipse", gpu_cfg("ellipse"))
+    assert len(keys) == 0
+    s = splat((-500, -500), (4, 0, 4), 0.9, 1 / 255)
+    keys, idx, counts = ctx.generate_pairs(s, 64, 64, "ellipse", gpu_cfg("ellipse"))
+    assert list(counts) == [0]
+
+
+def test_generate_pairs_random_splats_vs_oracle(ctx, port):
+    """Random splats incl. off-image centres (test_pair_gen.cpp:117-144 distribution)."""
+    rng = np.random.default_rng(21)
+    n = 3000
+    a, b, c, d = (rng.uniform(-20, 20, n).astype(np.float32) for _ in range(4))
+    s = np.zeros(n, capi.SPLAT_DTYPE)
+    cov = np.stack([a * a + b * b + np.float32(0.4), a * c + b * d, c * c + d * d + np.float32(0.4)], 1).astype(np.float32)
+    det = cov[:, 0] * cov[:, 2] - cov[:, 1] * cov[:, 1]
+    inv = np.float32(1) / det
+    s["cov2d"] = cov
+    s["inv_cov"] = np.stack([cov[:, 2] * inv, -cov[:, 1] * inv, cov[:, 0] * inv], 1)
+    s["mean2d"] = np.stack([rng.uniform(-50, 690, n), rng.uniform(-50, 530, n)], 1)
+    op = rng.uniform(0.05, 0.99, n).astype(np.float32)
+    s["opacity"] = op
+    s["th"] = np.maximum(np.minimum(op * rng.uniform(0.1, 0.9, n).astype(np.float32), op - np.float32(1e-4)),
+                         np.float32(1 / 255))
+    s["depth"] = rng.uniform(0.3, 90, n)
+    for m in ("aabb", "obb", "ellipse", "adagscale"):
+        ok = port.generate_pairs(s, 640, 480, m, port.config(m))
+        gk = ctx.generate_pairs(s, 640, 480, m, gpu_cfg(m))
+        for x, y in zip(gk, ok):
+            assert np.array_equal(x, y), m
+
+
+def test_sort_matches_stable_sort(ctx):
+    """test_pair_sort.cpp:31-52 (1e5, coarse depths -> many equal keys) and acceptance C7 (1e6)."""
+    for n, tiles, seed in ((100_000, 300, 17), (1_000_000, 62_208, 515)):
+        rng = np.random.default_rng(seed)
+        depth = (0.25 * (1 + rng.integers(0, 64, n))).astype(np.float32)
+        keys = (rng.integers(0, tiles, n).astype(np.uint64) << np.uint64(32)) | depth.view(np.uint32).astype(np.uint64)
+        idx = np.arange(n, dtype=np.uint32)
+        order = np.argsort(keys, kind="stable")
+        gk, gi, gr = ctx.sort_pairs(keys, idx, tiles)
+        assert np.array_equal(gk, keys[order])
+        assert np.array_equal(gi, idx[order])
+        t = (gk >> np.uint64(32)).astype(np.int64)
+        for tile in (0, tiles // 2, tiles - 1):
+            hit = np.nonzero(t == tile)[0]
+            want = (hit[0], hit[-1] + 1) if len(hit) else (0, 0)
+            assert tuple(gr[tile]) == want
+
+
+def test_sort_edge_cases(ctx):
+    """test_pair_sort.cpp:12-29, 94-103."""
+    gk, gi, gr = ctx.sort_pairs(np.zeros(0, np.uint64), np.zeros(0, np.uint32), 12)
+    assert len(gk) == 0 and np.all(gr == 0)
+    k = np.array([(4 << 32) | 0x40000000, (4 << 32) | 0x3F800000], np.uint64)
+    gk, gi, gr = ctx.sort_pairs(k, np.array([0, 1], np.uint32), 8)
+    assert list(gi) == [1, 0] and tuple(gr[4]) == (0, 2) and tuple(gr[3]) == (0, 0)
+    keys = np.array([(7 << 32) | 0x40500000] * 64 + [(2 << 32) | 0x41100000], np.uint64)
+    idx = np.array(list(range(64)) + [999], np.uint32)
+    gk, gi, gr = ctx.sort_pairs(keys, idx, 16)
+    assert gi[0] == 999 and list(gi[1:]) == list(range(64))
+    # arbitrary 64-bit keys, tiles past tile_count are sorted but get no range
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 2**63, 50_000, dtype=np.uint64)
+    gk, gi, gr = ctx.sort_pairs(keys, np.arange(50_000, dtype=np.uint32), 4)
+    assert np.array_equal(gk, np.sort(keys, kind="stable"))
+
+
+def test_raster_known_answers(ctx, port):
+    """test_rasterizer.cpp:60-95."""
+    def flat(mean, sigma, op, rgb, depth):
+        return splat(mean, (sigma * sigma, 0, sigma * sigma), op, 1 / 255, depth, rgb)
+
+    def raster(splats, w, h, cfg):
+        keys, idx, counts = ctx.generate_pairs(splats, w, h, "ellipse", cfg)
+        tiles = ((w + 15) // 16) * ((h + 15) // 16)
+        sk, si, rg = ctx.sort_pairs(keys, idx, tiles)
+        return ctx.raster(splats, si, rg, w, h, cfg)
+
+    img = raster(flat((8, 8), 1e4, 0.5, (1, 1, 1), 1.0), 16, 16, gpu_cfg("ellipse", exact=True))
+    assert abs(img[8, 8, 0] - 0.5) < 1e-4 and abs(img[12, 3, 1] - 0.5) < 1e-4
+    two = np.concatenate([flat((8, 8), 1e4, 0.5, (1, 1, 1), 1.0), flat((8, 8), 1e4, 0.5, (0, 0, 0), 2.0)])
+    img = raster(two, 16, 16, gpu_cfg("ellipse", exact=True, background=(1, 1, 1)))
+    assert abs(img[8, 8, 0] - 0.75) < 1e-4
+    img = raster(flat((8, 8), 1e4, 0.001, (1, 1, 1), 1.0), 16, 16,
+                 gpu_cfg("ellipse", exact=True, background=(0.25, 0.5, 0.75)))
+    assert img[8, 8, 0] == np.float32(0.25) and img[8, 8, 1] == np.float32(0.5) and img[8, 8, 2] == np.float32(0.75)
+
+
+def test_stage_preprocess_matches_oracle(ctx, port):
+    oscene, dev = scene_pair(port, ctx, 2, 3000, "ramp", 2, 640, 480, 500.0)
+    for mode, k, bins in (("ellipse", 0.0, None), ("adagscale", 0.5, [0.7] * 20)):
+        ocfg = port.config(mode, k=k)
+        want = port.preprocess(oscene, oscene.cameras[0], ocfg, port.lut(bins) if bins else None)
+        got = ctx.preprocess_view(dev, to_gpu_cam(oscene.cameras[0]), gpu_cfg(mode, k),
+                                  capi.make_lut(bins) if bins else None)
+        assert got.tobytes() == want.tobytes()
+
+
+# --------------------------------------------------------------------------- device libm
+def test_device_logf_matches_host_glibc(ctx, port):
+    """glibc-exact logf on device over every float in [1, 256) and samples elsewhere."""
+    bits = np.arange(0x3F800000, 0x43800000, dtype=np.uint32)
+    x = bits.view(np.float32)
+    assert np.array_equal(ctx.logf(x).view(np.uint32), port.logf(x).view(np.uint32))
+    rng = np.random.default_rng(0)
+    x = rng.integers(1, 0x7F800000, 4_000_000, dtype=np.uint32).view(np.float32)
+    assert np.array_equal(ctx.logf(x).view(np.uint32), port.logf(x).view(np.uint32))
+
+
+def test_device_expf_matches_host_glibc(ctx, port):
+    """glibc-exact expf on device over every float in [-20, -0] and samples down to -110."""
+    bits = np.arange(0x80000000, 0xC1A00001, dtype=np.uint32)
+    for chunk in np.array_split(bits, 8):
+        x = chunk.view(np.float32)
+        assert np.array_equal(ctx.expf(x).view(np.uint32), port.expf(x).view(np.uint32))
+    x = np.linspace(-110, 88, 3_000_000, dtype=np.float32)
+    assert np.array_equal(ctx.expf(x).view(np.uint32), port.expf(x).view(np.uint32))
