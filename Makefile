@@ -11,7 +11,9 @@ CSRC     := $(PKG)/csrc
 LIBDIR   := $(PKG)/lib
 PYTHON   ?= python3
 NVCC     ?= /usr/local/cuda/bin/nvcc
-CXX      ?= g++
+# The image default $CXX (/opt/gcc wrapper) links libstdc++ statically; every shared
+# object loaded into one Python process must use the system libstdc++.so.
+CXX      := $(shell command -v /usr/bin/g++ || echo g++)
 CUDA_INC := /usr/local/cuda/include
 CUDA_LIB := /usr/local/cuda/lib64
 

@@ -1,0 +1,423 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 AdaGScale render path (BASELINE.json metric).
+
+Workload (N=1): BASELINE config 3 -- synthetic `veil` scene, 3M Gaussians,
+4608x3456, view 0, AdaGScale on with the reference-calibrated LUT and K scaled
+to the resolution.  One step = one frame (preprocess ->
+pair generation -> sort -> rasterize) with the scene resident in HBM.
+N>1 (torchrun): view-partitioned replicas, rank r renders view r of the
+camera path each step (weak scaling); no collective on the data path, only a
+max-over-ranks of the timed region and a sum of the frame counts.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref, built from the reference sources) on the
+host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FPS at 4608x3456, 3M Gaussians; tile pairs/frame; PSNR vs CPU ref"
+K1080 = 0.3985099792480469
+LUT_BINS = [1.0] * 20
+LUT_BINS[7] = 0.003038157941773534
+LUT_BINS[8] = 0.007012989837676287
+
+CONFIGS = {
+    # name: (gaussians, width, height, camera_count)
+    "1": (100_000, 1920, 1080, 16),
+    "2": (1_000_000, 4608, 3456, 16),
+    "3": (3_000_000, 4608, 3456, 16),
+    "4": (3_000_000, 3660, 3200, 16),
+    "5": (6_000_000, 4608, 3456, 64),
+}
+
+
+def scaled_k(width: int) -> float:
+    f = 500.0 * width / 640.0
+    return float(np.float32(K1080 * (f / 1500.0) ** 2))
+
+
+def workload_name(cfg: str, mode: str) -> str:
+    n, w, h, _ = CONFIGS[cfg]
+    return f"config{cfg}: synthetic veil {n} Gaussians, {w}x{h}, {mode}" + (
+        f" (K={scaled_k(w):.4f}, calibrated LUT)" if mode == "adagscale" else ""
+    )
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------ algorithmic bytes
+def stage_bytes(n, s, p, p_it, tiles, px):
+    """Algorithmic bytes per frame, SURVEY.md §8(d) (d = 1 SH coefficient)."""
+    return {
+        "preprocess": n * (44 + 12) + 4 * n + 44 * s,
+        "pair_gen": 8 * n + 28 * s + 12 * p,
+        "sort": 160 * p + 8 * tiles,
+        "raster": 40 * p_it + 8 * tiles + 12 * px,
+    }
+
+
+# ---------------------------------------------------------- reference arm
+def cpu_reference(cfg: str, mode: str, frames: int, warmup: int, want_image=False):
+    """The reference CPU render (oracle/_ref, unmodified reference sources)."""
+    from oracle.ffi import Oracle, available
+
+    kind = "reference" if available("reference") else "port"
+    o = Oracle(kind)
+    n, w, h, cams = CONFIGS[cfg]
+    f = 500.0 * w / 640.0
+    scene = o.synth_scene(1, n, "veil", cameras=cams, width=w, height=h, focal=f)
+    threads = os.cpu_count() or 1
+    c = o.config(mode, k=scaled_k(w) if mode == "adagscale" else 0.0, thread_count=threads)
+    lut = o.lut(LUT_BINS) if mode == "adagscale" else None
+    times, out = [], None
+    for i in range(warmup + frames):
+        out = o.render(scene, scene.cameras[0], c, lut)
+        if i >= warmup:
+            times.append(sum(out["stage_times"].values()) if kind == "reference" else None)
+    return kind, threads, times, out
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return
+    mode = args.mode
+    t0 = time.perf_counter()
+    kind, threads, times, out = cpu_reference(args.config, mode, args.steps, args.warmup)
+    wall = time.perf_counter() - t0
+    frame_s = sum(times) / len(times) if times and times[0] is not None else wall / (args.steps + args.warmup)
+    fps = 1.0 / frame_s
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": fps,
+        "unit": "frames/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": frame_s * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (reference synth_scene, seed 1)",
+        "config": {"workload": workload_name(args.config, mode), "mode": mode,
+                   "pair_count": out["pair_count"], "splat_count": out["splat_count"]},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": kind,
+                         "sample": f"{args.steps} full frames of config {args.config} after {args.warmup} "
+                                   f"warm-up, stage_times summed (reference render() on {threads} threads)"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "stage_times_s": out["stage_times"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    os.environ["AGS_DEVICE"] = str(local_rank)  # device of the module-level render()
+    import torch
+    import paper_2604_18980_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    mode = args.mode
+    n, w, h, cams = CONFIGS[args.config]
+    focal = 500.0 * w / 640.0
+    k = scaled_k(w) if mode == "adagscale" else 0.0
+    bins = LUT_BINS if mode == "adagscale" else []
+    scene = P.synth_scene(1, n, "veil", cameras=cams, width=w, height=h, focal=focal)
+    view = rank % scene.camera_count
+    r = P.Renderer(local_rank)
+    r.upload(scene)
+    stream = torch.cuda.ExternalStream(r.stream, device=torch.device("cuda", local_rank))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (also sizes the pair arena)
+    for _ in range(max(args.warmup, 3)):
+        r.render_async(scene, view, mode, k, bins, exact=args.exact)
+    r.wait()
+    stats = r.frame_stats()
+    launches0 = r.kernel_launches
+
+    # timed region: K frames back to back on the renderer's stream
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        r.render_async(scene, view, mode, k, bins, exact=args.exact)
+    ev1.record(stream)
+    r.wait()
+    barrier()
+    clocks = sampler.stop()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    launches = r.kernel_launches - launches0
+    hist = r.stage_history(min(args.steps, 64))
+    stats = r.frame_stats()
+
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    frames = torch.tensor([args.steps], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(frames, op=dist.ReduceOp.SUM)
+    max_ms = float(t.item())
+    total_frames = float(frames.item())
+    fps = total_frames / (max_ms * 1e-3)
+
+    # ---- end to end through the public API (host image out, per step) ----
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(2):
+            P.render(scene, view, mode, k, bins, exact=args.exact)
+        barrier()
+        steps_e2e = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(steps_e2e):
+            out = P.render(scene, view, mode, k, bins, exact=args.exact)
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / steps_e2e
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        from paper_2604_18980_b200 import capi
+
+        h2d = ctypes.sizeof(capi.Camera) + ctypes.sizeof(capi.Config) + 4 * len(bins)
+        e2e = {"value": world / float(tt.item()), "unit": "frames/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": int(out["image"].nbytes) + 128,
+               "api": "paper_2604_18980_b200.render(scene, view, ...) -> host numpy image (scene resident)"}
+
+    # ---- AdaGScale off, same scene (pairs + FPS) --------------------------
+    off = None
+    if mode == "adagscale" and not args.no_off:
+        for _ in range(3):
+            r.render_async(scene, view, "ellipse", 0.0, [], exact=args.exact)
+        r.wait()
+        steps_off = max(3, min(args.steps, 20))
+        barrier()
+        ev0.record(stream)
+        for _ in range(steps_off):
+            r.render_async(scene, view, "ellipse", 0.0, [], exact=args.exact)
+        ev1.record(stream)
+        r.wait()
+        barrier()
+        off_stats = r.frame_stats()
+        off = {"fps_per_gpu": steps_off / (ev0.elapsed_time(ev1) * 1e-3), "pair_count": off_stats["pair_count"],
+               "splat_count": off_stats["splat_count"]}
+        # restore the on-frame state for the image comparison below
+        r.render_async(scene, view, mode, k, bins, exact=args.exact)
+        r.wait()
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- per-stage roofline from the live stage events --------------------
+    peaks = measured_peaks()
+    stage_ms = hist.mean(axis=0) if len(hist) else np.zeros(4)
+    tiles = stats["tiles"]
+    sb = stage_bytes(n, stats["splat_count"], stats["pair_count"], stats["p_it"], tiles, w * h)
+    names = ("preprocess", "pair_gen", "sort", "raster")
+    stages = {}
+    for i, nm in enumerate(names):
+        gbs = sb[nm] / (stage_ms[i] * 1e-3) / 1e9 if stage_ms[i] > 0 else 0.0
+        stages[nm] = {"ms": float(stage_ms[i]), "algorithmic_bytes": int(sb[nm]), "achieved_gbs": gbs,
+                      "frac_hbm": gbs / peaks["hbm_gbs"]}
+    stages["sort"]["keys_per_s"] = stats["pair_count"] / (stage_ms[2] * 1e-3) if stage_ms[2] else 0.0
+    stages["pair_gen"]["pairs_per_s"] = stats["pair_count"] / (stage_ms[1] * 1e-3) if stage_ms[1] else 0.0
+    dom = int(np.argmax(stage_ms))
+    roofline = {
+        "bound": "hbm",
+        "kernel": names[dom],
+        "achieved": stages[names[dom]]["achieved_gbs"],
+        "peak": peaks["hbm_gbs"],
+        "unit": "GB/s",
+        "frac": stages[names[dom]]["frac_hbm"],
+        "traffic": None,
+        "peak_src": peaks["src"],
+        "algorithmic_bytes_per_launch": stages[names[dom]]["algorithmic_bytes"],
+        "note": "raster is issue-bound (SURVEY §8(d)); HBM fraction reported as asked",
+    }
+
+    # ---- CPU baseline (reference render on host cores) + PSNR vs CPU ref ---
+    cpu = None
+    quality = None
+    if not args.no_cpu and world == 1:
+        kind, threads, times, ref_out = cpu_reference(args.config, mode, args.cpu_frames, 0)
+        if times and times[0] is not None:
+            cpu_fps = 1.0 / (sum(times) / len(times))
+        else:
+            cpu_fps = None
+        cpu = {"value": cpu_fps, "unit": "frames/s", "cores": threads, "kind": kind,
+               "sample": f"{args.cpu_frames} full frame(s) of the same workload (view 0), reference "
+                         f"render() stage_times summed, {threads} threads"}
+        img = P.render(scene, 0, mode, k, bins, exact=args.exact)["image"]
+        ref_img = ref_out["image"]
+        d = img.astype(np.float64) - ref_img.astype(np.float64)
+        mse = float(np.mean(d * d))
+        quality = {"psnr_vs_cpu_ref_db": (float("inf") if mse == 0 else 10 * np.log10(1 / mse)),
+                   "max_abs_vs_cpu_ref": float(np.max(np.abs(d))),
+                   "bit_exact_image": bool(mse == 0),
+                   "pair_count_equal": ref_out["pair_count"] == stats["pair_count"],
+                   "splat_count_equal": ref_out["splat_count"] == stats["splat_count"]}
+
+    line = {
+        "metric": METRIC,
+        "value": fps,
+        "unit": "frames/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": max_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (veil layout, seed 1, host synth_scene byte-identical to the reference)",
+        "config": {
+            "workload": workload_name(args.config, mode),
+            "gaussians": n, "width": w, "height": h, "mode": mode, "view_per_rank": "rank r renders view r",
+            "parallelism": f"view-partitioned replicas x{world}",
+            "l2": "inputs larger than L2 (scene 168 MB + image 191 MB per frame)",
+            "alpha": "exact glibc expf" if args.exact else "MUFU.EX2 + exact guard band",
+        },
+        "pairs_per_frame": stats["pair_count"],
+        "splats_per_frame": stats["splat_count"],
+        "p_it": stats["p_it"],
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "roofline": roofline,
+        "stages": stages,
+        "cpu_baseline": cpu,
+        "quality": quality,
+        "adagscale_off": off,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
+    ap.add_argument("--mode", default="adagscale", choices=["adagscale", "ellipse", "aabb", "obb"])
+    ap.add_argument("--exact", action="store_true", help="glibc-exact alpha (bit-identical images)")
+    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-off", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

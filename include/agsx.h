@@ -154,6 +154,16 @@ int agsx_render_async(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera*
                       const agsx_config* cfg, const agsx_lut* lut);
 int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out);
 
+/* Device-timed stage durations (ms: preprocess, pair_gen, sort, raster) of
+ * the last min(max_frames, 64) frames enqueued on this ctx, oldest first;
+ * synchronises the stream. */
+int agsx_stage_history(agsx_ctx* ctx, float* stage_ms, int32_t max_frames, int32_t* out_frames);
+
+/* Counters of the most recent frame: {splat_count (survivors), splats with
+ * >= 1 tile, pair_count, P_it (pairs iterated before tile saturation, the
+ * rasterizer's work unit), overflow flag, tile count}; synchronises. */
+int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n);
+
 /* Device pointer to the ctx-owned image of the most recent frame
  * (H*W*3 f32, HWC) and its dimensions. */
 int agsx_device_image(agsx_ctx* ctx, float** dptr, int32_t* width, int32_t* height);

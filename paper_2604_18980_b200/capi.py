@@ -26,7 +26,8 @@ EXPORTS = (
     "agsx_render_async", "agsx_render_wait", "agsx_device_image", "agsx_dump_tile_counts",
     "agsx_dump_sorted_pairs", "agsx_dump_ranges", "agsx_preprocess_view",
     "agsx_generate_pairs", "agsx_sort_pairs", "agsx_raster", "agsx_device_logf",
-    "agsx_device_expf", "agsx_kernel_launches",
+    "agsx_device_expf", "agsx_kernel_launches", "agsx_stage_history",
+    "agsx_frame_stats",
 )
 
 SPLAT_DTYPE = np.dtype(
@@ -193,6 +194,8 @@ class Lib:
         L.agsx_raster.argtypes = [vp, vp, u64, vp, u64, vp, i32, i32, C.POINTER(Config), vp, vp]
         L.agsx_device_logf.argtypes = [vp, vp, vp, u64]
         L.agsx_device_expf.argtypes = [vp, vp, vp, u64]
+        L.agsx_stage_history.argtypes = [vp, vp, i32, C.POINTER(i32)]
+        L.agsx_frame_stats.argtypes = [vp, vp, i32]
         L.agsx_kernel_launches.argtypes = [vp]
         L.agsx_kernel_launches.restype = u64
 
@@ -275,6 +278,18 @@ class Context:
         f = Frame()
         self._check(self.L.agsx_render_wait(self.h, C.byref(f)))
         return {"pair_count": f.pair_count, "splat_count": f.splat_count, "stage_ms": list(f.stage_ms)}
+
+    def stage_history(self, max_frames=64):
+        ms = np.zeros((max_frames, 4), np.float32)
+        n = C.c_int32()
+        self._check(self.L.agsx_stage_history(self.h, _p(ms), max_frames, C.byref(n)))
+        return ms[: n.value]
+
+    def frame_stats(self):
+        v = np.zeros(6, np.uint64)
+        self._check(self.L.agsx_frame_stats(self.h, _p(v), 6))
+        return dict(zip(("splat_count", "splats_with_tiles", "pair_count", "p_it", "overflow", "tiles"),
+                        (int(x) for x in v)))
 
     def device_image(self):
         p = C.c_void_p()

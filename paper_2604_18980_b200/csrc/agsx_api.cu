@@ -82,7 +82,10 @@ struct agsx_ctx {
     uint64_t pair_capacity = 0;
 
     Counters* h_ctr = nullptr;  // pinned
-    cudaEvent_t ev[6] = {};
+    static constexpr int kRing = 64;  // frames of stage events kept for timing
+    cudaEvent_t ev_ring[kRing][6] = {};
+    cudaEvent_t* ev = ev_ring[0];
+    uint64_t frames = 0;
 
     // most recent fused frame
     bool have_frame = false;
@@ -241,12 +244,12 @@ int raster_ppt(int tile_size) {
 
 void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
                    const float4* P0, const float4* P1, const float4* P2, float* image,
-                   uint32_t* maxt) {
+                   uint32_t* maxt, unsigned long long* pit) {
     const int grid = p.tiles_x * p.tiles_y;
     if (grid == 0) return;
     const bool exact = (p.flags & AGSX_FLAG_EXACT_ALPHA) != 0;
     launch_raster_kernel(raster_ppt(p.tile_size), exact, maxt != nullptr, grid, ctx->stream, p, ranges, vals,
-                         P0, P1, P2, image, maxt);
+                         P0, P1, P2, image, maxt, pit);
     check_launch(ctx);
 }
 
@@ -348,6 +351,8 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     uint32_t* hist_depth = reinterpret_cast<uint32_t*>(ctr + 1);
     uint32_t* hist_tile = hist_depth + 8 * 256;
     cudaStream_t st = ctx->stream;
+    ctx->ev = ctx->ev_ring[ctx->frames % agsx_ctx::kRing];
+    ++ctx->frames;
 
     AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
     AGSX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters) + 2 * 8 * 256 * 4, st));
@@ -402,7 +407,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
     // K6
     launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ptr<float>(ctx->image),
-                  maxt ? ptr<uint32_t>(ctx->maxt) : nullptr);
+                  maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, &ctr->p_it);
     AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
     AGSX_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     ctx->f_tkeys = tk[cur];
@@ -497,7 +502,8 @@ int agsx_create(int device, agsx_ctx** out) {
         ctx->occ_sort32 = std::max(ctx->occ_sort32, 1);
         ctx->occ_sort64 = std::max(ctx->occ_sort64, 1);
         ctx->occ_emit = std::max(ctx->occ_emit, 1);
-        for (auto& e : ctx->ev) AGSX_CUDA(cudaEventCreate(&e));
+        for (auto& set : ctx->ev_ring)
+            for (auto& e : set) AGSX_CUDA(cudaEventCreate(&e));
         AGSX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ctr), sizeof(Counters)));
         std::memset(ctx->h_ctr, 0, sizeof(Counters));
         return AGSX_OK;
@@ -521,8 +527,9 @@ void agsx_destroy(agsx_ctx* ctx) {
                    &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
                    &ctx->tmp3, &ctx->tmp4})
         release(*b);
-    for (auto& e : ctx->ev)
-        if (e) cudaEventDestroy(e);
+    for (auto& set : ctx->ev_ring)
+        for (auto& e : set)
+            if (e) cudaEventDestroy(e);
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -628,6 +635,39 @@ int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
                                       ctx->stream));
         }
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return AGSX_OK;
+    });
+}
+
+int agsx_stage_history(agsx_ctx* ctx, float* stage_ms, int32_t max_frames, int32_t* out_frames) {
+    if (!ctx || !stage_ms || !out_frames) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        const uint64_t avail = std::min<uint64_t>(ctx->frames, agsx_ctx::kRing);
+        const int n = static_cast<int>(std::min<uint64_t>(avail, static_cast<uint64_t>(std::max(max_frames, 0))));
+        for (int i = 0; i < n; ++i) {
+            // oldest first among the last n frames
+            const uint64_t f = ctx->frames - n + i;
+            cudaEvent_t* e = ctx->ev_ring[f % agsx_ctx::kRing];
+            float ms[5];
+            for (int k = 0; k < 5; ++k) AGSX_CUDA(cudaEventElapsedTime(&ms[k], e[k], e[k + 1]));
+            stage_ms[4 * i + 0] = ms[0];
+            stage_ms[4 * i + 1] = ms[2];
+            stage_ms[4 * i + 2] = ms[1] + ms[3];
+            stage_ms[4 * i + 3] = ms[4];
+        }
+        *out_frames = n;
+        return AGSX_OK;
+    });
+}
+
+int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n) {
+    if (!ctx || !stats) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        const Counters c = *ctx->h_ctr;
+        const uint64_t v[6] = {c.s, c.m, c.p, c.p_it, c.overflow, static_cast<uint64_t>(ctx->f_tile_count)};
+        for (int i = 0; i < n && i < 6; ++i) stats[i] = v[i];
         return AGSX_OK;
     });
 }
@@ -903,7 +943,7 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
         AGSX_CUDA(cudaMemcpyAsync(ctx->tmp4.p, ranges, tiles * 8, cudaMemcpyHostToDevice, st));
         if (max_t) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, std::max<uint64_t>(n_splats, 1) * 4, st));
         launch_raster(ctx, p, ptr<uint2>(ctx->tmp4), ptr<uint32_t>(ctx->tmp3), pl.p0, pl.p1, pl.p2,
-                      ptr<float>(ctx->image), max_t ? ptr<uint32_t>(ctx->maxt) : nullptr);
+                      ptr<float>(ctx->image), max_t ? ptr<uint32_t>(ctx->maxt) : nullptr, nullptr);
         AGSX_CUDA(cudaMemcpyAsync(image, ctx->image.p, static_cast<size_t>(width) * height * 12,
                                   cudaMemcpyDeviceToHost, st));
         if (max_t && n_splats)

@@ -344,7 +344,9 @@ struct Counters {
     uint32_t p;             // total pairs (saturating)
     uint32_t overflow;      // pair buffer capacity exceeded
     uint32_t p_eff;         // p if it fits the pair buffers, else 0 (memory safety)
-    uint32_t pad[11];
+    uint32_t pad0;
+    unsigned long long p_it;  // pairs iterated before tile saturation (raster work)
+    uint32_t pad[8];
 };
 
 }  // namespace agsx

@@ -101,17 +101,18 @@ __device__ __forceinline__ float glibc_expf(float x) {
         if (x < -0x1.9fe368p6f) return 0.0f;
     }
     const double xd = static_cast<double>(x);
-    const double z = 0x1.71547652b82fep+5 * xd;
-    double kd = z + 0x1.8p+52;
+    // glibc is built with FMA on x86-64 (IFUNC variant): r = fma(InvLn2N, x, -kd) etc.;
+    // verified over all 2^32 floats against the host libm (tests/test_device_libm.py).
+    double kd = fma(0x1.71547652b82fep+5, xd, 0x1.8p+52);
     const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
     kd -= 0x1.8p+52;
-    const double r = z - kd;
+    const double r = fma(0x1.71547652b82fep+5, xd, -kd);
     const uint64_t t = kExp2fTab[ki % 32] + (ki << 47);
     const double s = __longlong_as_double(static_cast<long long>(t));
-    const double zz = 0x1.c6af84b912394p-20 * r + 0x1.ebfce50fac4f3p-13;
+    const double zz = fma(0x1.c6af84b912394p-20, r, 0x1.ebfce50fac4f3p-13);
     const double r2 = r * r;
-    double y = 0x1.62e42ff0c52d6p-6 * r + 1.0;
-    y = zz * r2 + y;
+    double y = fma(0x1.62e42ff0c52d6p-6, r, 1.0);
+    y = fma(zz, r2, y);
     y = y * s;
     return static_cast<float>(y);
 }

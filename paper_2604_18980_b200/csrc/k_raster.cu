@@ -43,17 +43,18 @@ __device__ __forceinline__ float glibc_expf_smem(float x, const uint64_t* tab) {
         if (x < -0x1.9fe368p6f) return 0.0f;
     }
     const double xd = static_cast<double>(x);
-    const double z = 0x1.71547652b82fep+5 * xd;
-    double kd = z + 0x1.8p+52;
+    // glibc is built with FMA on x86-64 (IFUNC variant): r = fma(InvLn2N, x, -kd) etc.;
+    // verified over all 2^32 floats against the host libm (tests/test_device_libm.py).
+    double kd = fma(0x1.71547652b82fep+5, xd, 0x1.8p+52);
     const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
     kd -= 0x1.8p+52;
-    const double r = z - kd;
+    const double r = fma(0x1.71547652b82fep+5, xd, -kd);
     const uint64_t t = tab[ki % 32] + (ki << 47);
     const double s = __longlong_as_double(static_cast<long long>(t));
-    const double zz = 0x1.c6af84b912394p-20 * r + 0x1.ebfce50fac4f3p-13;
+    const double zz = fma(0x1.c6af84b912394p-20, r, 0x1.ebfce50fac4f3p-13);
     const double r2 = r * r;
-    double y = 0x1.62e42ff0c52d6p-6 * r + 1.0;
-    y = zz * r2 + y;
+    double y = fma(0x1.62e42ff0c52d6p-6, r, 1.0);
+    y = fma(zz, r2, y);
     y = y * s;
     return static_cast<float>(y);
 }
@@ -67,7 +68,7 @@ template <int PPT, bool EXACT, bool MAXT>
 __global__ void __launch_bounds__(256)
 k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
          const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
-         float* __restrict__ image, uint32_t* __restrict__ maxt) {
+         float* __restrict__ image, uint32_t* __restrict__ maxt, unsigned long long* __restrict__ pit) {
     constexpr int B = 256;
     __shared__ __align__(16) float4 sA[2][B];
     __shared__ __align__(16) float4 sB[2][B];
@@ -75,9 +76,11 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
     __shared__ uint32_t sG[MAXT ? 2 : 1][MAXT ? B : 1];
     __shared__ uint64_t sTab[32];
     __shared__ __align__(16) float sOut[PPT == 1 ? 16 * 16 * 3 : 4];
+    __shared__ uint32_t sPit;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < 32) sTab[tid] = kExp2fTab[tid];
+    if (tid == 0) sPit = 0;
 
     const int tile = blockIdx.x;
     const int ts = p.tile_size;
@@ -90,6 +93,7 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
     int lx[PPT], ly[PPT];
     bool has[PPT];
     float px[PPT], py[PPT], T[PPT], Cr[PPT], Cg[PPT], Cb[PPT];
+    uint32_t death = 0;  // 1 + pair index that saturated my last pixel (P_it accounting)
     bool done = true;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
@@ -185,6 +189,7 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
                     Cg[k] += wgt * sc.y;
                     Cb[k] += wgt * sc.z;
                     T[k] = t_cur * (1.0f - a);
+                    if (T[k] < tfloor) death = b * B + j + 1;
                     blended = true;
                 }
                 if (__any_sync(0xffffffffu, blended)) {
@@ -199,6 +204,16 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
         if (__syncthreads_and(done)) break;
     }
     cp_async_wait<0>();
+
+    // P_it of this tile: pairs the reference iterates before `active == 0`
+    // (rasterizer.cpp:55-56): n if any pixel stays unsaturated.
+    {
+        const uint32_t mine = done ? death : n;
+        const uint32_t wmax = __reduce_max_sync(0xffffffffu, mine);
+        if (lane == 0 && wmax) atomicMax(&sPit, wmax);
+        __syncthreads();
+        if (tid == 0 && pit && sPit) atomicAdd(pit, static_cast<unsigned long long>(sPit));
+    }
 
     // epilogue: C + T * background, clamped (rasterizer.cpp:89-99)
     if (t16) {
@@ -239,22 +254,22 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
 template <int PPT>
 static void launch_ppt(bool exact, bool maxt, int grid, cudaStream_t st, const FrameParams& p,
                        const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
-                       const float4* P2, float* image, uint32_t* mt) {
+                       const float4* P2, float* image, uint32_t* mt, unsigned long long* pit) {
     if (exact) {
-        if (maxt) k_raster<PPT, true, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt);
-        else k_raster<PPT, true, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt);
+        if (maxt) k_raster<PPT, true, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else k_raster<PPT, true, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
     } else {
-        if (maxt) k_raster<PPT, false, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt);
-        else k_raster<PPT, false, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt);
+        if (maxt) k_raster<PPT, false, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else k_raster<PPT, false, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
     }
 }
 
 void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t st, const FrameParams& p,
                           const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
-                          const float4* P2, float* image, uint32_t* maxt_buf) {
-    if (ppt == 1) launch_ppt<1>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf);
-    else if (ppt == 4) launch_ppt<4>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf);
-    else launch_ppt<16>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf);
+                          const float4* P2, float* image, uint32_t* maxt_buf, unsigned long long* pit) {
+    if (ppt == 1) launch_ppt<1>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
+    else if (ppt == 4) launch_ppt<4>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
+    else launch_ppt<16>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
 }
 
 }  // namespace agsx

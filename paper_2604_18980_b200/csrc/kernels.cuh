@@ -41,7 +41,7 @@ cudaError_t onesweep_configure(size_t smem, int* occupancy);
 
 void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t st, const FrameParams& p,
                           const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
-                          const float4* P2, float* image, uint32_t* maxt_buf);
+                          const float4* P2, float* image, uint32_t* maxt_buf, unsigned long long* pit);
 
 __global__ void k_logf(const float* x, float* y, uint64_t n);
 __global__ void k_expf(const float* x, float* y, uint64_t n);

@@ -202,6 +202,26 @@ public:
         return out;
     }
 
+    py::array_t<float> stage_history(int max_frames) {
+        std::vector<float> ms(static_cast<std::size_t>(std::max(max_frames, 0)) * 4);
+        int32_t n = 0;
+        const int rc = agsx_stage_history(ctx_, ms.data(), max_frames, &n);
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        py::array_t<float> out({static_cast<py::ssize_t>(n), py::ssize_t(4)});
+        std::memcpy(out.mutable_data(), ms.data(), static_cast<std::size_t>(n) * 4 * sizeof(float));
+        return out;
+    }
+
+    py::dict frame_stats() {
+        std::uint64_t v[6] = {};
+        const int rc = agsx_frame_stats(ctx_, v, 6);
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        py::dict d;
+        const char* names[6] = {"splat_count", "splats_with_tiles", "pair_count", "p_it", "overflow", "tiles"};
+        for (int i = 0; i < 6; ++i) d[names[i]] = v[i];
+        return d;
+    }
+
     py::tuple device_image() {
         float* p = nullptr;
         int32_t w = 0, h = 0;
@@ -461,6 +481,8 @@ PYBIND11_MODULE(_core, m) {
              py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27)
         .def("wait", &Renderer::wait)
         .def("device_image", &Renderer::device_image)
+        .def("stage_history", &Renderer::stage_history, py::arg("max_frames") = 64)
+        .def("frame_stats", &Renderer::frame_stats)
         .def("dump_tile_counts", &Renderer::dump_tile_counts, py::arg("n"))
         .def("dump_sorted_pairs", &Renderer::dump_sorted_pairs)
         .def("dump_ranges", &Renderer::dump_ranges, py::arg("tile_count"))
