@@ -85,6 +85,9 @@ class ClockSampler:
             return
         self.thread = threading.Thread(target=self._read, daemon=True)
         self.thread.start()
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 3.0:  # first sample before the timed region
+            time.sleep(0.02)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -194,7 +197,15 @@ def run_reference_arm(args, rank):
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "stage_times_s": out["stage_times"],
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_jsonable), flush=True)
+
+
+def _jsonable(o):
+    if isinstance(o, (np.floating, np.integer)):
+        return o.item()
+    if isinstance(o, np.ndarray):
+        return o.tolist()
+    raise TypeError(type(o).__name__)
 
 
 # ------------------------------------------------------------- our arm
@@ -390,7 +401,7 @@ def run_ours(args, rank, world, local_rank):
         "quality": quality,
         "adagscale_off": off,
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line, default=_jsonable), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
@@ -399,8 +410,8 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
     ap.add_argument("--mode", default="adagscale", choices=["adagscale", "ellipse", "aabb", "obb"])

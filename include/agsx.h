@@ -207,6 +207,10 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
 int agsx_device_logf(agsx_ctx* ctx, const float* x, float* y, uint64_t n);
 int agsx_device_expf(agsx_ctx* ctx, const float* x, float* y, uint64_t n);
 
+/* Page-locked host buffers for frame egress (full-bandwidth D2H of images). */
+int agsx_host_alloc(size_t bytes, void** out);
+void agsx_host_free(void* p);
+
 /* Number of kernels this ctx has launched since creation. */
 uint64_t agsx_kernel_launches(const agsx_ctx* ctx);
 

@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -73,6 +74,7 @@ struct agsx_ctx {
     uint32_t epoch = 1;
     int num_sms = 148;
     int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1;
+    Buf sort_counts;  // grid x 256 per-chunk digit counts (one pass at a time)
 
     // device arenas (grow-only)
     Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2;
@@ -218,6 +220,8 @@ FrameParams make_params(const agsx_camera& cam, const agsx_config& cfg, const ag
     p.k = cfg.k;
     for (int i = 0; i < 3; ++i) p.bg[i] = cfg.background[i];
     p.flags = cfg.flags;
+    p.raster_ppt = 2;
+    if (const char* e = std::getenv("AGSX_RASTER_PPT")) p.raster_ppt = std::atoi(e) == 4 ? 4 : 2;
     p.adaptive = cfg.mode == AGSX_MODE_ADAGSCALE ? 1 : 0;
     p.lut_dmin = 0.0f;
     p.lut_dmax = 100.0f;
@@ -253,25 +257,27 @@ void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, con
     check_launch(ctx);
 }
 
-size_t onesweep_smem(bool k64) {
+size_t sort_smem(bool k64) {
     return (k64 ? 8 : 4) * static_cast<size_t>(kSortTile) + 4 * static_cast<size_t>(kSortTile) +
            (kSortThreads / 32) * 256 * 4;
 }
 
-// One stable onesweep pass; returns nothing, counts launches.
+constexpr int kTotalsSlots = 16;  // zeroed 256-bin totals per sort pass (frame memset)
+size_t counters_bytes() { return sizeof(Counters) + kTotalsSlots * 256 * 4; }
+
+int sort_grid(agsx_ctx* ctx, bool k64) { return ctx->num_sms * (k64 ? ctx->occ_sort64 : ctx->occ_sort32); }
+
+// One stable LSD pass; `slot` selects the zeroed totals array.
 template <typename K>
-void onesweep_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout,
-                   const uint32_t* n_dev, uint64_t n_host, int shift, const uint32_t* hist,
-                   uint32_t* tile_ctr) {
-    const int occ = sizeof(K) == 8 ? ctx->occ_sort64 : ctx->occ_sort32;
-    int grid = ctx->num_sms * occ;
-    if (!n_dev) {
-        const uint64_t tiles = (n_host + kSortTile - 1) / kSortTile;
-        grid = static_cast<int>(std::min<uint64_t>(grid, std::max<uint64_t>(tiles, 1)));
-    }
-    launch_onesweep<K>(grid, onesweep_smem(sizeof(K) == 8), ctx->stream, kin, vin, kout, vout, n_dev, n_host,
-                       shift, hist, ptr<uint64_t>(ctx->lb), tile_ctr, ctx->epoch++);
+void sort_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, const uint32_t* n_dev,
+               uint64_t n_host, int shift, bool sentinel, uint32_t* totals, uint32_t* n_out) {
+    const bool k64 = sizeof(K) == 8;
+    const int grid = sort_grid(ctx, k64);
+    ensure(ctx->sort_counts, static_cast<size_t>(grid) * 256 * 4);
+    launch_sort_pass<K>(grid, sort_smem(k64), ctx->stream, kin, vin, kout, vout, n_dev, n_host, shift, sentinel,
+                        static_cast<K>(~K(0)), ptr<uint32_t>(ctx->sort_counts), totals, n_out);
     check_launch(ctx);
+    ctx->launches += 1;  // two kernels per pass
 }
 
 void ensure_lb(agsx_ctx* ctx, uint64_t max_elems) {
@@ -295,7 +301,7 @@ void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pi
     ensure(ctx->dvals2, std::max<uint64_t>(n, 1) * 4);
     ensure(ctx->ranges, std::max<uint64_t>(tiles, 1) * 8);
     ensure(ctx->image, std::max<uint64_t>(pixels, 1) * 12);
-    ensure(ctx->ctr, sizeof(Counters) + 2 * 8 * 256 * 4);
+    ensure(ctx->ctr, counters_bytes());
     if (ctx->pair_capacity == 0) {
         // first guess: 12 pairs per Gaussian, at most the budget, at least 1M
         ctx->pair_capacity = std::min<uint64_t>(std::max<uint64_t>(12 * n, 1u << 20),
@@ -348,36 +354,32 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     const uint64_t n = sc->n;
     const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
     Counters* ctr = ptr<Counters>(ctx->ctr);
-    uint32_t* hist_depth = reinterpret_cast<uint32_t*>(ctr + 1);
-    uint32_t* hist_tile = hist_depth + 8 * 256;
+    uint32_t* totals = reinterpret_cast<uint32_t*>(ctr + 1);  // kTotalsSlots x 256
     cudaStream_t st = ctx->stream;
     ctx->ev = ctx->ev_ring[ctx->frames % agsx_ctx::kRing];
     ++ctx->frames;
 
     AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
-    AGSX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters) + 2 * 8 * 256 * 4, st));
+    AGSX_CUDA(cudaMemsetAsync(ctr, 0, counters_bytes(), st));
     AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
     if (maxt) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, n * 4, st));
     const SplatPlanes pl = planes_of(ctx);
     if (n > 0) {
         const int grid = static_cast<int>((n + 255) / 256);
-        k_preprocess<<<grid, 256, 0, st>>>(p, sc->view(), pl, ptr<uint32_t>(ctx->status),
-                                            ptr<uint32_t>(ctx->dkeys), ptr<uint32_t>(ctx->dvals),
-                                            ptr<uint64_t>(ctx->lb), ctr, ctx->epoch++, dump);
+        k_preprocess<<<grid, 256, 0, st>>>(p, sc->view(), pl, ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys),
+                                            ctr, dump);
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[1], st));
-    // K4a: stable sort of the splats with tiles by depth bits (4 x 8-bit)
+    // K4a: stable sort by depth bits (4 x 8-bit); pass 0 drops the sentinel
+    // keys of splats without tiles (the ordered compaction) and sets m.
     uint32_t* dk[2] = {ptr<uint32_t>(ctx->dkeys), ptr<uint32_t>(ctx->dkeys2)};
     uint32_t* dv[2] = {ptr<uint32_t>(ctx->dvals), ptr<uint32_t>(ctx->dvals2)};
     if (n > 0) {
-        const int hgrid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->num_sms * 4));
-        launch_hist<uint32_t>(hgrid, st, dk[0], &ctr->m, 0, 0, 4, hist_depth);
-        check_launch(ctx);
-        for (int ps = 0; ps < 4; ++ps) {
-            onesweep_pass<uint32_t>(ctx, dk[ps & 1], dv[ps & 1], dk[(ps + 1) & 1], dv[(ps + 1) & 1],
-                                    &ctr->m, 0, 8 * ps, hist_depth + 256 * ps, &ctr->tile_ctr[2 + ps]);
-        }
+        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, totals, &ctr->m);
+        for (int ps = 1; ps < 4; ++ps)
+            sort_pass<uint32_t>(ctx, dk[ps & 1], dv[ps & 1], dk[(ps + 1) & 1], dv[(ps + 1) & 1], &ctr->m, 0, 8 * ps,
+                                false, totals + 256 * ps, nullptr);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[2], st));
     // K3: scan + emit in depth order
@@ -394,11 +396,9 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     const int passes = (tile_bits(static_cast<uint32_t>(tiles)) + 7) / 8;
     int cur = 0;
     if (n > 0) {
-        launch_hist<uint32_t>(ctx->num_sms * 4, st, tk[0], &ctr->p_eff, 0, 0, passes, hist_tile);
-        check_launch(ctx);
         for (int ps = 0; ps < passes; ++ps) {
-            onesweep_pass<uint32_t>(ctx, tk[cur], pv[cur], tk[cur ^ 1], pv[cur ^ 1], &ctr->p_eff, 0,
-                                    8 * ps, hist_tile + 256 * ps, &ctr->tile_ctr[6 + ps]);
+            sort_pass<uint32_t>(ctx, tk[cur], pv[cur], tk[cur ^ 1], pv[cur ^ 1], &ctr->p_eff, 0, 8 * ps, false,
+                                totals + 256 * (4 + ps), nullptr);
             cur ^= 1;
         }
         k_ranges_u32<<<ctx->num_sms * 4, 256, 0, st>>>(tk[cur], &ctr->p_eff, ptr<uint2>(ctx->ranges));
@@ -487,6 +487,18 @@ extern "C" {
 
 int agsx_abi_version(void) { return AGSX_ABI_VERSION; }
 
+int agsx_host_alloc(size_t bytes, void** out) {
+    if (!out) return AGSX_EINVAL;
+    *out = nullptr;
+    const cudaError_t e = cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable);
+    if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? AGSX_ENOMEM : AGSX_ECUDA;
+    return AGSX_OK;
+}
+
+void agsx_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int agsx_create(int device, agsx_ctx** out) {
     if (!out) return AGSX_EINVAL;
     *out = nullptr;
@@ -496,8 +508,8 @@ int agsx_create(int device, agsx_ctx** out) {
     const int rc = guarded(ctx, [&]() -> int {
         AGSX_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
         AGSX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
-        AGSX_CUDA(onesweep_configure<uint32_t>(onesweep_smem(false), &ctx->occ_sort32));
-        AGSX_CUDA(onesweep_configure<uint64_t>(onesweep_smem(true), &ctx->occ_sort64));
+        AGSX_CUDA(sort_configure<uint32_t>(sort_smem(false), &ctx->occ_sort32));
+        AGSX_CUDA(sort_configure<uint64_t>(sort_smem(true), &ctx->occ_sort64));
         AGSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ_emit, k_emit, 256, 0));
         ctx->occ_sort32 = std::max(ctx->occ_sort32, 1);
         ctx->occ_sort64 = std::max(ctx->occ_sort64, 1);
@@ -524,7 +536,7 @@ void agsx_destroy(agsx_ctx* ctx) {
     for (Buf* b : {&ctx->status, &ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4, &ctx->dkeys,
                    &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
                    &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
-                   &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
+                   &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
                    &ctx->tmp3, &ctx->tmp4})
         release(*b);
     for (auto& set : ctx->ev_ring)
@@ -768,8 +780,7 @@ int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_came
         AGSX_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), ctx->stream));
         if (n) {
             k_preprocess<<<static_cast<int>((n + 255) / 256), 256, 0, ctx->stream>>>(
-                p, scene->view(), planes_of(ctx), ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys),
-                ptr<uint32_t>(ctx->dvals), ptr<uint64_t>(ctx->lb), ctr, ctx->epoch++,
+                p, scene->view(), planes_of(ctx), ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys), ctr,
                 ptr<agsx_splat_view>(ctx->dump));
             check_launch(ctx);
         }
@@ -859,13 +870,12 @@ int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64
         ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 8);
         ensure(ctx->tmp2, std::max<uint64_t>(n, 1) * 4);
         ensure(ctx->tmp3, std::max<uint64_t>(n, 1) * 4);
-        ensure(ctx->hist, 8 * 256 * 4 + sizeof(Counters));
+        ensure(ctx->hist, 2 * 8 * 256 * 4);
         ensure(ctx->ranges, std::max<int>(tile_count, 1) * 8);
-        ensure_lb(ctx, n);
         uint32_t* hist = ptr<uint32_t>(ctx->hist);
-        Counters* ctr = reinterpret_cast<Counters*>(hist + 8 * 256);
+        uint32_t* totals = hist + 8 * 256;
         cudaStream_t st = ctx->stream;
-        AGSX_CUDA(cudaMemsetAsync(ctx->hist.p, 0, 8 * 256 * 4 + sizeof(Counters), st));
+        AGSX_CUDA(cudaMemsetAsync(ctx->hist.p, 0, 2 * 8 * 256 * 4, st));
         if (tile_count) AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, static_cast<size_t>(tile_count) * 8, st));
         uint64_t* k[2] = {ptr<uint64_t>(ctx->tmp0), ptr<uint64_t>(ctx->tmp1)};
         uint32_t* v[2] = {ptr<uint32_t>(ctx->tmp2), ptr<uint32_t>(ctx->tmp3)};
@@ -874,7 +884,7 @@ int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64
             AGSX_CUDA(cudaMemcpyAsync(k[0], keys, n * 8, cudaMemcpyHostToDevice, st));
             AGSX_CUDA(cudaMemcpyAsync(v[0], splat_index, n * 4, cudaMemcpyHostToDevice, st));
             const int hgrid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->num_sms * 4));
-            launch_hist<uint64_t>(hgrid, st, k[0], nullptr, n, 0, 8, hist);
+            launch_hist64(hgrid, st, k[0], n, 8, hist);
             check_launch(ctx);
             std::vector<uint32_t> h(8 * 256);
             AGSX_CUDA(cudaMemcpyAsync(h.data(), hist, h.size() * 4, cudaMemcpyDeviceToHost, st));
@@ -884,8 +894,8 @@ int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64
                 bool trivial = false;
                 for (int d = 0; d < 256; ++d) trivial = trivial || h[ps * 256 + d] == n;
                 if (trivial) continue;
-                onesweep_pass<uint64_t>(ctx, k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], nullptr, n, 8 * ps,
-                                        hist + 256 * ps, &ctr->tile_ctr[ps]);
+                sort_pass<uint64_t>(ctx, k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], nullptr, n, 8 * ps, false,
+                                    totals + 256 * ps, nullptr);
                 cur ^= 1;
             }
             if (tile_count) {

@@ -1,6 +1,7 @@
 // agsx_internal.cuh -- device data layout and shared device functions of the
 // B200 render path.  See DESIGN.md §3 for the HBM layout.
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,6 +32,7 @@ struct FrameParams {
     float tau, tfloor, aclamp, near_plane, guard, k;
     float bg[3];
     uint32_t flags;
+    int raster_ppt;  // pixels per thread of the 16x16 rasterizer (2 or 4)
     // T_upper LUT (lut.hpp:11-26)
     int adaptive;
     float lut_dmin, lut_dmax;
@@ -52,9 +54,9 @@ struct DevScene {
 
 // Per-splat planes written by preprocess for splats that hit >= 1 tile,
 // indexed by Gaussian id (value of every pair).
-//   P0 = {mean.x, mean.y, inv.xx, inv.xy}            raster + emit
-//   P1 = {inv.yy, opacity, pcut, bbox_x (2 x int16)} raster + emit(inv.yy)
-//   P2 = {r, g, b, bbox_y (2 x int16)}               raster
+//   P0 = {mean.x, mean.y, inv.xx, 2*inv.xy}          raster + emit
+//   P1 = {inv.yy, opacity, qcut, qsafe}              raster + emit(inv.yy)
+//   P2 = {r, g, b, half2(ex, ey)}                    raster
 //   P3 = {rx, ry, r2, r}                             emit (tile test)
 //   P4 = {v1.x, v1.y, a, b}                          emit, OBB mode only
 struct SplatPlanes {
@@ -236,44 +238,47 @@ __device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FramePa
     return n;
 }
 
-// Conservative blend-side culling data for the rasterizer (not part of the
-// reference; it only lets whole warps skip splats whose alpha is provably
-// below tau at every pixel of the warp):
-//   pcut : power < pcut  =>  opacity * expf(power) < tau
-//   bbox : pixel-index box outside of which power < pcut.
-__device__ __forceinline__ void blend_cull_data(float mx, float my, float ixx, float ixy, float iyy, float opacity,
-                                float tau, float& pcut, uint32_t& bbx, uint32_t& bby) {
-    auto pack = [](double lo, double hi) {
-        const int a = static_cast<int>(fmax(-32768.0, fmin(32767.0, lo)));
-        const int b = static_cast<int>(fmax(-32768.0, fmin(32767.0, hi)));
-        return (static_cast<uint32_t>(a) & 0xffffu) | (static_cast<uint32_t>(b) << 16);
-    };
+// Blend-side culling data for the rasterizer (not part of the reference; it
+// only lets the rasterizer skip, or take a fast path for, pixels whose
+// decision alpha >= tau is provable with a margin).  In
+// terms of q = d^T inv d (power = -0.5 q exactly):
+//   q > qcut              =>  opacity * expf(-q/2) < tau          (skip)
+//   0 <= q < qsafe        =>  opacity * expf(-q/2) >= tau, < clamp (fast)
+//   ex, ey                :  |d.x| > ex or |d.y| > ey  =>  q > qcut
+// qsafe = 0 disables the fast path (opacity >= clamp or < tau).
+__device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy, float opacity, float tau,
+                                                float aclamp, float& qcut, float& qsafe, float& ex, float& ey) {
+    const float inf = __int_as_float(0x7f800000);
     if (!(opacity >= tau)) {  // alpha <= opacity < tau everywhere (or NaN): never blends
-        pcut = __int_as_float(0x7f800000);
-        bbx = bby = pack(32767.0, -32768.0);
+        qcut = 0.0f;          // q > 0 skips; q <= 0 (or NaN) takes the exact path
+        qsafe = 0.0f;
+        ex = ey = 0.0f;
         return;
     }
     const double lr = log(static_cast<double>(opacity) / static_cast<double>(tau));  // >= 0
-    const double cut = -lr - 1e-4 * (1.0 + lr);
-    pcut = __double2float_rd(cut);
-    // q = -2 * power, evaluated in float: q_f >= Q * (1 - 64 u kappa).
+    const double m = 1e-4 * (1.0 + lr);
+    qcut = __double2float_ru(2.0 * (lr + m));
+    qsafe = (opacity < aclamp && lr > m) ? __double2float_rd(2.0 * (lr - m)) : 0.0f;
+    // Box of {q <= qcut} inflated for the float evaluation error of q:
+    // q_f >= Q (1 - 64 u kappa).
     const double a = ixx, b = ixy, c = iyy;
     const double det = a * c - b * b;
-    const double tr = a + c;
     const double disc = sqrt(fmax(0.0, 0.25 * (a - c) * (a - c) + b * b));
-    const double lmax = 0.5 * tr + disc, lmin = 0.5 * tr - disc;
+    const double lmax = 0.5 * (a + c) + disc, lmin = 0.5 * (a + c) - disc;
     const double relerr = 64.0 * 0x1p-24 * (lmin > 0.0 ? lmax / lmin : 1e300);
-    if (!(det > 0.0) || !(lmin > 0.0) || !(relerr < 0.5) || !isfinite(mx) || !isfinite(my)) {
-        bbx = bby = pack(-32768.0, 32767.0);  // no culling for this splat
+    if (!(det > 0.0) || !(lmin > 0.0) || !(relerr < 0.5)) {
+        ex = ey = inf;  // no culling for this splat
         return;
     }
-    const double r2 = (-2.0 * cut) / (1.0 - relerr);
-    const double ex = sqrt(r2 * c / det) * 1.0001 + 1e-3;  // (M^-1)_xx = iyy / det
-    const double ey = sqrt(r2 * a / det) * 1.0001 + 1e-3;
-    bbx = pack(floor(mx - ex - 0.5) - 1.0, ceil(mx + ex - 0.5) + 1.0);
-    bby = pack(floor(my - ey - 0.5) - 1.0, ceil(my + ey - 0.5) + 1.0);
+    const double r2 = static_cast<double>(qcut) / (1.0 - relerr);
+    ex = __double2float_ru(sqrt(r2 * c / det) * 1.0001 + 1e-3);  // (M^-1)_xx = iyy / det
+    ey = __double2float_ru(sqrt(r2 * a / det) * 1.0001 + 1e-3);
 }
 
+__device__ __forceinline__ uint32_t pack_extent(float ex, float ey) {
+    const __half hx = __float2half_ru(ex), hy = __float2half_ru(ey);
+    return static_cast<uint32_t>(__half_as_ushort(hx)) | (static_cast<uint32_t>(__half_as_ushort(hy)) << 16);
+}
 
 // ---- decoupled look-back state words -----------------------------------
 // u64 = [63:62] flag | [61:32] epoch | [31:0] value.  The epoch (bumped per

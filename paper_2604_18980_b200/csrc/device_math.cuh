@@ -117,6 +117,13 @@ __device__ __forceinline__ float glibc_expf(float x) {
     return static_cast<float>(y);
 }
 
+// Hardware 2^x (MUFU.EX2).
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Hardware exp2 (MUFU.EX2), flush-to-zero for tiny results.
 __device__ __forceinline__ float fast_exp(float x) {
     float y;

@@ -25,7 +25,7 @@ __device__ __forceinline__ TileTest planes_tile_test(const FrameParams& p, const
     t.cx = a.x;
     t.cy = a.y;
     t.ixx = a.z;
-    t.ixy = a.w;
+    t.ixy = 0.5f * a.w;  // P0.w holds 2*inv.xy (exact doubling)
     t.iyy = iyy;
     t.rx = c.x;
     t.ry = c.y;
@@ -125,13 +125,11 @@ __global__ void k_splats_to_planes(FrameParams p, const agsx_splat_view* __restr
                                       s.inv_cov[0], s.inv_cov[1], s.inv_cov[2], s.opacity, s.th, p);
     counts[j] = count_tiles(t, p);
     depth_bits[j] = __float_as_uint(s.depth);
-    float pcut;
-    uint32_t bbx, bby;
-    blend_cull_data(s.mean2d[0], s.mean2d[1], s.inv_cov[0], s.inv_cov[1], s.inv_cov[2], s.opacity,
-                    p.tau, pcut, bbx, bby);
-    pl.p0[j] = make_float4(s.mean2d[0], s.mean2d[1], s.inv_cov[0], s.inv_cov[1]);
-    pl.p1[j] = make_float4(s.inv_cov[2], s.opacity, pcut, __uint_as_float(bbx));
-    pl.p2[j] = make_float4(s.rgb[0], s.rgb[1], s.rgb[2], __uint_as_float(bby));
+    float qcut, qsafe, ex, ey;
+    blend_cull_data(s.inv_cov[0], s.inv_cov[1], s.inv_cov[2], s.opacity, p.tau, p.aclamp, qcut, qsafe, ex, ey);
+    pl.p0[j] = make_float4(s.mean2d[0], s.mean2d[1], s.inv_cov[0], 2.0f * s.inv_cov[1]);
+    pl.p1[j] = make_float4(s.inv_cov[2], s.opacity, qcut, qsafe);
+    pl.p2[j] = make_float4(s.rgb[0], s.rgb[1], s.rgb[2], __uint_as_float(pack_extent(ex, ey)));
     pl.p3[j] = make_float4(t.rx, t.ry, t.r2, 0.0f);
     if (p.mode == AGSX_MODE_OBB) pl.p4[j] = make_float4(t.v1x, t.v1y, t.a, t.b);
 }

@@ -7,9 +7,10 @@
 //              compute_th       preprocess.cpp:107-116
 //              count pass       pair_gen.cpp:167-175 (intersect_tiles :108-159)
 //
-// One thread per Gaussian; one 256-thread CTA per 256 Gaussians, CTA order
-// taken from an atomic counter so the single-pass (decoupled look-back)
-// compaction only ever waits on CTAs that are already resident.
+// One thread per Gaussian.  Output depth keys stay in Gaussian order, with
+// 0xffffffff for splats that hit no tile; the first depth-sort pass drops
+// those sentinels, which is the order-preserving compaction of the
+// reference (preprocess.cpp:158-162) done inside the sort.
 #include "agsx_internal.cuh"
 #include "kernels.cuh"
 
@@ -80,16 +81,9 @@ __device__ __forceinline__ void eval_color(const DevScene& sc, uint64_t i, float
 
 __global__ void __launch_bounds__(256)
 k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ status,
-             uint32_t* __restrict__ dkeys, uint32_t* __restrict__ dvals, uint64_t* lb_states,
-             Counters* ctr, uint32_t epoch, agsx_splat_view* __restrict__ dump) {
-    __shared__ uint32_t s_tile;
-    __shared__ uint32_t s_warp_keep[8];
-    __shared__ uint32_t s_prefix;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(&ctr->tile_ctr[0], 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint64_t i = static_cast<uint64_t>(tile) * 256u + tid;
+             uint32_t* __restrict__ dkeys, Counters* ctr, agsx_splat_view* __restrict__ dump) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
 
     bool alive = false, keep = false;
     float depth = 0.0f;
@@ -221,12 +215,11 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
                 eval_color(sc, i, sr.w, gb.x, gb.y, ux, uy, uz, rgb);
             }
             if (keep) {
-                float pcut;
-                uint32_t bbx, bby;
-                blend_cull_data(m2x, m2y, ixx, ixy, iyy, opacity, p.tau, pcut, bbx, bby);
-                pl.p0[i] = make_float4(m2x, m2y, ixx, ixy);
-                pl.p1[i] = make_float4(iyy, opacity, pcut, __uint_as_float(bbx));
-                pl.p2[i] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(bby));
+                float qcut, qsafe, ex, ey;
+                blend_cull_data(ixx, ixy, iyy, opacity, p.tau, p.aclamp, qcut, qsafe, ex, ey);
+                pl.p0[i] = make_float4(m2x, m2y, ixx, 2.0f * ixy);
+                pl.p1[i] = make_float4(iyy, opacity, qcut, qsafe);
+                pl.p2[i] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(pack_extent(ex, ey)));
                 pl.p3[i] = make_float4(tt.rx, tt.ry, tt.r2, 0.0f);
                 if (p.mode == AGSX_MODE_OBB) pl.p4[i] = make_float4(tt.v1x, tt.v1y, tt.a, tt.b);
             }
@@ -253,33 +246,9 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         status[i] = cnt | (alive ? kAliveBit : 0u);
     }
 
-    // ---- order-preserving compaction of `keep` (single pass) -----------
-    const uint32_t keep_mask = __ballot_sync(0xffffffffu, keep);
+    if (i < sc.n) dkeys[i] = keep ? __float_as_uint(depth) : 0xffffffffu;
     const uint32_t alive_cnt = __popc(__ballot_sync(0xffffffffu, alive));
-    if (lane == 0) s_warp_keep[warp] = __popc(keep_mask);
     if (alive_cnt && lane == 0) atomicAdd(&ctr->s, alive_cnt);
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t v = lane < 8 ? s_warp_keep[lane] : 0u;
-        uint32_t incl = v;
-        for (int o = 1; o < 8; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += t;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 7);
-        if (lane < 8) s_warp_keep[lane] = incl - v;
-        const uint32_t prefix = lookback_warp(lb_states, tile, total, epoch);
-        if (lane == 0) {
-            s_prefix = prefix;
-            if (tile == gridDim.x - 1) ctr->m = prefix + total;
-        }
-    }
-    __syncthreads();
-    if (keep) {
-        const uint32_t pos = s_prefix + s_warp_keep[warp] + __popc(keep_mask & ((1u << lane) - 1u));
-        dkeys[pos] = __float_as_uint(depth);
-        dvals[pos] = static_cast<uint32_t>(i);
-    }
 }
 
 // Scene upload: host SoA (agsx_scene_desc) -> device planes.

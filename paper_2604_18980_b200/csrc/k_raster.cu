@@ -59,11 +59,209 @@ __device__ __forceinline__ float glibc_expf_smem(float x, const uint64_t* tab) {
     return static_cast<float>(y);
 }
 
-__device__ __forceinline__ int lo16(uint32_t v) { return static_cast<int>(static_cast<int16_t>(v & 0xffffu)); }
-__device__ __forceinline__ int hi16(uint32_t v) { return static_cast<int>(static_cast<int16_t>(v >> 16)); }
+// Splat extents packed as half2 (rounded up) in P2.w.
+__device__ __forceinline__ float2 unpack_extent(float w) {
+    const uint32_t v = __float_as_uint(w);
+    return make_float2(__half2float(__ushort_as_half(static_cast<unsigned short>(v & 0xffffu))),
+                       __half2float(__ushort_as_half(static_cast<unsigned short>(v >> 16))));
+}
+
+// Can the splat reach alpha >= tau at a pixel centre of the box?
+__device__ __forceinline__ bool meets_box(float mx, float my, float2 e, float cx0, float cx1, float cy0, float cy1) {
+    return mx + e.x >= cx0 && mx - e.x <= cx1 && my + e.y >= cy0 && my - e.y <= cy1;
+}
+
+// The reference's alpha_at (rasterizer.hpp:44-50) from q = d^T inv d
+// (power = -0.5 q exactly); returns a value < tau when the splat does not
+// blend.
+__device__ __forceinline__ float exact_alpha(float q, float opacity, float aclamp, const uint64_t* tab) {
+    const float power = -0.5f * q;
+    if (power > 0.0f) return 0.0f;
+    const float a = opacity * glibc_expf_smem(power, tab);
+    return a < aclamp ? a : aclamp;
+}
 
 }  // namespace
 
+
+// 16x16 tiles, PPT pixels per thread in a vertical column (PPT in {2,4}).
+// Warp w of the 16*16/PPT/32 warps owns rows [w*R, (w+1)*R), R = 2*PPT:
+// lane l -> column l%16, rows w*R + (l/16)*PPT + k.  Each warp streams the
+// tile's sorted splat list on its own, 32 records per step (prefetched one
+// step ahead), keeps the splats whose conservative extent meets its rows
+// (ballot) and blends them in order; no block barrier until the store.
+//
+// Per pixel the alpha >= tau decision is taken on q = d^T inv d, the exact
+// float value of the reference (power = -0.5 q exactly), against per-splat
+// thresholds with a 1e-4 relative margin (blend_cull_data):
+//   q > qcut        -> alpha < tau: skip
+//   0 <= q < qsafe  -> alpha >= tau: alpha = opacity * 2^(-q log2(e)/2)
+//   otherwise (margin band, q < 0, NaN, opacity >= clamp): deferred to a
+//   warp-uniform block that evaluates the reference expression with the
+//   glibc-exact expf.  EXACT routes every non-skipped pixel there.
+template <int PPT, bool EXACT, bool MAXT>
+__global__ void __launch_bounds__(256 / PPT)
+k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+           const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
+           float* __restrict__ image, uint32_t* __restrict__ maxt, unsigned long long* __restrict__ pit) {
+    constexpr int NW = 8 / PPT;  // warps per tile
+    constexpr int R = 2 * PPT;   // rows per warp
+    __shared__ __align__(16) float4 sA[NW][32];
+    __shared__ __align__(16) float4 sB[NW][32];
+    __shared__ __align__(16) float4 sC[NW][32];
+    __shared__ uint32_t sG[MAXT ? NW : 1][32];
+    __shared__ uint64_t sTab[32];
+    __shared__ __align__(16) float sOut[16 * 16 * 3];
+    __shared__ uint32_t sPit;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 32) sTab[tid] = kExp2fTab[tid];
+    if (tid == 0) sPit = 0;
+    __syncthreads();
+
+    const int tile = blockIdx.x;
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int x0 = tx * 16, y0 = ty * 16;
+    const int w = imin(16, p.W - x0), h = imin(16, p.H - y0);
+    const int lx = lane & 15, ly0 = warp * R + (lane >> 4) * PPT;
+    const float px = static_cast<float>(x0 + lx) + 0.5f;
+    float py[PPT], T[PPT], Cr[PPT], Cg[PPT], Cb[PPT];
+    uint32_t live = 0;  // bit k: pixel k exists and is not saturated
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        py[k] = static_cast<float>(y0 + ly0 + k) + 0.5f;
+        T[k] = 1.0f;
+        Cr[k] = Cg[k] = Cb[k] = 0.0f;
+        if (lx < w && ly0 + k < h) live |= 1u << k;
+    }
+    uint32_t death = 0;
+    const bool warp_empty = warp * R >= h;
+    // pixel-centre box of the warp's pixels inside the image
+    const float cx0 = x0 + 0.5f, cx1 = x0 + w - 0.5f;
+    const float cy0 = y0 + warp * R + 0.5f, cy1 = y0 + imin(warp * R + R, h) - 0.5f;
+    const float tau = p.tau, tfloor = p.tfloor, aclamp = p.aclamp;
+    const float c_ex2 = -0.5f * 1.4426950408889634f;
+
+    const uint2 rg = ranges[tile];
+    const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x;
+    float4 nA = make_float4(0, 0, 0, 0), nB = nA, nC = nA;
+    uint32_t nG = 0;
+    auto fetch = [&](uint32_t base) {
+        const uint32_t i = base + lane;
+        if (i < end) {
+            nG = __ldg(&vals[i]);
+            nA = __ldg(&P0[nG]);
+            nB = __ldg(&P1[nG]);
+            nC = __ldg(&P2[nG]);
+        }
+    };
+    bool all_done = warp_empty || !__any_sync(0xffffffffu, live != 0);
+    if (!all_done) fetch(start);
+    for (uint32_t base = start; base < end && !all_done; base += 32) {
+        const float4 cA = nA, cB = nB, cC = nC;
+        const uint32_t cG = nG;
+        if (base + 32 < end) fetch(base + 32);
+        const bool rel = base + lane < end && meets_box(cA.x, cA.y, unpack_extent(cC.w), cx0, cx1, cy0, cy1);
+        uint32_t m = __ballot_sync(0xffffffffu, rel);
+        if (!m) continue;
+        sA[warp][lane] = cA;
+        sB[warp][lane] = cB;
+        sC[warp][lane] = cC;
+        if (MAXT) sG[warp][lane] = cG;
+        __syncwarp();
+        while (m) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            const float4 sa = sA[warp][j];  // mx, my, inv.xx, 2*inv.xy
+            const float4 sb = sB[warp][j];  // inv.yy, opacity, qcut, qsafe
+            const float4 sc = sC[warp][j];  // r, g, b, extent
+            const uint32_t qcut = __float_as_uint(sb.z);
+            const uint32_t qsafe = EXACT ? 0u : __float_as_uint(sb.w);
+            // column-shared terms of ((xx*dx)*dx + ((2xy)*dx)*dy) + (yy*dy)*dy
+            const float dx = px - sa.x;
+            const float t1 = sa.z * dx * dx;
+            const float t2 = sa.w * dx;
+            float q[PPT];
+            uint32_t need = 0;
+            bool newly_done = false;
+            auto blend = [&](int k, float a) {
+                const float t_cur = T[k];
+                if (MAXT) atomicMax(&maxt[sG[warp][j]], __float_as_uint(t_cur));
+                const float wgt = a * t_cur;
+                Cr[k] += wgt * sc.x;
+                Cg[k] += wgt * sc.y;
+                Cb[k] += wgt * sc.z;
+                T[k] = t_cur * (1.0f - a);
+                if (T[k] < tfloor) {
+                    live &= ~(1u << k);
+                    newly_done = true;
+                    death = base - start + j + 1;
+                }
+            };
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const float dy = py[k] - sa.y;
+                q[k] = (t1 + t2 * dy) + sb.x * dy * dy;
+                const uint32_t qb = __float_as_uint(q[k]);
+                const bool on = (live >> k) & 1u;
+                if (on && qb < qsafe) {
+                    blend(k, sb.y * fast_exp2(q[k] * c_ex2));
+                } else if (on && !(qb > qcut && qb <= 0x7f800000u)) {
+                    need |= 1u << k;
+                }
+            }
+            if (__any_sync(0xffffffffu, need != 0)) {
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    if (!((need >> k) & 1u)) continue;
+                    const float a = exact_alpha(q[k], sb.y, aclamp, sTab);
+                    if (!(a < tau)) blend(k, a);
+                }
+            }
+            if (__any_sync(0xffffffffu, newly_done) && !__any_sync(0xffffffffu, live != 0)) {
+                all_done = true;
+                break;
+            }
+        }
+        __syncwarp();
+    }
+
+    // P_it of this tile (rasterizer.cpp:55-56): n if any pixel stays unsaturated
+    {
+        const uint32_t n = end - start;
+        const uint32_t wmax = __reduce_max_sync(0xffffffffu, live ? n : death);
+        if (lane == 0 && wmax) atomicMax(&sPit, wmax);
+    }
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        if (lx < w && ly0 + k < h) {
+            float* o = &sOut[((ly0 + k) * 16 + lx) * 3];
+            o[0] = sclamp(Cr[k] + T[k] * p.bg[0], 0.0f, 1.0f);
+            o[1] = sclamp(Cg[k] + T[k] * p.bg[1], 0.0f, 1.0f);
+            o[2] = sclamp(Cb[k] + T[k] * p.bg[2], 0.0f, 1.0f);
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && pit && sPit) atomicAdd(pit, static_cast<unsigned long long>(sPit));
+    constexpr int NT = 256 / PPT;
+    if (w == 16 && (p.W & 3) == 0) {
+        for (int i = tid; i < 12 * h; i += NT) {
+            const int row = i / 12, col = i % 12;
+            float4* dst = reinterpret_cast<float4*>(image + (static_cast<size_t>(y0 + row) * p.W + x0) * 3);
+            __stcs(&dst[col], reinterpret_cast<const float4*>(sOut)[row * 12 + col]);
+        }
+    } else {
+        for (int i = tid; i < w * h * 3; i += NT) {
+            const int c = i % 3, pix = i / 3, row = pix / w, col = pix % w;
+            image[(static_cast<size_t>(y0 + row) * p.W + x0 + col) * 3 + c] = sOut[(row * 16 + col) * 3 + c];
+        }
+    }
+}
+
+// Any tile size in [1, 64]: 256 threads, pixel k of thread t is tile pixel
+// t + 256 k (row-major).  Batches of 256 splat records are staged with
+// cp.async (double-buffered); each warp skips splats whose extent misses
+// all of its pixels.  Same per-pixel arithmetic as k_raster16.
 template <int PPT, bool EXACT, bool MAXT>
 __global__ void __launch_bounds__(256)
 k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
@@ -75,10 +273,9 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
     __shared__ __align__(16) float4 sC[2][B];
     __shared__ uint32_t sG[MAXT ? 2 : 1][MAXT ? B : 1];
     __shared__ uint64_t sTab[32];
-    __shared__ __align__(16) float sOut[PPT == 1 ? 16 * 16 * 3 : 4];
     __shared__ uint32_t sPit;
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     if (tid < 32) sTab[tid] = kExp2fTab[tid];
     if (tid == 0) sPit = 0;
 
@@ -87,50 +284,42 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const int x0 = tx * ts, y0 = ty * ts;
     const int w = imin(ts, p.W - x0), h = imin(ts, p.H - y0);
-    const bool t16 = (ts == 16 && PPT == 1);
 
-    // pixel ownership
     int lx[PPT], ly[PPT];
-    bool has[PPT];
     float px[PPT], py[PPT], T[PPT], Cr[PPT], Cg[PPT], Cb[PPT];
-    uint32_t death = 0;  // 1 + pair index that saturated my last pixel (P_it accounting)
-    bool done = true;
+    uint32_t live = 0, death = 0;
+    float bx0 = 1e30f, bx1 = -1e30f, by0 = 1e30f, by1 = -1e30f;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-        if (t16) {
-            lx[k] = (warp & 1) * 8 + (lane & 7);
-            ly[k] = (warp >> 1) * 4 + (lane >> 3);
-        } else {
-            const int lp = tid + k * 256;
-            lx[k] = lp % ts;
-            ly[k] = lp / ts;
-            if (lp >= ts * ts) ly[k] = ts;  // out of tile
-        }
-        has[k] = lx[k] < w && ly[k] < h;
+        const int lp = tid + k * 256;
+        lx[k] = lp % ts;
+        ly[k] = lp < ts * ts ? lp / ts : ts;
         px[k] = static_cast<float>(x0 + lx[k]) + 0.5f;
         py[k] = static_cast<float>(y0 + ly[k]) + 0.5f;
         T[k] = 1.0f;
         Cr[k] = Cg[k] = Cb[k] = 0.0f;
-        done = done && !has[k];
-    }
-    // conservative pixel box of this warp
-    int bx0 = 1 << 30, bx1 = -(1 << 30), by0 = 1 << 30, by1 = -(1 << 30);
-#pragma unroll
-    for (int k = 0; k < PPT; ++k)
-        if (has[k]) {
-            bx0 = imin(bx0, x0 + lx[k]);
-            bx1 = imax(bx1, x0 + lx[k]);
-            by0 = imin(by0, y0 + ly[k]);
-            by1 = imax(by1, y0 + ly[k]);
+        if (lx[k] < w && ly[k] < h) {
+            live |= 1u << k;
+            bx0 = fminf(bx0, px[k]);
+            bx1 = fmaxf(bx1, px[k]);
+            by0 = fminf(by0, py[k]);
+            by1 = fmaxf(by1, py[k]);
         }
-    const int wx0 = __reduce_min_sync(0xffffffffu, bx0), wx1 = __reduce_max_sync(0xffffffffu, bx1);
-    const int wy0 = __reduce_min_sync(0xffffffffu, by0), wy1 = __reduce_max_sync(0xffffffffu, by1);
+    }
+    // warp pixel-centre box (float min/max via shuffles)
+    for (int o = 16; o > 0; o >>= 1) {
+        bx0 = fminf(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
+        bx1 = fmaxf(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
+        by0 = fminf(by0, __shfl_xor_sync(0xffffffffu, by0, o));
+        by1 = fmaxf(by1, __shfl_xor_sync(0xffffffffu, by1, o));
+    }
 
     const uint2 rg = ranges[tile];
     const uint32_t start = rg.x, end = rg.y;
     const uint32_t n = end > start ? end - start : 0u;
     const uint32_t nb = (n + B - 1) / B;
     const float tau = p.tau, tfloor = p.tfloor, aclamp = p.aclamp;
+    const float c_ex2 = -0.5f * 1.4426950408889634f;
 
     auto issue = [&](uint32_t b, int buf) {
         const uint32_t i = start + b * B + tid;
@@ -155,33 +344,29 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
         }
         __syncthreads();
         const int cnt = static_cast<int>(n - b * B < B ? n - b * B : B);
-        if (!__all_sync(0xffffffffu, done)) {
+        if (__any_sync(0xffffffffu, live != 0)) {
             for (int j = 0; j < cnt; ++j) {
-                const float4 sb = sB[buf][j];
                 const float4 sc = sC[buf][j];
-                const uint32_t bbx = __float_as_uint(sb.w), bby = __float_as_uint(sc.w);
-                if (hi16(bbx) < wx0 || lo16(bbx) > wx1 || hi16(bby) < wy0 || lo16(bby) > wy1)
-                    continue;  // warp-uniform: alpha < tau on every pixel of the warp
                 const float4 sa = sA[buf][j];
-                bool blended = false;
+                if (!meets_box(sa.x, sa.y, unpack_extent(sc.w), bx0, bx1, by0, by1)) continue;
+                const float4 sb = sB[buf][j];
+                const uint32_t qcut = __float_as_uint(sb.z);
+                const uint32_t qsafe = EXACT ? 0u : __float_as_uint(sb.w);
+                bool newly_done = false;
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
-                    if (!has[k] || T[k] < tfloor) continue;
-                    // alpha_at (rasterizer.hpp:44-50), no contraction
+                    if (!((live >> k) & 1u)) continue;
                     const float dx = px[k] - sa.x, dy = py[k] - sa.y;
-                    const float power = -0.5f * quad_form(sa.z, sa.w, sb.x, dx, dy);
-                    if (power > 0.0f) continue;  // alpha = 0 < tau
-                    if (power < sb.z) continue;  // provably alpha < tau
+                    const float q = (sa.z * dx * dx + sa.w * dx * dy) + sb.x * dy * dy;
+                    const uint32_t qb = __float_as_uint(q);
                     float a;
-                    if (EXACT) {
-                        a = sb.y * glibc_expf_smem(power, sTab);
+                    if (qb < qsafe) {
+                        a = sb.y * fast_exp2(q * c_ex2);
                     } else {
-                        a = sb.y * fast_exp(power);
-                        if (fabsf(a - tau) <= 1e-5f * tau || fabsf(a - aclamp) <= 1e-5f)
-                            a = sb.y * glibc_expf_smem(power, sTab);
+                        if (qb > qcut && qb <= 0x7f800000u) continue;
+                        a = exact_alpha(q, sb.y, aclamp, sTab);
+                        if (a < tau) continue;
                     }
-                    a = a < aclamp ? a : aclamp;
-                    if (a < tau) continue;
                     const float t_cur = T[k];
                     if (MAXT) atomicMax(&maxt[sG[buf][j]], __float_as_uint(t_cur));
                     const float wgt = a * t_cur;
@@ -189,65 +374,44 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
                     Cg[k] += wgt * sc.y;
                     Cb[k] += wgt * sc.z;
                     T[k] = t_cur * (1.0f - a);
-                    if (T[k] < tfloor) death = b * B + j + 1;
-                    blended = true;
+                    if (T[k] < tfloor) {
+                        live &= ~(1u << k);
+                        newly_done = true;
+                        death = b * B + j + 1;
+                    }
                 }
-                if (__any_sync(0xffffffffu, blended)) {
-                    bool all = true;
-#pragma unroll
-                    for (int k = 0; k < PPT; ++k) all = all && (!has[k] || T[k] < tfloor);
-                    done = all;
-                    if (__all_sync(0xffffffffu, done)) break;
-                }
+                if (__any_sync(0xffffffffu, newly_done) && !__any_sync(0xffffffffu, live != 0)) break;
             }
         }
-        if (__syncthreads_and(done)) break;
+        if (__syncthreads_and(live == 0)) break;
     }
     cp_async_wait<0>();
-
-    // P_it of this tile: pairs the reference iterates before `active == 0`
-    // (rasterizer.cpp:55-56): n if any pixel stays unsaturated.
     {
-        const uint32_t mine = done ? death : n;
-        const uint32_t wmax = __reduce_max_sync(0xffffffffu, mine);
+        const uint32_t wmax = __reduce_max_sync(0xffffffffu, live ? n : death);
         if (lane == 0 && wmax) atomicMax(&sPit, wmax);
         __syncthreads();
         if (tid == 0 && pit && sPit) atomicAdd(pit, static_cast<unsigned long long>(sPit));
     }
-
-    // epilogue: C + T * background, clamped (rasterizer.cpp:89-99)
-    if (t16) {
-        if (has[0]) {
-            float* o = &sOut[(ly[0] * 16 + lx[0]) * 3];
-            o[0] = sclamp(Cr[0] + T[0] * p.bg[0], 0.0f, 1.0f);
-            o[1] = sclamp(Cg[0] + T[0] * p.bg[1], 0.0f, 1.0f);
-            o[2] = sclamp(Cb[0] + T[0] * p.bg[2], 0.0f, 1.0f);
-        }
-        __syncthreads();
-        if (w == 16 && (p.W & 3) == 0) {
-            // 16 px * 3 ch = 12 float4 per row
-            if (tid < 12 * h) {
-                const int row = tid / 12, col = tid % 12;
-                float4* dst = reinterpret_cast<float4*>(
-                    image + (static_cast<size_t>(y0 + row) * p.W + x0) * 3);
-                dst[col] = reinterpret_cast<const float4*>(sOut)[row * 12 + col];
-            }
-        } else {
-            for (int i = tid; i < w * h * 3; i += 256) {
-                const int c = i % 3, pix = i / 3, row = pix / w, col = pix % w;
-                image[(static_cast<size_t>(y0 + row) * p.W + x0 + col) * 3 + c] =
-                    sOut[(row * 16 + col) * 3 + c];
-            }
-        }
-    } else {
 #pragma unroll
-        for (int k = 0; k < PPT; ++k)
-            if (has[k]) {
-                float* o = image + (static_cast<size_t>(y0 + ly[k]) * p.W + x0 + lx[k]) * 3;
-                o[0] = sclamp(Cr[k] + T[k] * p.bg[0], 0.0f, 1.0f);
-                o[1] = sclamp(Cg[k] + T[k] * p.bg[1], 0.0f, 1.0f);
-                o[2] = sclamp(Cb[k] + T[k] * p.bg[2], 0.0f, 1.0f);
-            }
+    for (int k = 0; k < PPT; ++k)
+        if (lx[k] < w && ly[k] < h) {
+            float* o = image + (static_cast<size_t>(y0 + ly[k]) * p.W + x0 + lx[k]) * 3;
+            o[0] = sclamp(Cr[k] + T[k] * p.bg[0], 0.0f, 1.0f);
+            o[1] = sclamp(Cg[k] + T[k] * p.bg[1], 0.0f, 1.0f);
+            o[2] = sclamp(Cb[k] + T[k] * p.bg[2], 0.0f, 1.0f);
+        }
+}
+
+template <int Q>
+static void launch16(bool exact, bool maxt, int grid, cudaStream_t st, const FrameParams& p, const uint2* ranges,
+                     const uint32_t* vals, const float4* P0, const float4* P1, const float4* P2, float* image,
+                     uint32_t* mt, unsigned long long* pit) {
+    if (exact) {
+        if (maxt) k_raster16<Q, true, true><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else k_raster16<Q, true, false><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+    } else {
+        if (maxt) k_raster16<Q, false, true><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else k_raster16<Q, false, false><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
     }
 }
 
@@ -267,6 +431,13 @@ static void launch_ppt(bool exact, bool maxt, int grid, cudaStream_t st, const F
 void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t st, const FrameParams& p,
                           const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
                           const float4* P2, float* image, uint32_t* maxt_buf, unsigned long long* pit) {
+    if (p.tile_size == 16) {
+        if (p.raster_ppt == 4)
+            launch16<4>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
+        else
+            launch16<2>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
+        return;
+    }
     if (ppt == 1) launch_ppt<1>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
     else if (ppt == 4) launch_ppt<4>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
     else launch_ppt<16>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);

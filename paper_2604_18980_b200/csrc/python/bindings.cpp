@@ -96,6 +96,58 @@ struct LutHolder {
     }
 };
 
+// Pool of page-locked image buffers: a returned numpy image owns one block
+// (capsule) and gives it back to the pool when the array is freed, so the
+// device->host image copy runs at full link bandwidth without re-pinning.
+class PinnedPool {
+public:
+    static PinnedPool& get() {
+        static PinnedPool* p = new PinnedPool();  // never destroyed (capsules may outlive exit order)
+        return *p;
+    }
+    void* acquire(std::size_t bytes) {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            for (auto it = free_.begin(); it != free_.end(); ++it)
+                if (it->second >= bytes && it->second <= 2 * bytes) {
+                    void* p = it->first;
+                    sizes_[p] = it->second;
+                    free_.erase(it);
+                    return p;
+                }
+        }
+        void* p = nullptr;
+        if (agsx_host_alloc(bytes, &p) != AGSX_OK) return nullptr;
+        std::lock_guard<std::mutex> g(mu_);
+        sizes_[p] = bytes;
+        return p;
+    }
+    void release(void* p) {
+        std::lock_guard<std::mutex> g(mu_);
+        auto it = sizes_.find(p);
+        if (it == sizes_.end()) return;
+        free_.emplace_back(p, it->second);
+        sizes_.erase(it);
+        while (free_.size() > 4) {  // bound the cached pinned memory
+            agsx_host_free(free_.front().first);
+            free_.erase(free_.begin());
+        }
+    }
+
+private:
+    std::mutex mu_;
+    std::vector<std::pair<void*, std::size_t>> free_;
+    std::map<void*, std::size_t> sizes_;
+};
+
+py::array_t<float> pinned_image(int h, int w) {
+    const std::size_t bytes = static_cast<std::size_t>(h) * w * 3 * sizeof(float);
+    void* p = PinnedPool::get().acquire(bytes);
+    if (!p) return py::array_t<float>({h, w, 3});  // pageable fallback for the host buffer only
+    py::capsule owner(p, [](void* q) { PinnedPool::get().release(q); });
+    return py::array_t<float>({h, w, 3}, static_cast<float*>(p), owner);
+}
+
 class Renderer {
 public:
     explicit Renderer(int device) : device_(device) {
@@ -134,7 +186,7 @@ public:
         const LutHolder lut(lut_bins, dmin, dmax);
         agsx_scene* dev = device_scene(scene);
         py::array_t<float> img;
-        if (image) img = py::array_t<float>({cam.height, cam.width, 3});
+        if (image) img = pinned_image(cam.height, cam.width);
         std::vector<float> mt;
         agsx_frame f{};
         if (image) f.image = img.mutable_data();
