@@ -5,7 +5,7 @@
  * render path of the reference (arXiv 2604.18980 reproduction under
  * /root/reference/proj).  It is the checker for the CUDA product path and is
  * itself pinned bit-for-bit against the unmodified reference build
- * (oracle/_ref/libags_ref.so) by tests/test_oracle_pin.py and against the
+ * (oracle/_ref/libags_ref.so) by tests/test_oracle.py and against the
  * committed fixtures in tests/golden/.
  *
  * Floating-point contract (the same one the reference build has):
