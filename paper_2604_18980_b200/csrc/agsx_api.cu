@@ -220,8 +220,11 @@ FrameParams make_params(const agsx_camera& cam, const agsx_config& cfg, const ag
     p.k = cfg.k;
     for (int i = 0; i < 3; ++i) p.bg[i] = cfg.background[i];
     p.flags = cfg.flags;
-    p.raster_ppt = 2;
-    if (const char* e = std::getenv("AGSX_RASTER_PPT")) p.raster_ppt = std::atoi(e) == 4 ? 4 : 2;
+    p.raster_ppt = 4;
+    if (const char* e = std::getenv("AGSX_RASTER_PPT")) {
+        const int v = std::atoi(e);
+        p.raster_ppt = (v == 2 || v == 8) ? v : 4;
+    }
     p.adaptive = cfg.mode == AGSX_MODE_ADAGSCALE ? 1 : 0;
     p.lut_dmin = 0.0f;
     p.lut_dmax = 100.0f;

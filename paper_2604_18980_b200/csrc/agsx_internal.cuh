@@ -241,13 +241,18 @@ __device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FramePa
 // Blend-side culling data for the rasterizer (not part of the reference; it
 // only lets the rasterizer skip, or take a fast path for, pixels whose
 // decision alpha >= tau is provable with a margin).  In
-// terms of q = d^T inv d (power = -0.5 q exactly):
-//   q > qcut              =>  opacity * expf(-q/2) < tau          (skip)
-//   0 <= q < qsafe        =>  opacity * expf(-q/2) >= tau, < clamp (fast)
+// terms of q = d^T inv d (power = -0.5 q exactly), for q evaluated either in
+// the reference's operation order or with the rasterizer's FMA form
+// (|q_fma - q_ref| <= rho * q, rho = 16 u kappa, kappa = (max(|xx|,|yy|) +
+// |xy|) / lambda_min, folded into both thresholds):
+//   q > qcut              =>  opacity * expf(-q/2) < tau            (skip)
+//   0 <= q < qsafe        =>  opacity * expf(-q/2) >= tau           (fast;
+//                             the blended alpha is then clamped like alpha_at)
 //   ex, ey                :  |d.x| > ex or |d.y| > ey  =>  q > qcut
-// qsafe = 0 disables the fast path (opacity >= clamp or < tau).
+// qsafe = 0 disables the fast path (opacity < tau, or kappa too large).
 __device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy, float opacity, float tau,
                                                 float aclamp, float& qcut, float& qsafe, float& ex, float& ey) {
+    (void)aclamp;
     const float inf = __int_as_float(0x7f800000);
     if (!(opacity >= tau)) {  // alpha <= opacity < tau everywhere (or NaN): never blends
         qcut = 0.0f;          // q > 0 skips; q <= 0 (or NaN) takes the exact path
@@ -255,18 +260,24 @@ __device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy,
         ex = ey = 0.0f;
         return;
     }
-    const double lr = log(static_cast<double>(opacity) / static_cast<double>(tau));  // >= 0
-    const double m = 1e-4 * (1.0 + lr);
-    qcut = __double2float_ru(2.0 * (lr + m));
-    qsafe = (opacity < aclamp && lr > m) ? __double2float_rd(2.0 * (lr - m)) : 0.0f;
-    // Box of {q <= qcut} inflated for the float evaluation error of q:
-    // q_f >= Q (1 - 64 u kappa).
     const double a = ixx, b = ixy, c = iyy;
     const double det = a * c - b * b;
     const double disc = sqrt(fmax(0.0, 0.25 * (a - c) * (a - c) + b * b));
     const double lmax = 0.5 * (a + c) + disc, lmin = 0.5 * (a + c) - disc;
+    const double lr = log(static_cast<double>(opacity) / static_cast<double>(tau));  // >= 0
+    const double m = 1e-4 * (1.0 + lr);
+    const double rho = lmin > 0.0 ? 16.0 * 0x1p-24 * (fmax(fabs(a), fabs(c)) + fabs(b)) / lmin : 1e300;
+    if (!(rho < 0.25)) {  // ill-conditioned: every pixel takes the exact path
+        qcut = inf;
+        qsafe = 0.0f;
+    } else {
+        qcut = __double2float_ru(2.0 * (lr + m) * (1.0 + rho));
+        qsafe = lr > m ? __double2float_rd(2.0 * (lr - m) * (1.0 - rho)) : 0.0f;
+    }
+    // Box of {q <= qcut} inflated for the float evaluation error of q:
+    // q_f >= Q (1 - 64 u kappa).
     const double relerr = 64.0 * 0x1p-24 * (lmin > 0.0 ? lmax / lmin : 1e300);
-    if (!(det > 0.0) || !(lmin > 0.0) || !(relerr < 0.5)) {
+    if (!(det > 0.0) || !(lmin > 0.0) || !(relerr < 0.5) || !(qcut < inf)) {
         ex = ey = inf;  // no culling for this splat
         return;
     }

@@ -124,6 +124,13 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// Hardware log2 (MUFU.LG2).
+__device__ __forceinline__ float fast_log2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Hardware exp2 (MUFU.EX2), flush-to-zero for tiny results.
 __device__ __forceinline__ float fast_exp(float x) {
     float y;

@@ -130,9 +130,10 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         py[k] = static_cast<float>(y0 + ly0 + k) + 0.5f;
-        T[k] = 1.0f;
+        const bool exists = lx < w && ly0 + k < h;
+        T[k] = exists ? 1.0f : 0.0f;  // pixels outside the image count as saturated
         Cr[k] = Cg[k] = Cb[k] = 0.0f;
-        if (lx < w && ly0 + k < h) live |= 1u << k;
+        if (exists) live |= 1u << k;
     }
     uint32_t death = 0;
     const bool warp_empty = warp * R >= h;
@@ -175,12 +176,62 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
             const float4 sa = sA[warp][j];  // mx, my, inv.xx, 2*inv.xy
             const float4 sb = sB[warp][j];  // inv.yy, opacity, qcut, qsafe
             const float4 sc = sC[warp][j];  // r, g, b, extent
-            const uint32_t qcut = __float_as_uint(sb.z);
-            const uint32_t qsafe = EXACT ? 0u : __float_as_uint(sb.w);
             // column-shared terms of ((xx*dx)*dx + ((2xy)*dx)*dy) + (yy*dy)*dy
             const float dx = px - sa.x;
             const float t1 = sa.z * dx * dx;
             const float t2 = sa.w * dx;
+            if constexpr (!EXACT && !MAXT) {
+                // Fast path, branch-free per pixel: q by FMA (its error is
+                // folded into qcut/qsafe), alpha = 2^(q c + log2 opacity)
+                // on MUFU.EX2, blended with FMAs; a = 0 for pixels that are
+                // saturated, outside the image, or not provably >= tau.
+                const uint32_t qsafe = __float_as_uint(sb.w);
+                const float qcut = sb.z;
+                const float l2op = fast_log2(sb.y);
+                uint32_t need = 0;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const float dy = py[k] - sa.y;
+                    const float q = __fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1);
+                    const bool on = T[k] >= tfloor;
+                    const bool fast = on && __float_as_uint(q) < qsafe;
+                    const float e = fminf(fast_exp2(__fmaf_rn(q, c_ex2, l2op)), aclamp);
+                    const float a = fast ? e : 0.0f;
+                    const float wgt = a * T[k];
+                    Cr[k] = __fmaf_rn(wgt, sc.x, Cr[k]);
+                    Cg[k] = __fmaf_rn(wgt, sc.y, Cg[k]);
+                    Cb[k] = __fmaf_rn(wgt, sc.z, Cb[k]);
+                    T[k] = __fmaf_rn(-a, T[k], T[k]);
+                    if (on && !fast && !(q > qcut)) need |= 1u << k;
+                }
+                if (__any_sync(0xffffffffu, need != 0)) {
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) {
+                        if (!((need >> k) & 1u)) continue;
+                        const float dy = py[k] - sa.y;
+                        const float qr = (t1 + t2 * dy) + sb.x * dy * dy;  // reference order
+                        const float a = exact_alpha(qr, sb.y, aclamp, sTab);
+                        if (a < tau) continue;
+                        const float t_cur = T[k];
+                        const float wgt = a * t_cur;
+                        Cr[k] += wgt * sc.x;
+                        Cg[k] += wgt * sc.y;
+                        Cb[k] += wgt * sc.z;
+                        T[k] = t_cur * (1.0f - a);
+                    }
+                }
+                bool dead = true;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) dead = dead && !(T[k] >= tfloor);
+                if (__all_sync(0xffffffffu, dead)) {
+                    death = base - start + j + 1;
+                    live = 0;
+                    all_done = true;
+                    break;
+                }
+            } else {
+            const uint32_t qcut = __float_as_uint(sb.z);
+            const uint32_t qsafe = EXACT ? 0u : __float_as_uint(sb.w);
             float q[PPT];
             uint32_t need = 0;
             bool newly_done = false;
@@ -205,7 +256,7 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
                 const uint32_t qb = __float_as_uint(q[k]);
                 const bool on = (live >> k) & 1u;
                 if (on && qb < qsafe) {
-                    blend(k, sb.y * fast_exp2(q[k] * c_ex2));
+                    blend(k, fminf(sb.y * fast_exp2(q[k] * c_ex2), aclamp));
                 } else if (on && !(qb > qcut && qb <= 0x7f800000u)) {
                     need |= 1u << k;
                 }
@@ -221,6 +272,7 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
             if (__any_sync(0xffffffffu, newly_done) && !__any_sync(0xffffffffu, live != 0)) {
                 all_done = true;
                 break;
+            }
             }
         }
         __syncwarp();
@@ -361,7 +413,7 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
                     const uint32_t qb = __float_as_uint(q);
                     float a;
                     if (qb < qsafe) {
-                        a = sb.y * fast_exp2(q * c_ex2);
+                        a = fminf(sb.y * fast_exp2(q * c_ex2), aclamp);
                     } else {
                         if (qb > qcut && qb <= 0x7f800000u) continue;
                         a = exact_alpha(q, sb.y, aclamp, sTab);
@@ -432,7 +484,9 @@ void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t
                           const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
                           const float4* P2, float* image, uint32_t* maxt_buf, unsigned long long* pit) {
     if (p.tile_size == 16) {
-        if (p.raster_ppt == 4)
+        if (p.raster_ppt == 8)
+            launch16<8>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
+        else if (p.raster_ppt == 4)
             launch16<4>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
         else
             launch16<2>(exact, maxt, grid, st, p, ranges, vals, P0, P1, P2, image, maxt_buf, pit);
