@@ -74,7 +74,7 @@ struct agsx_ctx {
     uint32_t epoch = 1;
     int num_sms = 148;
     int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1;
-    Buf sort_counts;  // grid x 256 per-chunk digit counts (one pass at a time)
+    Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
     // device arenas (grow-only)
     Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2;
@@ -265,22 +265,34 @@ size_t sort_smem(bool k64) {
            (kSortThreads / 32) * 256 * 4;
 }
 
-constexpr int kTotalsSlots = 16;  // zeroed 256-bin totals per sort pass (frame memset)
-size_t counters_bytes() { return sizeof(Counters) + kTotalsSlots * 256 * 4; }
+size_t counters_bytes() { return sizeof(Counters); }
 
 int sort_grid(agsx_ctx* ctx, bool k64) { return ctx->num_sms * (k64 ? ctx->occ_sort64 : ctx->occ_sort32); }
 
-// One stable LSD pass; `slot` selects the zeroed totals array.
+// Histograms of the low `npasses` digits of n keys (hist zeroed by the caller).
+template <typename K>
+void sort_hist(agsx_ctx* ctx, const K* keys, const uint32_t* n_dev, uint64_t n_host, int npasses, bool sentinel,
+               uint32_t* hist) {
+    const int grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>((n_host + 127) / 128, static_cast<uint64_t>(ctx->num_sms) * 8)));
+    launch_hist<K>(grid, ctx->stream, keys, n_dev, n_host, npasses, sentinel, static_cast<K>(~K(0)), hist);
+    check_launch(ctx);
+}
+
+// One stable LSD pass over at most n_host keys (three kernels).
 template <typename K>
 void sort_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, const uint32_t* n_dev,
-               uint64_t n_host, int shift, bool sentinel, uint32_t* totals, uint32_t* n_out) {
+               uint64_t n_host, int shift, bool sentinel, uint32_t* n_out) {
     const bool k64 = sizeof(K) == 8;
-    const int grid = sort_grid(ctx, k64);
-    ensure(ctx->sort_counts, static_cast<size_t>(grid) * 256 * 4);
+    const uint64_t tiles = (n_host + kSortTile - 1) / kSortTile;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(
+        tiles, std::min(sort_grid(ctx, k64), 1024))));
+    ensure(ctx->sort_counts, static_cast<size_t>(grid) * 256 * 4 + 256 * 4);
+    uint32_t* counts = ptr<uint32_t>(ctx->sort_counts);
     launch_sort_pass<K>(grid, sort_smem(k64), ctx->stream, kin, vin, kout, vout, n_dev, n_host, shift, sentinel,
-                        static_cast<K>(~K(0)), ptr<uint32_t>(ctx->sort_counts), totals, n_out);
+                        static_cast<K>(~K(0)), counts, counts + static_cast<size_t>(grid) * 256, n_out);
     check_launch(ctx);
-    ctx->launches += 1;  // two kernels per pass
+    ctx->launches += 2;  // three kernels per pass
 }
 
 void ensure_lb(agsx_ctx* ctx, uint64_t max_elems) {
@@ -357,7 +369,6 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     const uint64_t n = sc->n;
     const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
     Counters* ctr = ptr<Counters>(ctx->ctr);
-    uint32_t* totals = reinterpret_cast<uint32_t*>(ctr + 1);  // kTotalsSlots x 256
     cudaStream_t st = ctx->stream;
     ctx->ev = ctx->ev_ring[ctx->frames % agsx_ctx::kRing];
     ++ctx->frames;
@@ -374,15 +385,16 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[1], st));
-    // K4a: stable sort by depth bits (4 x 8-bit); pass 0 drops the sentinel
-    // keys of splats without tiles (the ordered compaction) and sets m.
+    // K4a: stable sort by depth bits (4 x 8-bit, histograms in one read);
+    // pass 0 drops the sentinel keys of splats without tiles (the ordered
+    // compaction) and sets m.
     uint32_t* dk[2] = {ptr<uint32_t>(ctx->dkeys), ptr<uint32_t>(ctx->dkeys2)};
     uint32_t* dv[2] = {ptr<uint32_t>(ctx->dvals), ptr<uint32_t>(ctx->dvals2)};
     if (n > 0) {
-        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, totals, &ctr->m);
+        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m);
         for (int ps = 1; ps < 4; ++ps)
-            sort_pass<uint32_t>(ctx, dk[ps & 1], dv[ps & 1], dk[(ps + 1) & 1], dv[(ps + 1) & 1], &ctr->m, 0, 8 * ps,
-                                false, totals + 256 * ps, nullptr);
+            sort_pass<uint32_t>(ctx, dk[ps & 1], dv[ps & 1], dk[(ps + 1) & 1], dv[(ps + 1) & 1], &ctr->m, n, 8 * ps,
+                                false, nullptr);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[2], st));
     // K3: scan + emit in depth order
@@ -400,11 +412,11 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     int cur = 0;
     if (n > 0) {
         for (int ps = 0; ps < passes; ++ps) {
-            sort_pass<uint32_t>(ctx, tk[cur], pv[cur], tk[cur ^ 1], pv[cur ^ 1], &ctr->p_eff, 0, 8 * ps, false,
-                                totals + 256 * (4 + ps), nullptr);
+            sort_pass<uint32_t>(ctx, tk[cur], pv[cur], tk[cur ^ 1], pv[cur ^ 1], &ctr->p_eff, ctx->pair_capacity,
+                                8 * ps, false, nullptr);
             cur ^= 1;
         }
-        k_ranges_u32<<<ctx->num_sms * 4, 256, 0, st>>>(tk[cur], &ctr->p_eff, ptr<uint2>(ctx->ranges));
+        k_ranges_u32<<<ctx->num_sms * 8, 256, 0, st>>>(tk[cur], &ctr->p_eff, ptr<uint2>(ctx->ranges));
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
@@ -873,12 +885,12 @@ int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64
         ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 8);
         ensure(ctx->tmp2, std::max<uint64_t>(n, 1) * 4);
         ensure(ctx->tmp3, std::max<uint64_t>(n, 1) * 4);
-        ensure(ctx->hist, 2 * 8 * 256 * 4);
+        ensure(ctx->hist, 9 * 256 * 4);
         ensure(ctx->ranges, std::max<int>(tile_count, 1) * 8);
+        ensure_lb(ctx, n);
         uint32_t* hist = ptr<uint32_t>(ctx->hist);
-        uint32_t* totals = hist + 8 * 256;
         cudaStream_t st = ctx->stream;
-        AGSX_CUDA(cudaMemsetAsync(ctx->hist.p, 0, 2 * 8 * 256 * 4, st));
+        AGSX_CUDA(cudaMemsetAsync(ctx->hist.p, 0, 9 * 256 * 4, st));
         if (tile_count) AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, static_cast<size_t>(tile_count) * 8, st));
         uint64_t* k[2] = {ptr<uint64_t>(ctx->tmp0), ptr<uint64_t>(ctx->tmp1)};
         uint32_t* v[2] = {ptr<uint32_t>(ctx->tmp2), ptr<uint32_t>(ctx->tmp3)};
@@ -886,9 +898,7 @@ int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64
         if (n) {
             AGSX_CUDA(cudaMemcpyAsync(k[0], keys, n * 8, cudaMemcpyHostToDevice, st));
             AGSX_CUDA(cudaMemcpyAsync(v[0], splat_index, n * 4, cudaMemcpyHostToDevice, st));
-            const int hgrid = static_cast<int>(std::min<uint64_t>((n + 255) / 256, ctx->num_sms * 4));
-            launch_hist64(hgrid, st, k[0], n, 8, hist);
-            check_launch(ctx);
+            sort_hist<uint64_t>(ctx, k[0], nullptr, n, 8, false, hist);
             std::vector<uint32_t> h(8 * 256);
             AGSX_CUDA(cudaMemcpyAsync(h.data(), hist, h.size() * 4, cudaMemcpyDeviceToHost, st));
             AGSX_CUDA(cudaStreamSynchronize(st));
@@ -898,7 +908,7 @@ int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64
                 for (int d = 0; d < 256; ++d) trivial = trivial || h[ps * 256 + d] == n;
                 if (trivial) continue;
                 sort_pass<uint64_t>(ctx, k[cur], v[cur], k[cur ^ 1], v[cur ^ 1], nullptr, n, 8 * ps, false,
-                                    totals + 256 * ps, nullptr);
+                                    nullptr);
                 cur ^= 1;
             }
             if (tile_count) {

@@ -156,13 +156,32 @@ __global__ void k_emit_list(FrameParams p, uint64_t n, SplatPlanes pl,
 
 // ranges[tile] = [first, last+1) over the tile-sorted pair list; tiles
 // without pairs keep the {0,0} written by the frame memset.
-__global__ void k_ranges_u32(const uint32_t* __restrict__ keys, const uint32_t* n_dev,
-                             uint2* __restrict__ ranges) {
+__global__ void __launch_bounds__(256)
+k_ranges_u32(const uint32_t* __restrict__ keys, const uint32_t* n_dev, uint2* __restrict__ ranges) {
     const uint32_t n = *n_dev;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t t = keys[i];
-        if (i == 0 || keys[i - 1] != t) ranges[t].x = i;
-        if (i == n - 1 || keys[i + 1] != t) ranges[t].y = i + 1;
+    const uint32_t nq = (n + 3) / 4;  // 16-byte groups (the key buffer is 16-byte aligned)
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nq; g += gridDim.x * blockDim.x) {
+        const uint32_t i0 = 4 * g;
+        uint32_t k[6];
+        if (i0 + 4 <= n) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(keys) + g);
+            k[1] = v.x;
+            k[2] = v.y;
+            k[3] = v.z;
+            k[4] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) k[1 + j] = i0 + j < n ? keys[i0 + j] : 0xffffffffu;
+        }
+        k[0] = i0 > 0 ? __ldg(&keys[i0 - 1]) : 0xffffffffu;
+        k[5] = i0 + 4 < n ? __ldg(&keys[i0 + 4]) : 0xffffffffu;
+#pragma unroll
+        for (int j = 1; j <= 4; ++j) {
+            const uint32_t i = i0 + j - 1;
+            if (i >= n) break;
+            if (k[j - 1] != k[j] || i == 0) ranges[k[j]].x = i;
+            if (k[j + 1] != k[j] || i == n - 1) ranges[k[j]].y = i + 1;
+        }
     }
 }
 

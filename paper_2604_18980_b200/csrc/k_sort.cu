@@ -3,13 +3,11 @@
 //   reference: sort_pairs pair_sort.cpp:7-44 (stable LSD, 8-bit digits,
 //              8 passes over the 64-bit key, single-threaded)
 //
-// A pass is two kernels over G contiguous chunks (one CTA per chunk):
-//   upsweep   : per-chunk 256-bin digit histogram -> counts[c][d];
-//   downsweep : each CTA derives its global digit bases from the count
-//               matrix (column prefix + digit totals, no serial chains),
-//               then walks its chunk in 4096-key tiles: warp multisplit
-//               ranking (__match_any_sync) stable in input order, shared-
-//               memory staging, contiguous per-digit runs to global memory.
+// A pass is three kernels over G contiguous chunks (one CTA per chunk):
+//   upsweep    : per-chunk digit counts -> counts[c][d];
+//   scan       : column prefix of the count matrix + digit totals;
+//   downsweep  : per 2048-key tile: warp-multisplit ranking stable in input
+//                order, shared-memory staging, contiguous per-digit runs.
 // Keys equal to `sentinel` (when enabled) are dropped by the pass: the first
 // depth pass compacts the per-Gaussian key array this way.  `vin == nullptr`
 // means value = input index.  The element count may live on the device.
@@ -40,6 +38,8 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp
     return wbase + incl - v;
 }
 
+}  // namespace
+
 __device__ __forceinline__ void chunk_of(uint64_t n, int G, int c, uint64_t& lo, uint64_t& hi) {
     // chunk length rounded up to whole tiles so every tile but the last is full
     const uint64_t tiles = (n + kSortTile - 1) / kSortTile;
@@ -48,47 +48,88 @@ __device__ __forceinline__ void chunk_of(uint64_t n, int G, int c, uint64_t& lo,
     hi = min(n, lo + per * kSortTile);
 }
 
-}  // namespace
-
+// Upsweep: per-chunk 256-bin digit counts -> counts[c][d] (warp-private
+// shared histograms; a warp whose 32 digits agree adds once).
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
-          K sentinel, uint32_t* __restrict__ counts, uint32_t* __restrict__ totals) {
-    __shared__ uint32_t hist[256];
-    const int tid = threadIdx.x, lane = tid & 31;
-    hist[tid] = 0;
+          K sentinel, uint32_t* __restrict__ counts) {
+    constexpr int W = kSortThreads / 32;
+    __shared__ uint32_t sh[W][256];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < W * 256; i += kSortThreads) (&sh[0][0])[i] = 0;
     __syncthreads();
     const uint64_t n = n_dev ? *n_dev : n_host;
     uint64_t lo, hi;
     chunk_of(n, gridDim.x, blockIdx.x, lo, hi);
-    constexpr int U = 16;  // keys in flight per thread
+    constexpr int U = 8;  // keys in flight per thread
     for (uint64_t base = lo; base < hi; base += U * kSortThreads) {
         K k[U];
-        bool valid[U];
+        bool ok[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = base + u * kSortThreads + tid;
-            valid[u] = i < hi;
-            k[u] = valid[u] ? keys[i] : K(0);
+            k[u] = i < hi ? keys[i] : K(0);
+            ok[u] = i < hi && !(use_sentinel && k[u] == sentinel);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const bool ok = valid[u] && !(use_sentinel && k[u] == sentinel);
+            const uint32_t vmask = __ballot_sync(0xffffffffu, ok[u]);
+            if (!vmask) continue;
             const uint32_t d = digit_of(k[u], shift);
-            const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : 0x100u + lane);
-            if (ok && (__ffs(peers) - 1) == lane) atomicAdd(&hist[d], __popc(peers));
+            const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(vmask) - 1);
+            if (__all_sync(0xffffffffu, !ok[u] || d == d0)) {
+                if (lane == 0) sh[warp][d0] += __popc(vmask);
+            } else if (ok[u]) {
+                atomicAdd(&sh[warp][d], 1u);
+            }
         }
     }
     __syncthreads();
-    counts[static_cast<uint64_t>(blockIdx.x) * 256 + tid] = hist[tid];
-    if (hist[tid]) atomicAdd(&totals[tid], hist[tid]);
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) c += sh[w][tid];
+    counts[static_cast<uint64_t>(blockIdx.x) * 256 + tid] = c;
 }
 
+// Column scan of the G x 256 count matrix (one block per digit, G <= 1024
+// threads): counts[c][d] <- sum_{c' < c} counts[c'][d]; totals[d] = column sum.
+__global__ void __launch_bounds__(1024)
+k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ totals) {
+    __shared__ uint32_t s_warp[32];
+    const int d = blockIdx.x, c = threadIdx.x, lane = c & 31, warp = c >> 5;
+    const uint32_t v = c < G ? counts[static_cast<uint64_t>(c) * 256 + d] : 0u;
+    uint32_t incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (blockDim.x + 31) / 32;
+        const uint32_t x = lane < nw ? s_warp[lane] : 0u;
+        uint32_t xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += t;
+        }
+        if (lane < nw) s_warp[lane] = xi - x;
+        if (lane == nw - 1) totals[d] = xi;
+    }
+    __syncthreads();
+    if (c < G) counts[static_cast<uint64_t>(c) * 256 + d] = s_warp[warp] + incl - v;
+}
+
+// Downsweep: CTA c walks its chunk in kSortTile-key tiles: warp multisplit
+// ranking (__match_any_sync; stable in input order), shared-memory staging,
+// contiguous per-digit runs to global memory at base[d] = (digits below d)
+// + (earlier chunks' digit-d keys) + (earlier tiles of this chunk).
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, 3)
 k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
             uint32_t* __restrict__ vout, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
-            K sentinel, const uint32_t* __restrict__ counts, const uint32_t* __restrict__ totals,
+            K sentinel, const uint32_t* __restrict__ counts_excl, const uint32_t* __restrict__ totals,
             uint32_t* n_out) {
     constexpr int W = kSortThreads / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -96,23 +137,20 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     uint32_t* s_vals = reinterpret_cast<uint32_t*>(s_keys + kSortTile);
     uint32_t(*s_whist)[256] = reinterpret_cast<uint32_t(*)[256]>(s_vals + kSortTile);
     __shared__ uint32_t s_base[256], s_texcl[256], s_pos[256], s_scan[W];
+    __shared__ uint32_t s_tile_n;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int G = gridDim.x, c = blockIdx.x;
+    const int c = blockIdx.x;
     const uint64_t n = n_dev ? *n_dev : n_host;
 
-    // global base of digit `tid` for this chunk: digits below + earlier chunks
     const uint32_t total = totals[tid];
-    uint32_t before = 0;
-#pragma unroll 8
-    for (int cc = 0; cc < c; ++cc) before += counts[static_cast<uint64_t>(cc) * 256 + tid];
     const uint32_t dexcl = block_excl_scan(total, s_scan);
-    s_base[tid] = dexcl + before;
-    if (c == 0 && tid == 255 && n_out) *n_out = dexcl + total;  // surviving keys
+    s_base[tid] = dexcl + counts_excl[static_cast<uint64_t>(c) * 256 + tid];
+    if (c == 0 && tid == 255 && n_out) *n_out = dexcl + total;  // keys kept
     __syncthreads();
 
     uint64_t lo, hi;
-    chunk_of(n, G, c, lo, hi);
+    chunk_of(n, gridDim.x, c, lo, hi);
     for (uint64_t tbase = lo; tbase < hi; tbase += kSortTile) {
         K k[kSortItems];
         uint32_t v[kSortItems];
@@ -153,6 +191,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         const uint32_t texcl = block_excl_scan(count, s_scan);
         s_texcl[tid] = texcl;
         s_pos[tid] = s_base[tid] - texcl;  // output = s_pos[d] + tile-sorted index
+        if (tid == kSortThreads - 1) s_tile_n = texcl + count;
         __syncthreads();
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
@@ -164,11 +203,8 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             }
         }
         __syncthreads();
-        const uint32_t tile_n = texcl + count;  // valid keys in this tile (thread 255 holds it)
-        __shared__ uint32_t s_tile_n;
-        if (tid == kSortThreads - 1) s_tile_n = tile_n;
-        __syncthreads();
-        for (uint32_t i = tid; i < s_tile_n; i += kSortThreads) {
+        const uint32_t tn = s_tile_n;
+        for (uint32_t i = tid; i < tn; i += kSortThreads) {
             const K key = s_keys[i];
             const uint32_t pos = s_pos[digit_of(key, shift)] + i;
             kout[pos] = key;
@@ -183,8 +219,8 @@ template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
                       uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift, bool use_sentinel,
                       K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out) {
-    k_upsweep<K><<<grid, kSortThreads, 0, st>>>(kin, n_dev, n_host, shift, use_sentinel ? 1 : 0, sentinel, counts,
-                                                totals);
+    k_upsweep<K><<<grid, kSortThreads, 0, st>>>(kin, n_dev, n_host, shift, use_sentinel ? 1 : 0, sentinel, counts);
+    k_scan_counts<<<256, (grid + 31) / 32 * 32, 0, st>>>(counts, grid, totals);
     k_downsweep<K><<<grid, kSortThreads, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, shift,
                                                      use_sentinel ? 1 : 0, sentinel, counts, totals, n_out);
 }
@@ -206,35 +242,64 @@ template void launch_sort_pass<uint64_t>(int, size_t, cudaStream_t, const uint64
 template cudaError_t sort_configure<uint32_t>(size_t, int*);
 template cudaError_t sort_configure<uint64_t>(size_t, int*);
 
-// Digit histograms of all passes in one read (standalone sort: skip passes
-// whose digit is shared by every key).
+// Digit histograms of `npasses` consecutive 8-bit digits (from bit 0) in one
+// read; keys equal to `sentinel` (when enabled) are not counted.  The key
+// count may live on the device.
 template <typename K>
-__global__ void __launch_bounds__(256)
-k_hist(const K* __restrict__ keys, uint64_t n, int npasses, uint32_t* __restrict__ hist) {
-    __shared__ uint32_t sh[8][256];
-    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&sh[0][0])[i] = 0;
+__global__ void __launch_bounds__(128)
+k_hist(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, int npasses, int use_sentinel,
+       K sentinel, uint32_t* __restrict__ hist) {
+    // per-warp sub-histograms; a warp whose 32 digits agree adds once
+    __shared__ uint32_t sh[4][8][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 4 * 8 * 256; i += blockDim.x) (&sh[0][0][0])[i] = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x; base < n;
-         base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t i = base + threadIdx.x;
-        const bool valid = i < n;
-        const K k = valid ? keys[i] : K(0);
-        for (int ps = 0; ps < npasses; ++ps) {
-            const uint32_t d = digit_of(k, 8 * ps);
-            const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 0x100u + lane);
-            if (valid && (__ffs(peers) - 1) == lane) atomicAdd(&sh[ps][d], __popc(peers));
+    const uint64_t n = n_dev ? *n_dev : n_host;
+    constexpr int U = 4;  // keys in flight per thread
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x * U;
+    for (uint64_t base = static_cast<uint64_t>(blockIdx.x) * blockDim.x * U; base < n; base += stride) {
+        K kk[U];
+        bool vv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = base + u * blockDim.x + threadIdx.x;
+            kk[u] = i < n ? keys[i] : K(0);
+            vv[u] = i < n && !(use_sentinel && kk[u] == sentinel);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const K k = kk[u];
+            const bool valid = vv[u];
+            const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+            if (!vmask) continue;
+            for (int ps = 0; ps < npasses; ++ps) {
+                const uint32_t d = digit_of(k, 8 * ps);
+                const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(vmask) - 1);
+                if (__all_sync(0xffffffffu, !valid || d == d0)) {
+                    if (lane == 0) sh[warp][ps][d0] += __popc(vmask);
+                } else if (valid) {
+                    atomicAdd(&sh[warp][ps][d], 1u);
+                }
+            }
         }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < npasses * 256; i += blockDim.x) {
-        const uint32_t c = (&sh[0][0])[i];
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) c += (&sh[w][0][0])[i];
         if (c) atomicAdd(&hist[i], c);
     }
 }
 
-void launch_hist64(int grid, cudaStream_t st, const uint64_t* keys, uint64_t n, int npasses, uint32_t* hist) {
-    k_hist<uint64_t><<<grid, 256, 0, st>>>(keys, n, npasses, hist);
+template <typename K>
+void launch_hist(int grid, cudaStream_t st, const K* keys, const uint32_t* n_dev, uint64_t n_host, int npasses,
+                 bool use_sentinel, K sentinel, uint32_t* hist) {
+    k_hist<K><<<grid, 128, 0, st>>>(keys, n_dev, n_host, npasses, use_sentinel ? 1 : 0, sentinel, hist);
 }
+template void launch_hist<uint32_t>(int, cudaStream_t, const uint32_t*, const uint32_t*, uint64_t, int, bool,
+                                    uint32_t, uint32_t*);
+template void launch_hist<uint64_t>(int, cudaStream_t, const uint64_t*, const uint32_t*, uint64_t, int, bool,
+                                    uint64_t, uint32_t*);
 
 }  // namespace agsx

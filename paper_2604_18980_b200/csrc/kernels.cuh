@@ -5,7 +5,7 @@
 namespace agsx {
 
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 16;
+constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;  // keys per onesweep tile
 
 __global__ void k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* status,
@@ -28,16 +28,21 @@ __global__ void k_ranges_u64(const uint64_t* keys, uint64_t n, uint32_t tile_cou
 // Templated kernels are launched through host functions defined in the
 // translation unit that instantiates them (a template kernel's host stub is
 // only registered there).
-// One stable LSD pass (upsweep + downsweep) over `grid` chunks.  counts:
-// grid*256 u32 scratch; totals: 256 u32, zeroed before the pass; n_out
-// (optional) receives the number of keys kept (sentinels dropped).
+// One stable LSD pass over digit (key >> shift) & 0xff: upsweep + column
+// scan + downsweep over `grid` (<= 1024) chunks.  counts: grid*256 u32
+// scratch; totals: 256 u32 scratch.  n_out (optional) receives the number of
+// keys kept (sentinels dropped).
 template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
                       uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift, bool use_sentinel,
                       K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out);
 template <typename K>
 cudaError_t sort_configure(size_t smem, int* occupancy);
-void launch_hist64(int grid, cudaStream_t st, const uint64_t* keys, uint64_t n, int npasses, uint32_t* hist);
+// Histograms of the low `npasses` 8-bit digits into hist[npasses][256]
+// (accumulated; zero it first).
+template <typename K>
+void launch_hist(int grid, cudaStream_t st, const K* keys, const uint32_t* n_dev, uint64_t n_host, int npasses,
+                 bool use_sentinel, K sentinel, uint32_t* hist);
 
 void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t st, const FrameParams& p,
                           const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
