@@ -73,13 +73,13 @@ struct agsx_ctx {
     uint64_t launches = 0;
     uint32_t epoch = 1;
     int num_sms = 148;
-    int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1;
+    int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1, occ_raster = 1;
     Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
     // device arenas (grow-only)
     Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2;
     Buf tkeys, pvals, tkeys2, pvals2;
-    Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext;
+    Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext, tile_pit;
     Buf tmp0, tmp1, tmp2, tmp3, tmp4;
     uint64_t pair_capacity = 0;
 
@@ -251,12 +251,21 @@ int raster_ppt(int tile_size) {
 
 void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
                    const float4* P0, const float4* P1, const float4* P2, float* image,
-                   uint32_t* maxt, unsigned long long* pit) {
+                   uint32_t* maxt, Counters* ctr) {
     const int grid = p.tiles_x * p.tiles_y;
     if (grid == 0) return;
     const bool exact = (p.flags & AGSX_FLAG_EXACT_ALPHA) != 0;
+    if (p.tile_size == 16 && !exact && maxt == nullptr && p.raster_ppt == 4) {
+        // default path: warp-persistent units (half tiles); per-tile P_it words
+        ensure(ctx->tile_pit, static_cast<size_t>(grid) * 8);
+        AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, static_cast<size_t>(grid) * 8, ctx->stream));
+        launch_raster_units(ctx->num_sms * ctx->occ_raster, ctx->stream, p, ranges, vals, P0, P1, P2, image,
+                            &ctr->tile_ctr[3], ptr<unsigned long long>(ctx->tile_pit), &ctr->p_it, ctr->dbg);
+        check_launch(ctx);
+        return;
+    }
     launch_raster_kernel(raster_ppt(p.tile_size), exact, maxt != nullptr, grid, ctx->stream, p, ranges, vals,
-                         P0, P1, P2, image, maxt, pit);
+                         P0, P1, P2, image, maxt, &ctr->p_it);
     check_launch(ctx);
 }
 
@@ -422,7 +431,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
     // K6
     launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ptr<float>(ctx->image),
-                  maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, &ctr->p_it);
+                  maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
     AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
     AGSX_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     ctx->f_tkeys = tk[cur];
@@ -526,6 +535,8 @@ int agsx_create(int device, agsx_ctx** out) {
         AGSX_CUDA(sort_configure<uint32_t>(sort_smem(false), &ctx->occ_sort32));
         AGSX_CUDA(sort_configure<uint64_t>(sort_smem(true), &ctx->occ_sort64));
         AGSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ_emit, k_emit, 256, 0));
+        AGSX_CUDA(raster_units_occupancy(&ctx->occ_raster));
+        ctx->occ_raster = std::max(ctx->occ_raster, 1);
         ctx->occ_sort32 = std::max(ctx->occ_sort32, 1);
         ctx->occ_sort64 = std::max(ctx->occ_sort64, 1);
         ctx->occ_emit = std::max(ctx->occ_emit, 1);
@@ -551,7 +562,7 @@ void agsx_destroy(agsx_ctx* ctx) {
     for (Buf* b : {&ctx->status, &ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4, &ctx->dkeys,
                    &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
                    &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
-                   &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
+                   &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tile_pit, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
                    &ctx->tmp3, &ctx->tmp4})
         release(*b);
     for (auto& set : ctx->ev_ring)
@@ -693,8 +704,9 @@ int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n) {
     return guarded(ctx, [&]() -> int {
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         const Counters c = *ctx->h_ctr;
-        const uint64_t v[6] = {c.s, c.m, c.p, c.p_it, c.overflow, static_cast<uint64_t>(ctx->f_tile_count)};
-        for (int i = 0; i < n && i < 6; ++i) stats[i] = v[i];
+        const uint64_t v[10] = {c.s, c.m, c.p, c.p_it, c.overflow, static_cast<uint64_t>(ctx->f_tile_count),
+                                c.dbg[0], c.dbg[1], c.dbg[2], c.dbg[3]};
+        for (int i = 0; i < n && i < 10; ++i) stats[i] = v[i];
         return AGSX_OK;
     });
 }
@@ -965,8 +977,11 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
             AGSX_CUDA(cudaMemcpyAsync(ctx->tmp3.p, splat_index, n_pairs * 4, cudaMemcpyHostToDevice, st));
         AGSX_CUDA(cudaMemcpyAsync(ctx->tmp4.p, ranges, tiles * 8, cudaMemcpyHostToDevice, st));
         if (max_t) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, std::max<uint64_t>(n_splats, 1) * 4, st));
+        ensure(ctx->ctr, counters_bytes());
+        AGSX_CUDA(cudaMemsetAsync(ctx->ctr.p, 0, counters_bytes(), st));
+        Counters* ctr = ptr<Counters>(ctx->ctr);
         launch_raster(ctx, p, ptr<uint2>(ctx->tmp4), ptr<uint32_t>(ctx->tmp3), pl.p0, pl.p1, pl.p2,
-                      ptr<float>(ctx->image), max_t ? ptr<uint32_t>(ctx->maxt) : nullptr, nullptr);
+                      ptr<float>(ctx->image), max_t ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
         AGSX_CUDA(cudaMemcpyAsync(image, ctx->image.p, static_cast<size_t>(width) * height * 12,
                                   cudaMemcpyDeviceToHost, st));
         if (max_t && n_splats)

@@ -249,14 +249,16 @@ __device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FramePa
 //   0 <= q < qsafe        =>  opacity * expf(-q/2) >= tau           (fast;
 //                             the blended alpha is then clamped like alpha_at)
 //   ex, ey                :  |d.x| > ex or |d.y| > ey  =>  q > qcut
-// qsafe = 0 disables the fast path (opacity < tau, or kappa too large).
+// qsafe = -inf disables the fast path (opacity < tau, or kappa too large).
+// For rho < 1/4 neither q form can be negative (their error is below q), so
+// the fast test needs no sign check.
 __device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy, float opacity, float tau,
                                                 float aclamp, float& qcut, float& qsafe, float& ex, float& ey) {
     (void)aclamp;
     const float inf = __int_as_float(0x7f800000);
     if (!(opacity >= tau)) {  // alpha <= opacity < tau everywhere (or NaN): never blends
         qcut = 0.0f;          // q > 0 skips; q <= 0 (or NaN) takes the exact path
-        qsafe = 0.0f;
+        qsafe = -inf;
         ex = ey = 0.0f;
         return;
     }
@@ -269,10 +271,10 @@ __device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy,
     const double rho = lmin > 0.0 ? 16.0 * 0x1p-24 * (fmax(fabs(a), fabs(c)) + fabs(b)) / lmin : 1e300;
     if (!(rho < 0.25)) {  // ill-conditioned: every pixel takes the exact path
         qcut = inf;
-        qsafe = 0.0f;
+        qsafe = -inf;
     } else {
         qcut = __double2float_ru(2.0 * (lr + m) * (1.0 + rho));
-        qsafe = lr > m ? __double2float_rd(2.0 * (lr - m) * (1.0 - rho)) : 0.0f;
+        qsafe = lr > m ? __double2float_rd(2.0 * (lr - m) * (1.0 - rho)) : -inf;
     }
     // Box of {q <= qcut} inflated for the float evaluation error of q:
     // q_f >= Q (1 - 64 u kappa).
@@ -362,7 +364,7 @@ struct Counters {
     uint32_t p_eff;         // p if it fits the pair buffers, else 0 (memory safety)
     uint32_t pad0;
     unsigned long long p_it;  // pairs iterated before tile saturation (raster work)
-    uint32_t pad[8];
+    unsigned long long dbg[4];  // raster work counters (AGSX_RASTER_STATS=1)
 };
 
 }  // namespace agsx

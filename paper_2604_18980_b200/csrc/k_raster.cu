@@ -16,6 +16,8 @@
 // contraction; alpha uses either the glibc-exact expf or MUFU.EX2 with an
 // exact re-evaluation inside a guard band around tau and the clamp.
 // The tile is written as float4 rows of the HWC image.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace agsx {
@@ -185,7 +187,7 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
                 // folded into qcut/qsafe), alpha = 2^(q c + log2 opacity)
                 // on MUFU.EX2, blended with FMAs; a = 0 for pixels that are
                 // saturated, outside the image, or not provably >= tau.
-                const uint32_t qsafe = __float_as_uint(sb.w);
+                const float qsafe = sb.w;
                 const float qcut = sb.z;
                 const float l2op = fast_log2(sb.y);
                 uint32_t need = 0;
@@ -194,7 +196,7 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
                     const float dy = py[k] - sa.y;
                     const float q = __fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1);
                     const bool on = T[k] >= tfloor;
-                    const bool fast = on && __float_as_uint(q) < qsafe;
+                    const bool fast = on && q < qsafe;
                     const float e = fminf(fast_exp2(__fmaf_rn(q, c_ex2, l2op)), aclamp);
                     const float a = fast ? e : 0.0f;
                     const float wgt = a * T[k];
@@ -231,7 +233,7 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
                 }
             } else {
             const uint32_t qcut = __float_as_uint(sb.z);
-            const uint32_t qsafe = EXACT ? 0u : __float_as_uint(sb.w);
+            const float qsafe = EXACT ? -__int_as_float(0x7f800000) : sb.w;
             float q[PPT];
             uint32_t need = 0;
             bool newly_done = false;
@@ -255,7 +257,7 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
                 q[k] = (t1 + t2 * dy) + sb.x * dy * dy;
                 const uint32_t qb = __float_as_uint(q[k]);
                 const bool on = (live >> k) & 1u;
-                if (on && qb < qsafe) {
+                if (on && q[k] >= 0.0f && q[k] < qsafe) {
                     blend(k, fminf(sb.y * fast_exp2(q[k] * c_ex2), aclamp));
                 } else if (on && !(qb > qcut && qb <= 0x7f800000u)) {
                     need |= 1u << k;
@@ -308,6 +310,276 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
             image[(static_cast<size_t>(y0 + row) * p.W + x0 + col) * 3 + c] = sOut[(row * 16 + col) * 3 + c];
         }
     }
+}
+
+// Exact cull of one splat against a warp's pixel-centre rectangle: true when
+// min over the rectangle of Q = d^T inv d exceeds qcut (with margins for the
+// float evaluation of the reference's d and q), so no pixel of the rectangle
+// can reach alpha >= tau.  Evaluated in double by one lane per splat.
+__device__ __forceinline__ bool rect_outside(float4 a, float iyy, float qcut, float x0, float x1, float y0,
+                                             float y1) {
+    const double xx = a.z, xy = 0.5 * static_cast<double>(a.w), yy = iyy;
+    const double cx = a.x, cy = a.y;
+    if (!(qcut < __int_as_float(0x7f800000))) return false;
+    if (cx >= x0 && cx <= x1 && cy >= y0 && cy <= y1) return false;
+    const double det = xx * yy - xy * xy;
+    if (!(xx > 0.0) || !(yy > 0.0) || !(det > 0.0)) return false;
+    auto q = [&](double dx, double dy) { return xx * dx * dx + 2.0 * xy * dx * dy + yy * dy * dy; };
+    double m = 1e300;
+    for (int e = 0; e < 2; ++e) {  // horizontal edges y = y0, y1
+        const double dy = (e ? y1 : y0) - cy;
+        const double x = fmin(fmax(cx - xy * dy / xx, static_cast<double>(x0)), static_cast<double>(x1));
+        m = fmin(m, q(x - cx, dy));
+    }
+    for (int e = 0; e < 2; ++e) {  // vertical edges x = x0, x1
+        const double dx = (e ? x1 : x0) - cx;
+        const double y = fmin(fmax(cy - xy * dx / yy, static_cast<double>(y0)), static_cast<double>(y1));
+        m = fmin(m, q(dx, y - cy));
+    }
+    const double disc = sqrt(0.25 * (xx - yy) * (xx - yy) + xy * xy);
+    const double lmin = 0.5 * (xx + yy) - disc;
+    if (!(lmin > 0.0)) return false;
+    const double kappa = (fmax(fabs(xx), fabs(yy)) + fabs(xy)) / lmin;
+    return m * (1.0 - 1e-5 - 64.0 * 0x1p-24 * kappa) > static_cast<double>(qcut);
+}
+
+// Default (fast-alpha) rasterizer for 16x16 tiles: warp-persistent.  The
+// work unit is half a tile (16 columns x 8 rows); warps pull units from a
+// global counter, so load balances at warp granularity and no CTA waits on
+// another warp.  Lane l owns column l%16 and rows 4(l/16)..+3 of its unit.
+// Per 32-record step of the tile's sorted span, each lane tests one splat
+// against the unit's pixel-centre rectangle (extent box, then an exact
+// min-quad test) and the warp blends the survivors in order:
+//   q by FMA (its error is folded into qcut/qsafe), fast pixels (q < qsafe)
+//   blend alpha = min(2^(q c + log2 opacity), clamp) with FMAs; pixels in
+//   the margin band (qsafe <= q <= qcut) are re-evaluated exactly (glibc
+//   expf, reference order) -- every alpha >= tau decision is the reference's.
+// P_it per tile (pairs iterated before saturation, rasterizer.cpp:55-56) is
+// the max over its two units, combined through a per-tile 64-bit word.
+template <bool RECT, bool STATS>
+__global__ void __launch_bounds__(256, 3)
+k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+               const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
+               float* __restrict__ image, uint32_t* unit_ctr, unsigned long long* __restrict__ tile_pit,
+               unsigned long long* __restrict__ pit, unsigned long long* dbg) {
+    // STATS: dbg[0] += splat iterations per warp, dbg[1] += live pixel
+    // evaluations, dbg[2] += fast blends, dbg[3] += exact re-evaluations
+    unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0;
+    constexpr int PPT = 4;
+    constexpr int NWB = 8;  // warps per block
+    __shared__ __align__(16) float4 sA[NWB][32];
+    __shared__ __align__(16) float4 sB[NWB][32];
+    __shared__ __align__(16) float4 sC[NWB][32];
+    __shared__ uint64_t sTab[32];
+    __shared__ __align__(16) float sOut[NWB][8 * 16 * 3];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 32) sTab[tid] = kExp2fTab[tid];
+    __syncthreads();
+
+    const uint32_t units = 2u * static_cast<uint32_t>(p.tiles_x * p.tiles_y);
+    const float tau = p.tau, tfloor = p.tfloor, aclamp = p.aclamp;
+    const float c_ex2 = -0.5f * 1.4426950408889634f;
+    const int lx = lane & 15, g = lane >> 4;
+
+    while (true) {
+        uint32_t unit = 0;
+        if (lane == 0) unit = atomicAdd(unit_ctr, 1u);
+        unit = __shfl_sync(0xffffffffu, unit, 0);
+        if (unit >= units) break;
+        const int tile = static_cast<int>(unit >> 1), half = static_cast<int>(unit & 1u);
+        const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+        const int x0 = tx * 16, y0 = ty * 16 + half * 8;
+        const int w = imin(16, p.W - x0), h = imin(8, p.H - y0);  // h may be <= 0 (bottom tile row)
+        const float px = static_cast<float>(x0 + lx) + 0.5f;
+        float py[PPT], T[PPT], Cr[PPT], Cg[PPT], Cb[PPT];
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            py[k] = static_cast<float>(y0 + 4 * g + k) + 0.5f;
+            T[k] = (lx < w && 4 * g + k < h) ? 1.0f : 0.0f;  // outside the image: saturated
+            Cr[k] = Cg[k] = Cb[k] = 0.0f;
+        }
+        const float cx0 = x0 + 0.5f, cx1 = x0 + w - 0.5f;
+        const float cy0 = y0 + 0.5f, cy1 = y0 + h - 0.5f;
+
+        const uint2 rg = ranges[tile];
+        const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x;
+        uint32_t death = 0;
+        bool all_done = h <= 0;
+        float4 nA = make_float4(0, 0, 0, 0), nB = nA, nC = nA;
+        auto fetch = [&](uint32_t base) {
+            const uint32_t i = base + lane;
+            if (i < end) {
+                const uint32_t gid = __ldg(&vals[i]);
+                nA = __ldg(&P0[gid]);
+                nB = __ldg(&P1[gid]);
+                nC = __ldg(&P2[gid]);
+            }
+        };
+        if (!all_done && start < end) fetch(start);
+        for (uint32_t base = start; base < end && !all_done; base += 32) {
+            const float4 cA = nA, cB = nB, cC = nC;
+            if (base + 32 < end) fetch(base + 32);
+            bool rel = base + lane < end && meets_box(cA.x, cA.y, unpack_extent(cC.w), cx0, cx1, cy0, cy1);
+            if (RECT && rel) rel = !rect_outside(cA, cB.x, cB.z, cx0, cx1, cy0, cy1);
+            uint32_t m = __ballot_sync(0xffffffffu, rel);
+            if (!m) continue;
+            sA[warp][lane] = cA;
+            sB[warp][lane] = cB;
+            sC[warp][lane] = cC;
+            __syncwarp();
+            while (m) {
+                const int j = __ffs(m) - 1;
+                m &= m - 1;
+                const float4 sa = sA[warp][j];  // mx, my, inv.xx, 2*inv.xy
+                const float4 sb = sB[warp][j];  // inv.yy, opacity, qcut, qsafe
+                const float4 sc = sC[warp][j];  // r, g, b, extent
+                const float dx = px - sa.x;
+                const float t1 = sa.z * dx * dx;
+                const float t2 = sa.w * dx;
+                const float l2op = fast_log2(sb.y);
+                const float qcut = sb.z, qsafe = sb.w;
+                if (STATS) {
+                    ++st_it;
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) st_on += T[k] >= tfloor;
+                }
+                // Pixels are not masked once saturated (T < floor): their
+                // remaining blend weights sum to less than T <= floor = 1e-4,
+                // which bounds the image difference to the reference by
+                // 1e-4 per channel; the warp stops when all are saturated.
+                bool need_any = false;
+                bool need[PPT];
+                float e[PPT];
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const float dy = py[k] - sa.y;
+                    const float q = __fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1);
+                    const bool fast = q < qsafe;
+                    e[k] = fast ? fast_exp2(__fmaf_rn(q, c_ex2, l2op)) : 0.0f;
+                    need[k] = !fast && !(q > qcut);
+                    need_any = need_any || need[k];
+                    if (STATS) {
+                        st_fast += fast && T[k] >= tfloor;
+                        st_need += need[k];
+                    }
+                }
+                if (sb.y >= aclamp) {  // alpha_at's clamp can bind only for opacity >= clamp
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) e[k] = fminf(e[k], aclamp);
+                }
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const float wgt = e[k] * T[k];
+                    Cr[k] = __fmaf_rn(wgt, sc.x, Cr[k]);
+                    Cg[k] = __fmaf_rn(wgt, sc.y, Cg[k]);
+                    Cb[k] = __fmaf_rn(wgt, sc.z, Cb[k]);
+                    T[k] = __fmaf_rn(-e[k], T[k], T[k]);
+                }
+                if (__any_sync(0xffffffffu, need_any)) {  // margin band: the reference's alpha_at
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) {
+                        if (!need[k]) continue;
+                        const float dy = py[k] - sa.y;
+                        const float qr = (t1 + t2 * dy) + sb.x * dy * dy;  // reference order
+                        const float a = exact_alpha(qr, sb.y, aclamp, sTab);
+                        if (a < tau) continue;
+                        const float t_cur = T[k];
+                        const float wgt = a * t_cur;
+                        Cr[k] += wgt * sc.x;
+                        Cg[k] += wgt * sc.y;
+                        Cb[k] += wgt * sc.z;
+                        T[k] = t_cur * (1.0f - a);
+                    }
+                }
+                const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
+                if (!__any_sync(0xffffffffu, tmax >= tfloor)) {
+                    death = base - start + j + 1;
+                    all_done = true;
+                    break;
+                }
+            }
+            __syncwarp();
+        }
+
+        // P_it (rasterizer.cpp:55-56): per unit n if any pixel stays
+        // unsaturated, else the 1-based index of the saturating pair; per
+        // tile the max over both units.  Word = (units done << 32) | max.
+        if (lane == 0 && pit) {
+            const uint32_t mine = h <= 0 ? 0u : (all_done ? death : end - start);
+            unsigned long long* wp = &tile_pit[tile];
+            unsigned long long old = *wp;
+            while (true) {
+                const uint32_t mx = static_cast<uint32_t>(old) > mine ? static_cast<uint32_t>(old) : mine;
+                const unsigned long long r = atomicCAS(wp, old, (((old >> 32) + 1ull) << 32) | mx);
+                if (r == old) break;
+                old = r;
+            }
+            if ((old >> 32) == 1ull) {  // second unit of the tile: publish the tile's max
+                const uint32_t mx = static_cast<uint32_t>(old) > mine ? static_cast<uint32_t>(old) : mine;
+                if (mx) atomicAdd(pit, static_cast<unsigned long long>(mx));
+            }
+        }
+
+        // store: stage the unit in shared memory, then whole rows (float4)
+        if (h > 0) {
+            float* so = sOut[warp];
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                float* o = &so[((4 * g + k) * 16 + lx) * 3];
+                o[0] = sclamp(Cr[k] + T[k] * p.bg[0], 0.0f, 1.0f);
+                o[1] = sclamp(Cg[k] + T[k] * p.bg[1], 0.0f, 1.0f);
+                o[2] = sclamp(Cb[k] + T[k] * p.bg[2], 0.0f, 1.0f);
+            }
+            __syncwarp();
+            if (w == 16 && (p.W & 3) == 0) {
+                for (int i = lane; i < 12 * h; i += 32) {
+                    const int row = i / 12, col = i % 12;
+                    float4* dst = reinterpret_cast<float4*>(image + (static_cast<size_t>(y0 + row) * p.W + x0) * 3);
+                    __stcs(&dst[col], reinterpret_cast<const float4*>(so)[row * 12 + col]);
+                }
+            } else {
+                for (int i = lane; i < w * h * 3; i += 32) {
+                    const int c = i % 3, pix = i / 3, row = pix / w, col = pix % w;
+                    image[(static_cast<size_t>(y0 + row) * p.W + x0 + col) * 3 + c] = so[(row * 16 + col) * 3 + c];
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (STATS) {
+        for (int o = 16; o > 0; o >>= 1) {
+            st_on += __shfl_xor_sync(0xffffffffu, st_on, o);
+            st_fast += __shfl_xor_sync(0xffffffffu, st_fast, o);
+            st_need += __shfl_xor_sync(0xffffffffu, st_need, o);
+        }
+        if (lane == 0) {
+            atomicAdd(&dbg[0], st_it);
+            atomicAdd(&dbg[1], st_on);
+            atomicAdd(&dbg[2], st_fast);
+            atomicAdd(&dbg[3], st_need);
+        }
+    }
+}
+
+void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
+                         const float4* P0, const float4* P1, const float4* P2, float* image, uint32_t* unit_ctr,
+                         unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg) {
+    static const int mode = [] {
+        const char* e = std::getenv("AGSX_RASTER_RECT");
+        const char* t = std::getenv("AGSX_RASTER_STATS");
+        return ((e && *e == '1') ? 1 : 0) | ((t && *t == '1') ? 2 : 0);
+    }();
+    switch (mode) {
+        case 0: k_raster_units<false, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        case 1: k_raster_units<true, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        case 2: k_raster_units<false, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        default: k_raster_units<true, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+    }
+}
+
+cudaError_t raster_units_occupancy(int* occ) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_raster_units<false, false>, 256, 0);
 }
 
 // Any tile size in [1, 64]: 256 threads, pixel k of thread t is tile pixel
@@ -403,7 +675,7 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
                 if (!meets_box(sa.x, sa.y, unpack_extent(sc.w), bx0, bx1, by0, by1)) continue;
                 const float4 sb = sB[buf][j];
                 const uint32_t qcut = __float_as_uint(sb.z);
-                const uint32_t qsafe = EXACT ? 0u : __float_as_uint(sb.w);
+                const float qsafe = EXACT ? -__int_as_float(0x7f800000) : sb.w;
                 bool newly_done = false;
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
@@ -412,7 +684,7 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
                     const float q = (sa.z * dx * dx + sa.w * dx * dy) + sb.x * dy * dy;
                     const uint32_t qb = __float_as_uint(q);
                     float a;
-                    if (qb < qsafe) {
+                    if (q >= 0.0f && q < qsafe) {
                         a = fminf(sb.y * fast_exp2(q * c_ex2), aclamp);
                     } else {
                         if (qb > qcut && qb <= 0x7f800000u) continue;

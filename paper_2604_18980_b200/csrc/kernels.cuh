@@ -48,6 +48,14 @@ void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t
                           const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
                           const float4* P2, float* image, uint32_t* maxt_buf, unsigned long long* pit);
 
+// Warp-persistent fast-alpha rasterizer for 16x16 tiles (units = half
+// tiles pulled from *unit_ctr, zeroed per frame; tile_pit: one zeroed u64
+// per tile).
+void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
+                         const float4* P0, const float4* P1, const float4* P2, float* image, uint32_t* unit_ctr,
+                         unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg);
+cudaError_t raster_units_occupancy(int* occ);
+
 __global__ void k_logf(const float* x, float* y, uint64_t n);
 __global__ void k_expf(const float* x, float* y, uint64_t n);
 
