@@ -99,6 +99,8 @@ struct agsx_ctx {
     bool f_has_lut = false;
     FrameParams f_params{};
     bool f_maxt = false;
+    float* f_image = nullptr;     // raster target of the frame (device image or mapped host buffer)
+    bool f_image_on_host = false;  // the frame streamed its image into a mapped host buffer
     uint32_t* f_tkeys = nullptr;
     uint32_t* f_pvals = nullptr;
     int f_tile_count = 0;
@@ -430,7 +432,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
     // K6
-    launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ptr<float>(ctx->image),
+    launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ctx->f_image,
                   maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
     AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
     AGSX_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
@@ -440,7 +442,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
 }
 
 int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, const agsx_config* cfg,
-                const agsx_lut* lut, bool maxt) {
+                const agsx_lut* lut, bool maxt, float* host_image = nullptr) {
     if (!sc) return fail(ctx, AGSX_EINVAL, "render: null scene");
     if (sc->device != ctx->device) return fail(ctx, AGSX_EINVAL, "scene lives on another device");
     FrameParams p;
@@ -464,6 +466,20 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     }
     ctx->f_params = p;
     ctx->f_maxt = maxt;
+    // Frame egress: a page-locked, device-mapped destination is written by
+    // the rasterizer directly (the 191 MB PCIe transfer overlaps the blend);
+    // anything else gets the device image and a copy.
+    ctx->f_image = ptr<float>(ctx->image);
+    ctx->f_image_on_host = false;
+    if (host_image) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, host_image) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+            at.devicePointer != nullptr && std::getenv("AGSX_NO_ZERO_COPY") == nullptr) {
+            ctx->f_image = static_cast<float*>(at.devicePointer);
+            ctx->f_image_on_host = true;
+        }
+        cudaGetLastError();  // clear a pageable-pointer query error
+    }
     enqueue_frame(ctx, sc, p, maxt, nullptr);
     return AGSX_OK;
 }
@@ -659,11 +675,11 @@ int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
         const bool maxt = out && out->max_t;
-        int rc = start_frame(ctx, scene, cam, cfg, lut, maxt);
+        int rc = start_frame(ctx, scene, cam, cfg, lut, maxt, out ? out->image : nullptr);
         if (rc) return rc;
         rc = finish_frame(ctx, out);
         if (rc) return rc;
-        if (out && out->image) {
+        if (out && out->image && !ctx->f_image_on_host) {
             AGSX_CUDA(cudaMemcpyAsync(out->image, ctx->image.p,
                                       static_cast<size_t>(cam->width) * cam->height * 12,
                                       cudaMemcpyDeviceToHost, ctx->stream));
@@ -714,6 +730,7 @@ int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n) {
 int agsx_device_image(agsx_ctx* ctx, float** dptr, int32_t* width, int32_t* height) {
     if (!ctx || !dptr) return AGSX_EINVAL;
     if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame rendered yet");
+    if (ctx->f_image_on_host) return fail(ctx, AGSX_EINVAL, "the last frame streamed its image to the host");
     *dptr = ptr<float>(ctx->image);
     if (width) *width = ctx->f_cam.width;
     if (height) *height = ctx->f_cam.height;
