@@ -57,7 +57,7 @@ struct DevScene {
 //   P0 = {mean.x, mean.y, inv.xx, 2*inv.xy}          raster + emit
 //   P1 = {inv.yy, opacity, qcut, qsafe}              raster + emit(inv.yy)
 //   P2 = {r, g, b, half2(ex, ey)}                    raster
-//   P3 = {rx, ry, r2, r}                             emit (tile test)
+//   P3 = hit record (hit_record below)                emit
 //   P4 = {v1.x, v1.y, a, b}                          emit, OBB mode only
 struct SplatPlanes {
     float4* p0;
@@ -229,13 +229,82 @@ __device__ __forceinline__ bool tile_hit(const TileTest& t, int tx, int ty, cons
     return min_quad_to_rect(t, x0, y0, x1, y1) <= t.r2;
 }
 
-__device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FrameParams& p) {
+// Calls f(tx, ty) for every intersected tile in the reference's row-major
+// order (pair_gen.cpp:152-158).  For the ellipse / AdaGScale test the
+// horizontal-edge minimisers (one exact division each) depend only on the
+// tile row and are hoisted out of the column loop, and min(h0, h1, v0, v1)
+// <= r2 is decided edge by edge (the same values, so the same decision as
+// min_quad_to_rect, pair_gen.cpp:65-83).
+template <class F>
+__device__ __forceinline__ void for_each_tile_hit(const TileTest& t, const FrameParams& p, F&& f) {
     const Span s = tile_span(t, p);
-    if (s.empty) return 0;
+    if (s.empty) return;
+    if (t.mode == AGSX_MODE_AABB || t.mode == AGSX_MODE_OBB) {
+        for (int ty = s.ty0; ty <= s.ty1; ++ty)
+            for (int tx = s.tx0; tx <= s.tx1; ++tx)
+                if (tile_hit(t, tx, ty, p)) f(tx, ty);
+        return;
+    }
+    const float ts = static_cast<float>(p.tile_size);
+    const float W = static_cast<float>(p.W), H = static_cast<float>(p.H);
+    const float cx = t.cx, cy = t.cy;
+    for (int ty = s.ty0; ty <= s.ty1; ++ty) {
+        const float y0 = ty * ts;
+        const float y1 = smin(y0 + ts, H);
+        const float dy0 = y0 - cy, dy1 = y1 - cy;
+        const float xh0 = cx - t.ixy * dy0 / t.ixx;
+        const float xh1 = cx - t.ixy * dy1 / t.ixx;
+        const bool row_in = cy >= y0 && cy <= y1;
+        for (int tx = s.tx0; tx <= s.tx1; ++tx) {
+            const float x0 = tx * ts;
+            const float x1 = smin(x0 + ts, W);
+            if (!box_overlap(x0, y0, x1, y1, cx, cy, t.rx, t.ry)) continue;
+            bool hit = row_in && cx >= x0 && cx <= x1;  // centre inside: min = 0 <= r2
+            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh0, x0, x1) - cx, dy0) <= t.r2;
+            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh1, x0, x1) - cx, dy1) <= t.r2;
+            if (!hit) {
+                const float dx = x0 - cx;
+                const float y = sclamp(cy - t.ixy * dx / t.iyy, y0, y1);
+                hit = quad_form(t.ixx, t.ixy, t.iyy, dx, y - cy) <= t.r2;
+            }
+            if (!hit) {
+                const float dx = x1 - cx;
+                const float y = sclamp(cy - t.ixy * dx / t.iyy, y0, y1);
+                hit = quad_form(t.ixx, t.ixy, t.iyy, dx, y - cy) <= t.r2;
+            }
+            if (hit) f(tx, ty);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FrameParams& p) {
     uint32_t n = 0;
-    for (int ty = s.ty0; ty <= s.ty1; ++ty)
-        for (int tx = s.tx0; tx <= s.tx1; ++tx) n += tile_hit(t, tx, ty, p) ? 1u : 0u;
+    for_each_tile_hit(t, p, [&](int, int) { ++n; });
     return n;
+}
+
+// P3 hit record of a splat, written by the count pass so that emission
+// needs no second tile test: for a tile span of <= 64 tiles, {mask lo, mask
+// hi, tx0 | ty0 << 16, span width} with bit (ty-ty0)*w + (tx-tx0) set per
+// intersected tile (increasing bits = row-major emission order); for larger
+// spans {rx, ry, r2, kHitsRecompute} and the emitter re-runs the test.
+constexpr uint32_t kHitsRecompute = 0xffffffffu;
+
+__device__ __forceinline__ uint4 hit_record(const TileTest& t, const FrameParams& p, uint32_t& count) {
+    count = 0;
+    const Span s = tile_span(t, p);
+    if (s.empty) return make_uint4(0u, 0u, 0u, 0u);
+    const int sw = s.tx1 - s.tx0 + 1, sh = s.ty1 - s.ty0 + 1;
+    if (sw * sh <= 64) {
+        unsigned long long mask = 0;
+        for_each_tile_hit(t, p, [&](int tx, int ty) { mask |= 1ull << ((ty - s.ty0) * sw + (tx - s.tx0)); });
+        count = static_cast<uint32_t>(__popcll(mask));
+        return make_uint4(static_cast<uint32_t>(mask), static_cast<uint32_t>(mask >> 32),
+                          static_cast<uint32_t>(s.tx0) | (static_cast<uint32_t>(s.ty0) << 16),
+                          static_cast<uint32_t>(sw));
+    }
+    count = count_tiles(t, p);
+    return make_uint4(__float_as_uint(t.rx), __float_as_uint(t.ry), __float_as_uint(t.r2), kHitsRecompute);
 }
 
 // Blend-side culling data for the rasterizer (not part of the reference; it
@@ -252,7 +321,7 @@ __device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FramePa
 // qsafe = -inf disables the fast path (opacity < tau, or kappa too large).
 // For rho < 1/4 neither q form can be negative (their error is below q), so
 // the fast test needs no sign check.
-__device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy, float opacity, float tau,
+static __device__ __noinline__ void blend_cull_data_f64(float ixx, float ixy, float iyy, float opacity, float tau,
                                                 float aclamp, float& qcut, float& qsafe, float& ex, float& ey) {
     (void)aclamp;
     const float inf = __int_as_float(0x7f800000);
@@ -286,6 +355,38 @@ __device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy,
     const double r2 = static_cast<double>(qcut) / (1.0 - relerr);
     ex = __double2float_ru(sqrt(r2 * c / det) * 1.0001 + 1e-3);  // (M^-1)_xx = iyy / det
     ey = __double2float_ru(sqrt(r2 * a / det) * 1.0001 + 1e-3);
+}
+
+// Float evaluation of blend_cull_data_f64 for well-conditioned splats
+// (kappa <= 1e3, the common case); every quantity is rounded outward with
+// margins far above the float error (the decision margins are 1e-4 relative).
+__device__ __forceinline__ void blend_cull_data(float ixx, float ixy, float iyy, float opacity, float tau,
+                                                float aclamp, float& qcut, float& qsafe, float& ex, float& ey) {
+    const float inf = __int_as_float(0x7f800000);
+    if (!(opacity >= tau)) {
+        qcut = 0.0f;
+        qsafe = -inf;
+        ex = ey = 0.0f;
+        return;
+    }
+    const float a = ixx, b = ixy, c = iyy;
+    const float lmax = 0.5f * (a + c) + sqrtf(0.25f * (a - c) * (a - c) + b * b);
+    const float det = a * c - b * b;
+    const float lmin = det / lmax;
+    const float kappa = lmax / lmin;
+    if (!(det > 0.0f) || !(lmax > 0.0f) || !(kappa <= 1e3f)) {
+        blend_cull_data_f64(ixx, ixy, iyy, opacity, tau, aclamp, qcut, qsafe, ex, ey);
+        return;
+    }
+    const float lr = logf(opacity / tau);  // >= 0, error ~1e-7 (1 + lr)
+    const float m = 1e-4f * (1.0f + lr);
+    const float rho = 1.01f * 16.0f * 0x1p-24f * (fmaxf(fabsf(a), fabsf(c)) + fabsf(b)) / lmin;
+    qcut = 2.0f * (lr + m) * (1.0f + rho) * (1.0f + 4e-6f);
+    qsafe = lr > m ? 2.0f * (lr - m) * (1.0f - rho) * (1.0f - 4e-6f) : -inf;
+    const float relerr = 64.0f * 0x1p-24f * kappa;
+    const float r2 = qcut / (1.0f - relerr);
+    ex = sqrtf(r2 * c / det) * 1.001f + 1e-3f;
+    ey = sqrtf(r2 * a / det) * 1.001f + 1e-3f;
 }
 
 __device__ __forceinline__ uint32_t pack_extent(float ex, float ey) {

@@ -44,6 +44,27 @@ __device__ __forceinline__ TileTest planes_tile_test(const FrameParams& p, const
 // Persistent over the depth-sorted splat list; per 256-splat tile: block
 // scan of tile counts + look-back -> pair offsets, then emission of
 // (tile id, Gaussian id) for every intersected tile in row-major order.
+// Emits f(tx, ty) for the intersected tiles of splat g in row-major order
+// from its P3 hit record (mask) or, for spans over 64 tiles, by re-running
+// the tile test.
+template <class F>
+__device__ __forceinline__ void emit_hits(const FrameParams& p, const SplatPlanes& pl, uint32_t g, F&& f) {
+    const uint4 r = reinterpret_cast<const uint4*>(pl.p3)[g];
+    if (r.w != kHitsRecompute) {
+        unsigned long long mask = static_cast<unsigned long long>(r.x) | (static_cast<unsigned long long>(r.y) << 32);
+        const int tx0 = static_cast<int>(r.z & 0xffffu), ty0 = static_cast<int>(r.z >> 16);
+        const int sw = static_cast<int>(r.w);
+        while (mask) {
+            const int b = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            f(tx0 + b % sw, ty0 + b / sw);
+        }
+        return;
+    }
+    const TileTest t = planes_tile_test(p, pl, g);
+    for_each_tile_hit(t, p, f);
+}
+
 __global__ void __launch_bounds__(256)
 k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __restrict__ status,
        SplatPlanes pl, uint32_t* __restrict__ tkeys, uint32_t* __restrict__ pvals,
@@ -97,16 +118,12 @@ k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __rest
             if (off + cnt > capacity || s_prefix == 0xffffffffu) {
                 atomicOr(&ctr->overflow, 1u);
             } else {
-                const TileTest t = planes_tile_test(p, pl, g);
-                const Span s = tile_span(t, p);
                 uint64_t at = off;
-                for (int ty = s.ty0; ty <= s.ty1; ++ty)
-                    for (int tx = s.tx0; tx <= s.tx1; ++tx)
-                        if (tile_hit(t, tx, ty, p)) {
-                            tkeys[at] = static_cast<uint32_t>(ty * p.tiles_x + tx);
-                            pvals[at] = g;
-                            ++at;
-                        }
+                emit_hits(p, pl, g, [&](int tx, int ty) {
+                    tkeys[at] = static_cast<uint32_t>(ty * p.tiles_x + tx);
+                    pvals[at] = g;
+                    ++at;
+                });
             }
         }
         __syncthreads();
@@ -123,14 +140,15 @@ __global__ void k_splats_to_planes(FrameParams p, const agsx_splat_view* __restr
     const agsx_splat_view s = splats[j];
     const TileTest t = make_tile_test(s.mean2d[0], s.mean2d[1], s.cov2d[0], s.cov2d[1], s.cov2d[2],
                                       s.inv_cov[0], s.inv_cov[1], s.inv_cov[2], s.opacity, s.th, p);
-    counts[j] = count_tiles(t, p);
+    uint32_t cnt = 0;
+    reinterpret_cast<uint4*>(pl.p3)[j] = hit_record(t, p, cnt);
+    counts[j] = cnt;
     depth_bits[j] = __float_as_uint(s.depth);
     float qcut, qsafe, ex, ey;
     blend_cull_data(s.inv_cov[0], s.inv_cov[1], s.inv_cov[2], s.opacity, p.tau, p.aclamp, qcut, qsafe, ex, ey);
     pl.p0[j] = make_float4(s.mean2d[0], s.mean2d[1], s.inv_cov[0], 2.0f * s.inv_cov[1]);
     pl.p1[j] = make_float4(s.inv_cov[2], s.opacity, qcut, qsafe);
     pl.p2[j] = make_float4(s.rgb[0], s.rgb[1], s.rgb[2], __uint_as_float(pack_extent(ex, ey)));
-    pl.p3[j] = make_float4(t.rx, t.ry, t.r2, 0.0f);
     if (p.mode == AGSX_MODE_OBB) pl.p4[j] = make_float4(t.v1x, t.v1y, t.a, t.b);
 }
 
@@ -141,17 +159,13 @@ __global__ void k_emit_list(FrameParams p, uint64_t n, SplatPlanes pl,
                             uint32_t* __restrict__ vals) {
     const uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (j >= n || counts[j] == 0) return;
-    const TileTest t = planes_tile_test(p, pl, static_cast<uint32_t>(j));
-    const Span s = tile_span(t, p);
     uint64_t at = offsets[j];
     const uint64_t lo = depth_bits[j];
-    for (int ty = s.ty0; ty <= s.ty1; ++ty)
-        for (int tx = s.tx0; tx <= s.tx1; ++tx)
-            if (tile_hit(t, tx, ty, p)) {
-                keys[at] = (static_cast<uint64_t>(ty * p.tiles_x + tx) << 32) | lo;
-                vals[at] = static_cast<uint32_t>(j);
-                ++at;
-            }
+    emit_hits(p, pl, static_cast<uint32_t>(j), [&](int tx, int ty) {
+        keys[at] = (static_cast<uint64_t>(ty * p.tiles_x + tx) << 32) | lo;
+        vals[at] = static_cast<uint32_t>(j);
+        ++at;
+    });
 }
 
 // ranges[tile] = [first, last+1) over the tile-sorted pair list; tiles

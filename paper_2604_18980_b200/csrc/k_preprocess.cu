@@ -91,6 +91,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         const float4 po = sc.pos_op[i];
         const float4 q = sc.rot[i];
         const float4 sr = sc.scale_r[i];
+        const float2 gb = sc.sh_gb[i];  // issued with the other loads
         const float opacity = po.w;
         // to_camera (scene.hpp:41-43, Mat3f*Vec3f math.hpp:43-49)
         const float dx = po.x - p.cam_pos[0], dy = po.y - p.cam_pos[1], dz = po.z - p.cam_pos[2];
@@ -198,7 +199,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
             const float inv_det = 1.0f / det;  // SymMat2::inverse (math.hpp:85-88)
             const float ixx = cyy * inv_det, ixy = -cxy * inv_det, iyy = cxx * inv_det;
             const TileTest tt = make_tile_test(m2x, m2y, cxx, cxy, cyy, ixx, ixy, iyy, opacity, th, p);
-            cnt = count_tiles(tt, p);
+            const uint4 hits = hit_record(tt, p, cnt);
             keep = cnt > 0;
             float rgb[3] = {0.5f, 0.5f, 0.5f};
             if (keep || dump) {
@@ -211,7 +212,6 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
                     uy = dy * inv;
                     uz = dz * inv;
                 }
-                const float2 gb = sc.sh_gb[i];
                 eval_color(sc, i, sr.w, gb.x, gb.y, ux, uy, uz, rgb);
             }
             if (keep) {
@@ -220,7 +220,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
                 pl.p0[i] = make_float4(m2x, m2y, ixx, 2.0f * ixy);
                 pl.p1[i] = make_float4(iyy, opacity, qcut, qsafe);
                 pl.p2[i] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(pack_extent(ex, ey)));
-                pl.p3[i] = make_float4(tt.rx, tt.ry, tt.r2, 0.0f);
+                reinterpret_cast<uint4*>(pl.p3)[i] = hits;
                 if (p.mode == AGSX_MODE_OBB) pl.p4[i] = make_float4(tt.v1x, tt.v1y, tt.a, tt.b);
             }
             if (dump) {
