@@ -216,7 +216,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dist = None
-    if world > 1:
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # under torchrun (any N): NCCL process group
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -226,7 +226,23 @@ def run_ours(args, rank, world, local_rank):
     k = scaled_k(w) if mode == "adagscale" else 0.0
     bins = LUT_BINS if mode == "adagscale" else []
     scene = P.synth_scene(1, n, "veil", cameras=cams, width=w, height=h, focal=focal)
-    view = rank % scene.camera_count
+    from paper_2604_18980_b200.multiview import gather_frames, partition_views, stereo_cameras
+
+    # Work per rank: configs 1-3 -> rank r renders view r of the
+    # camera set (weak scaling); config 4 -> stereo, eye r % 2 of view 0;
+    # config 5 -> the 64-view camera path split into contiguous blocks
+    # (strong scaling: the whole path per step, frames / step fixed).
+    if args.config == "5":
+        jobs = [(v, None) for v in partition_views(cams, world, rank)]
+        frames_per_step_total = cams
+    elif args.config == "4":
+        eyes = stereo_cameras(scene.camera(0))
+        jobs = [(0, eyes[rank % 2])]
+        frames_per_step_total = world
+    else:
+        jobs = [(rank % scene.camera_count, None)]
+        frames_per_step_total = world
+    view = jobs[0][0] if jobs else 0
     r = P.Renderer(local_rank)
     r.upload(scene)
     stream = torch.cuda.ExternalStream(r.stream, device=torch.device("cuda", local_rank))
@@ -237,14 +253,18 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def step():
+        for v, cam in jobs:
+            r.render_async(scene, v, mode, k, bins, exact=args.exact, camera=cam)
+
     # warm-up (also sizes the pair arena)
     for _ in range(max(args.warmup, 3)):
-        r.render_async(scene, view, mode, k, bins, exact=args.exact)
+        step()
     r.wait()
     stats = r.frame_stats()
     launches0 = r.kernel_launches
 
-    # timed region: K frames back to back on the renderer's stream
+    # timed region: K steps back to back on the renderer's stream
     sampler = ClockSampler(local_rank)
     sampler.start()
     barrier()
@@ -252,24 +272,53 @@ def run_ours(args, rank, world, local_rank):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        r.render_async(scene, view, mode, k, bins, exact=args.exact)
+        step()
     ev1.record(stream)
     r.wait()
     barrier()
     clocks = sampler.stop()
     elapsed_ms = ev0.elapsed_time(ev1)
     launches = r.kernel_launches - launches0
-    hist = r.stage_history(min(args.steps, 64))
+    hist = r.stage_history(min(args.steps * max(len(jobs), 1), 64))
     stats = r.frame_stats()
 
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
-    frames = torch.tensor([args.steps], dtype=torch.float64, device="cuda")
+    frames = torch.tensor([args.steps * len(jobs)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(frames, op=dist.ReduceOp.SUM)
     max_ms = float(t.item())
     total_frames = float(frames.item())
     fps = total_frames / (max_ms * 1e-3)
+
+    # ---- frames gathered on rank 0 (NCCL over NVLink), N > 1 -----------------
+    gather = None
+    if dist is not None and not args.no_gather:
+        n_local = max(len(jobs), 1)
+        slots = torch.empty((n_local, h, w, 3), dtype=torch.float32, device="cuda")
+        steps_g = max(2, min(args.steps, 10))
+        with torch.cuda.stream(stream):
+            for it in range(steps_g + 1):
+                if it == 1:
+                    barrier()
+                    ev0.record(stream)
+                for i, (v, cam) in enumerate(jobs):
+                    r.render_async_to(scene, v, slots[i].data_ptr(), mode, k, bins, exact=args.exact, camera=cam)
+                if args.config == "5":
+                    gather_frames(slots[: len(jobs)], cams, world, rank, None, 0)
+                else:
+                    gather_frames(slots[: len(jobs)], world, world, rank, None, 0)
+            ev1.record(stream)
+        r.wait()
+        barrier()
+        tg = torch.tensor([ev0.elapsed_time(ev1) / steps_g], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tg, op=dist.ReduceOp.MAX)
+        gms = float(tg.item())
+        gather = {"fps_with_gather": frames_per_step_total / (gms * 1e-3), "ms_per_step_render_plus_gather": gms,
+                  "ms_per_step_render": max_ms / args.steps,
+                  "bytes_to_rank0_per_step": int((frames_per_step_total - len(jobs)) * h * w * 12),
+                  "how": "frames rasterised into per-rank slots (render_async_to), torch.distributed.gather "
+                         "(NCCL) onto rank 0 each step, CUDA events on the render stream, max over ranks"}
 
     # ---- end to end through the public API (host image out, per step) ----
     e2e = None
@@ -380,13 +429,15 @@ def run_ours(args, rank, world, local_rank):
         "warmup": args.warmup,
         "ms_per_step": max_ms / args.steps,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.config == "5" else "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (veil layout, seed 1, host synth_scene byte-identical to the reference)",
         "config": {
             "workload": workload_name(args.config, mode),
-            "gaussians": n, "width": w, "height": h, "mode": mode, "view_per_rank": "rank r renders view r",
+            "gaussians": n, "width": w, "height": h, "mode": mode,
+            "views": ("64-view camera path, contiguous blocks per rank" if args.config == "5" else
+                      "stereo: eye r % 2 of view 0 on rank r" if args.config == "4" else "rank r renders view r"),
             "parallelism": f"view-partitioned replicas x{world}",
             "l2": "inputs larger than L2 (scene 168 MB + image 191 MB per frame)",
             "alpha": "exact glibc expf" if args.exact else "MUFU.EX2 + exact guard band",
@@ -402,6 +453,7 @@ def run_ours(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "quality": quality,
         "adagscale_off": off,
+        "gather": gather,
     }
     print(json.dumps(line, default=_jsonable), flush=True)
     if dist is not None:
@@ -422,6 +474,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-off", action="store_true")
+    ap.add_argument("--no-gather", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -153,6 +153,12 @@ int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
 int agsx_render_async(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
                       const agsx_config* cfg, const agsx_lut* lut);
 int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out);
+/* As agsx_render_async, with the image rasterised into `target` (H*W*3 f32,
+ * HWC): device memory of the ctx's device (e.g. a frame slot that a
+ * collective then gathers) or a page-locked, device-mapped host buffer.
+ * `target` must stay valid until agsx_render_wait returns. */
+int agsx_render_async_to(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                         const agsx_config* cfg, const agsx_lut* lut, float* target);
 
 /* Device-timed stage durations (ms: preprocess, pair_gen, sort, raster) of
  * the last min(max_frames, 64) frames enqueued on this ctx, oldest first;

@@ -442,7 +442,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
 }
 
 int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, const agsx_config* cfg,
-                const agsx_lut* lut, bool maxt, float* host_image = nullptr) {
+                const agsx_lut* lut, bool maxt, float* host_image = nullptr, float* device_target = nullptr) {
     if (!sc) return fail(ctx, AGSX_EINVAL, "render: null scene");
     if (sc->device != ctx->device) return fail(ctx, AGSX_EINVAL, "scene lives on another device");
     FrameParams p;
@@ -469,9 +469,9 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     // Frame egress: a page-locked, device-mapped destination is written by
     // the rasterizer directly (the 191 MB PCIe transfer overlaps the blend);
     // anything else gets the device image and a copy.
-    ctx->f_image = ptr<float>(ctx->image);
-    ctx->f_image_on_host = false;
-    if (host_image) {
+    ctx->f_image = device_target ? device_target : ptr<float>(ctx->image);
+    ctx->f_image_on_host = device_target != nullptr;  // the ctx image is not this frame's
+    if (host_image && !device_target) {
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, host_image) == cudaSuccess && at.type == cudaMemoryTypeHost &&
             at.devicePointer != nullptr && std::getenv("AGSX_NO_ZERO_COPY") == nullptr) {
@@ -665,6 +665,13 @@ int agsx_render_async(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera*
     return guarded(ctx, [&]() -> int { return start_frame(ctx, scene, cam, cfg, lut, false); });
 }
 
+int agsx_render_async_to(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                         const agsx_config* cfg, const agsx_lut* lut, float* target) {
+    if (!ctx) return AGSX_EINVAL;
+    if (!target) return fail(ctx, AGSX_EINVAL, "render_async_to: null target");
+    return guarded(ctx, [&]() -> int { return start_frame(ctx, scene, cam, cfg, lut, false, nullptr, target); });
+}
+
 int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int { return finish_frame(ctx, out); });
@@ -730,7 +737,7 @@ int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n) {
 int agsx_device_image(agsx_ctx* ctx, float** dptr, int32_t* width, int32_t* height) {
     if (!ctx || !dptr) return AGSX_EINVAL;
     if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame rendered yet");
-    if (ctx->f_image_on_host) return fail(ctx, AGSX_EINVAL, "the last frame streamed its image to the host");
+    if (ctx->f_image_on_host) return fail(ctx, AGSX_EINVAL, "the last frame was rasterised into a caller buffer");
     *dptr = ptr<float>(ctx->image);
     if (width) *width = ctx->f_cam.width;
     if (height) *height = ctx->f_cam.height;

@@ -148,6 +148,20 @@ py::array_t<float> pinned_image(int h, int w) {
     return py::array_t<float>({h, w, 3}, static_cast<float*>(p), owner);
 }
 
+agsx_camera camera_from(const py::dict& d) {
+    agsx_camera c{};
+    auto pos = d["position"].cast<std::vector<float>>();
+    auto rot = d["rotation"].cast<std::vector<float>>();
+    if (pos.size() != 3 || rot.size() != 9) throw py::value_error("camera needs position[3], rotation[9]");
+    std::copy(pos.begin(), pos.end(), c.position);
+    std::copy(rot.begin(), rot.end(), c.rotation);
+    c.fx = d["fx"].cast<float>();
+    c.fy = d["fy"].cast<float>();
+    c.width = d["width"].cast<int>();
+    c.height = d["height"].cast<int>();
+    return c;
+}
+
 class Renderer {
 public:
     explicit Renderer(int device) : device_(device) {
@@ -226,8 +240,8 @@ public:
 
     void render_async(Scene& scene, int view, const std::string& mode, double k,
                       const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size,
-                      bool exact, std::size_t pair_budget) {
-        const agsx_camera cam = view_of(scene, view);
+                      bool exact, std::size_t pair_budget, py::object camera) {
+        const agsx_camera cam = camera.is_none() ? view_of(scene, view) : camera_from(camera.cast<py::dict>());
         const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
         const LutHolder lut(lut_bins, dmin, dmax);
         agsx_scene* dev = device_scene(scene);
@@ -235,6 +249,24 @@ public:
         {
             py::gil_scoped_release nogil;
             rc = agsx_render_async(ctx_, dev, &cam, &cfg, cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr);
+        }
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+    }
+
+    // Frame rasterised into caller-owned device memory (e.g. a torch tensor
+    // that a collective gathers); `target` is its address (H*W*3 f32).
+    void render_async_to(Scene& scene, int view, std::uintptr_t target, const std::string& mode, double k,
+                         const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size, bool exact,
+                         std::size_t pair_budget, py::object camera) {
+        const agsx_camera cam = camera.is_none() ? view_of(scene, view) : camera_from(camera.cast<py::dict>());
+        const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
+        const LutHolder lut(lut_bins, dmin, dmax);
+        agsx_scene* dev = device_scene(scene);
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = agsx_render_async_to(ctx_, dev, &cam, &cfg, cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr,
+                                      reinterpret_cast<float*>(target));
         }
         if (rc != AGSX_OK) raise_status(rc, ctx_);
     }
@@ -531,7 +563,12 @@ PYBIND11_MODULE(_core, m) {
         .def("render_async", &Renderer::render_async, py::arg("scene"), py::arg("view") = 0,
              py::arg("mode") = "ellipse", py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{},
              py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("tile_size") = 16,
-             py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27)
+             py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27, py::arg("camera") = py::none())
+        .def("render_async_to", &Renderer::render_async_to, py::arg("scene"), py::arg("view"), py::arg("target"),
+             py::arg("mode") = "ellipse", py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{},
+             py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("tile_size") = 16,
+             py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27,
+             py::arg("camera") = py::none())
         .def("wait", &Renderer::wait)
         .def("device_image", &Renderer::device_image)
         .def("stage_history", &Renderer::stage_history, py::arg("max_frames") = 64)

@@ -1,0 +1,157 @@
+"""View-partitioned multi-GPU rendering.
+
+The render path shards by viewpoint: every frame is independent and the scene is
+read-only (``render`` takes ``std::span<const Gaussian3D>``, rasterizer.hpp:63).  So
+each rank (one process per GPU) holds a replica of the scene, renders its own block
+of views with no collective on the data path, and only finished frames and
+per-frame stats cross GPUs.  The frames go to a destination rank via
+``torch.distributed`` (NCCL over NVLink on B200, gloo in the CPU tests), and the
+stats go through an all-reduce (sums of pair and splat counts, max of stage times).
+
+Partitioning follows §8(e):
+* config 5 is a camera path split into contiguous blocks of views per rank;
+* config 4 is stereo, with the left eye on rank 0 and the right eye on rank 1.
+
+The rasteriser writes each frame straight into a slot of a rank-local frame tensor
+(``Renderer.render_async_to``), and the gather sends that tensor.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, Sequence
+
+import numpy as np
+
+
+def partition_views(n_views: int, world: int, rank: int) -> list[int]:
+    """Contiguous block of the camera path owned by `rank`.
+
+    The first ``n_views % world`` ranks hold one extra view."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("rank must be in [0, world)")
+    if n_views < 0:
+        raise ValueError("n_views must be >= 0")
+    base, extra = divmod(n_views, world)
+    start = rank * base + min(rank, extra)
+    count = base + (1 if rank < extra else 0)
+    return list(range(start, start + count))
+
+
+def stereo_cameras(cam: dict, baseline: float = 0.064) -> tuple[dict, dict]:
+    """Left and right eye of a camera.
+
+    The right eye is the left eye moved by ``baseline`` along the camera's right
+    vector. That vector is row 0 of the world-to-camera rotation (look_at,
+    synth.cpp:25-34). The arithmetic is float32, like the reference's Vec3f."""
+    pos = np.asarray(cam["position"], np.float32)
+    right = np.asarray(cam["rotation"], np.float32)[:3]
+    right_pos = (pos + np.float32(baseline) * right).astype(np.float32)
+    left = dict(cam)
+    rcam = dict(cam)
+    rcam["position"] = [float(v) for v in right_pos]
+    return left, rcam
+
+
+@dataclass
+class PathStats:
+    """Frame statistics reduced over ranks."""
+
+    frames: int = 0
+    pair_count: int = 0  # summed over frames and ranks
+    splat_count: int = 0
+    stage_ms_max: list = field(default_factory=lambda: [0.0, 0.0, 0.0, 0.0])  # max over frames and ranks
+    per_view_pairs: dict = field(default_factory=dict)  # view -> pair count (this rank)
+
+
+RenderInto = Callable[[object, int, object, dict], dict]
+"""render_into(scene, view, frame_slot, kwargs) -> {"pair_count", "splat_count", "stage_ms"}"""
+
+
+def gpu_render_into(renderer) -> RenderInto:
+    """A `RenderInto` over the CUDA path: the rasteriser writes the slot in place."""
+
+    def fn(scene, view, slot, kw):
+        cam = kw.get("camera")
+        renderer.render_async_to(scene, view, slot.data_ptr(), mode=kw.get("mode", "ellipse"), k=kw.get("k", 0.0),
+                                 lut_bins=kw.get("lut_bins", []), exact=kw.get("exact", False), camera=cam)
+        return renderer.wait()
+
+    return fn
+
+
+class MultiViewRenderer:
+    """Renders the views of a camera path owned by this rank and gathers them.
+
+    ``render_into`` renders one view into a preallocated frame slot. It defaults
+    to the CUDA renderer of this rank's device. The CPU tests inject the oracle
+    here, so the gloo test exercises the partition and gather logic without a GPU.
+    """
+
+    def __init__(self, render_into: RenderInto, device="cuda"):
+        self.render_into = render_into
+        self.device = device
+
+    def render_local(self, scene, views: Sequence[int], height: int, width: int, **kw):
+        import torch
+
+        frames = torch.empty((max(len(views), 1), height, width, 3), dtype=torch.float32, device=self.device)
+        stats = PathStats()
+        for i, v in enumerate(views):
+            st = self.render_into(scene, v, frames[i], kw)
+            stats.frames += 1
+            stats.pair_count += int(st["pair_count"])
+            stats.splat_count += int(st["splat_count"])
+            stats.stage_ms_max = [max(a, float(b)) for a, b in zip(stats.stage_ms_max, st["stage_ms"])]
+            stats.per_view_pairs[v] = int(st["pair_count"])
+        return frames[: len(views)], stats
+
+    def render_path(self, scene, n_views: int, height: int, width: int, group=None, dst: int = 0,
+                    gather: bool = True, **kw):
+        """Render views [0, n_views) across the group; frames gathered on `dst`.
+
+        Returns ``(frames, stats)``:
+        * ``frames`` is a ``[n_views, H, W, 3]`` tensor on `dst` (on its
+          device), or None on the other ranks and when ``gather`` is False;
+        * ``stats`` is a `PathStats` reduced over all ranks.
+        """
+        import torch
+        import torch.distributed as dist
+
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        views = partition_views(n_views, world, rank)
+        local, stats = self.render_local(scene, views, height, width, **kw)
+        frames = local if world == 1 else None
+        if world > 1:
+            if gather:
+                frames = gather_frames(local, n_views, world, rank, group, dst)
+            red = torch.tensor([stats.frames, stats.pair_count, stats.splat_count], dtype=torch.float64,
+                               device=self.device)
+            mx = torch.tensor(stats.stage_ms_max, dtype=torch.float64, device=self.device)
+            dist.all_reduce(red, group=group)
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX, group=group)
+            stats.frames, stats.pair_count, stats.splat_count = (int(x) for x in red.tolist())
+            stats.stage_ms_max = mx.tolist()
+        return frames, stats
+
+
+def gather_frames(local, n_views: int, world: int, rank: int, group=None, dst: int = 0):
+    """Gather every rank's block of frames onto `dst` in camera-path order.
+
+    Ranks hold blocks of unequal length (`partition_views`), so each rank sends a
+    block padded to the largest one. `dst` then drops the padding."""
+    import torch
+    import torch.distributed as dist
+
+    counts = [len(partition_views(n_views, world, r)) for r in range(world)]
+    cap = max(counts)
+    h, w = local.shape[1], local.shape[2]
+    send = local
+    if local.shape[0] != cap:
+        send = torch.zeros((cap, h, w, 3), dtype=local.dtype, device=local.device)
+        send[: local.shape[0]] = local
+    recv = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
+    dist.gather(send, gather_list=recv, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([recv[r][: counts[r]] for r in range(world)], dim=0)

@@ -356,3 +356,35 @@ def test_device_expf_matches_host_glibc(ctx, port):
         assert np.array_equal(ctx.expf(x).view(np.uint32), port.expf(x).view(np.uint32))
     x = np.linspace(-110, 88, 3_000_000, dtype=np.float32)
     assert np.array_equal(ctx.expf(x).view(np.uint32), port.expf(x).view(np.uint32))
+
+
+def test_multiview_single_rank_gpu(port):
+    """multiview driver on the CUDA path: frames rasterised into torch slots
+    (render_async_to) in camera-path order; stereo eye via a camera override."""
+    import torch
+
+    import paper_2604_18980_b200 as P
+    from oracle.ffi import camera_from_dict
+    from paper_2604_18980_b200.multiview import MultiViewRenderer, gpu_render_into, stereo_cameras
+
+    spec = dict(seed=5, count=3000, layout="veil", cameras=4, width=160, height=96, focal=120.0)
+    s = P.synth_scene(**spec)
+    o = port.synth_scene(**spec)
+    r = P.Renderer(0)
+    mv = MultiViewRenderer(gpu_render_into(r), device="cuda")
+    frames, stats = mv.render_path(s, 4, 96, 160, mode="ellipse")
+    frames = frames.cpu().numpy()
+    total = 0
+    for v in range(4):
+        want = port.render(o, o.cameras[v], port.config("ellipse"))
+        total += want["pair_count"]
+        assert np.max(np.abs(frames[v] - want["image"])) <= IMG_MAX_ABS
+        assert stats.per_view_pairs[v] == want["pair_count"]
+    assert stats.frames == 4 and stats.pair_count == total
+    left, right = stereo_cameras(s.camera(0))
+    slot = torch.empty((96, 160, 3), dtype=torch.float32, device="cuda")
+    r.render_async_to(s, 0, slot.data_ptr(), "ellipse", camera=right)
+    st = r.wait()
+    want = port.render(o, camera_from_dict(right), port.config("ellipse"))
+    assert st["pair_count"] == want["pair_count"]
+    assert np.max(np.abs(slot.cpu().numpy() - want["image"])) <= IMG_MAX_ABS

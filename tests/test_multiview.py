@@ -1,0 +1,108 @@
+"""CPU tests of the view-partitioned multi-GPU path.
+
+The partition, gather and stats-reduction logic of
+`paper_2604_18980_b200.multiview` runs here with world_size 2 over gloo. The
+renderer is injected: each rank renders its views with the CPU oracle (test
+infrastructure) into CPU frame slots. Rank 0 then checks the gathered camera
+path frame by frame against single-process oracle renders. On the GPU the same
+driver runs with the CUDA renderer and NCCL (bench.py --gpus N,
+tests/test_gpu_parity.py::test_multiview_single_rank_gpu)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2604_18980_b200.multiview import MultiViewRenderer, partition_views, stereo_cameras
+
+
+@pytest.mark.parametrize("n,world", [(64, 1), (64, 2), (64, 8), (5, 2), (3, 4), (0, 2), (7, 3)])
+def test_partition_views_covers_path_in_order(n, world):
+    blocks = [partition_views(n, world, r) for r in range(world)]
+    flat = [v for b in blocks for v in b]
+    assert flat == list(range(n))
+    sizes = [len(b) for b in blocks]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_partition_views_rejects_bad_rank():
+    with pytest.raises(ValueError):
+        partition_views(4, 2, 2)
+
+
+def test_stereo_right_eye_moves_along_right_vector():
+    cam = {"position": [1.0, 2.0, 3.0], "rotation": [0.6, 0.0, -0.8, 0.0, 1.0, 0.0, 0.8, 0.0, 0.6],
+           "fx": 100.0, "fy": 100.0, "width": 64, "height": 48}
+    left, right = stereo_cameras(cam)
+    assert left["position"] == cam["position"]
+    d = np.asarray(right["position"], np.float32) - np.asarray(cam["position"], np.float32)
+    assert np.allclose(d, 0.064 * np.array([0.6, 0.0, -0.8]), atol=1e-6)
+    assert right["rotation"] == cam["rotation"]
+
+
+SCENE = dict(seed=5, count=600, layout="veil", cameras=5, width=96, height=64, focal=80.0)
+
+
+def _oracle_render_into():
+    from oracle.ffi import Oracle
+
+    port = Oracle("port")
+    scene = port.synth_scene(**SCENE)
+
+    def fn(_scene, view, slot, kw):
+        out = port.render(scene, scene.cameras[view], port.config(kw.get("mode", "ellipse")))
+        slot.copy_(torch.from_numpy(out["image"]))
+        return {"pair_count": out["pair_count"], "splat_count": out["splat_count"],
+                "stage_ms": [1.0 + view, 0.0, 0.0, 0.0]}
+
+    return port, scene, fn
+
+
+def _worker(rank, world, port_no, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _, scene, fn = _oracle_render_into()
+        mv = MultiViewRenderer(fn, device="cpu")
+        frames, stats = mv.render_path(scene, SCENE["cameras"], SCENE["height"], SCENE["width"], mode="ellipse")
+        result_q.put((rank, None if frames is None else frames.numpy(), stats.frames, stats.pair_count,
+                      stats.stage_ms_max))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_gather_camera_path_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = {}
+    for _ in procs:
+        rank, frames, n, pairs, stage_max = q.get(timeout=300)
+        results[rank] = (frames, n, pairs, stage_max)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    port, scene, _ = _oracle_render_into()
+    want = [port.render(scene, scene.cameras[v], port.config("ellipse")) for v in range(SCENE["cameras"])]
+    frames0, n0, pairs0, stage0 = results[0]
+    assert results[1][0] is None  # only the destination receives frames
+    assert frames0.shape == (SCENE["cameras"], SCENE["height"], SCENE["width"], 3)
+    for v in range(SCENE["cameras"]):  # camera-path order, bit-exact copies
+        assert np.array_equal(frames0[v].view(np.uint32), want[v]["image"].view(np.uint32)), v
+    # stats reduced over both ranks: frame and pair counts summed, stage times max
+    for r in (0, 1):
+        assert results[r][1] == SCENE["cameras"]
+        assert results[r][2] == sum(w["pair_count"] for w in want)
+        assert results[r][3][0] == 1.0 + (SCENE["cameras"] - 1)
