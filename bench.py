@@ -385,6 +385,26 @@ def run_ours(args, rank, world, local_rank):
     stages["sort"]["keys_per_s"] = stats["pair_count"] / (stage_ms[2] * 1e-3) if stage_ms[2] else 0.0
     stages["pair_gen"]["pairs_per_s"] = stats["pair_count"] / (stage_ms[1] * 1e-3) if stage_ms[1] else 0.0
     dom = int(np.argmax(stage_ms))
+    # ncu evidence of the same frame (profiles/ncu_frame.json, one --set full
+    # capture): DRAM bytes and warp instructions per frame per stage
+    prof = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_frame.json")) as f:
+            prof = json.load(f)["per_frame"]
+    except Exception:
+        prof = {}
+    for nm in names:
+        if nm in prof:
+            stages[nm]["ncu_dram_bytes"] = prof[nm]["dram_bytes"]
+    props = torch.cuda.get_device_properties(local_rank)
+    sm_mhz = clocks.get("sm_mhz") or 1965.0
+    issue_peak = props.multi_processor_count * 4 * sm_mhz * 1e6  # warp-instructions / s
+    if "raster" in prof and stage_ms[3] > 0:
+        stages["raster"]["issue_roofline"] = {
+            "bound": "issue", "achieved": prof["raster"]["warp_inst"] / (stage_ms[3] * 1e-3),
+            "peak": issue_peak, "unit": "warp-inst/s", "frac": prof["raster"]["warp_inst"] / (stage_ms[3] * 1e-3) / issue_peak,
+            "warp_inst_per_frame": prof["raster"]["warp_inst"],
+            "peak_def": f"{props.multi_processor_count} SMs x 4 SMSPs x 1 warp-inst/clk x {sm_mhz:.0f} MHz"}
     roofline = {
         "bound": "hbm",
         "kernel": names[dom],
@@ -392,10 +412,13 @@ def run_ours(args, rank, world, local_rank):
         "peak": peaks["hbm_gbs"],
         "unit": "GB/s",
         "frac": stages[names[dom]]["frac_hbm"],
-        "traffic": None,
+        "traffic": prof.get(names[dom], {}).get("dram_bytes"),
+        "traffic_src": "profiles/ncu_frame.json (dram__bytes_read.sum + dram__bytes_write.sum, one ncu --set full "
+                       "capture of the same frame)" if names[dom] in prof else None,
         "peak_src": peaks["src"],
         "algorithmic_bytes_per_launch": stages[names[dom]]["algorithmic_bytes"],
-        "note": "raster is issue-bound (SURVEY §8(d)); HBM fraction reported as asked",
+        "note": "raster is issue-bound (SURVEY §8(d)); HBM fraction reported as asked, issue roofline in "
+                "stages.raster.issue_roofline",
     }
 
     # ---- CPU baseline (reference render on host cores) + PSNR vs CPU ref ---

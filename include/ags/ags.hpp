@@ -318,6 +318,35 @@ SynthScene synth_scene(std::uint64_t seed, int count, const SynthSpec& spec);
 // --------------------------------------------------------------- misc
 double psnr(const Image& a, const Image& b);
 
+// analysis.hpp:15-22: PSNR capped at 100 dB (what calibration uses).
+inline constexpr double kPsnrCap = 100.0;
+double psnr_capped(const Image& a, const Image& b);
+
+// ------------------------------------------------- calibration (calibrate.hpp)
+// t_const * 2*pi*sqrt(det(cov2d)) * (x - tau) (calibrate.cpp:67-74).
+double peripheral_score_closed(const SymMat2& cov2d, float x, float t_const, float tau);
+
+struct CalibrationResult {
+    double k = 0.0;
+    TUpperLUT lut;
+    double target_drop = 0.0;    // dB
+    double achieved_drop = 0.0;  // dB, on calibration views
+    int iterations = 0;          // drop evaluations performed
+    std::vector<int> calib_view_ids;
+};
+
+// calibrate.hpp:18-50.  Every render of the loop runs on the GPU with the
+// glibc-exact alpha (images bit-identical to the reference's); reference
+// frames stay in HBM and PSNR numerators are reduced on the device.
+TUpperLUT build_lut(std::span<const Gaussian3D> scene, std::span<const Camera> calib_views,
+                    const RenderConfig& cfg);
+TUpperLUT build_lut(const DeviceScene& scene, std::span<const Camera> calib_views, const RenderConfig& cfg);
+CalibrationResult search_k(std::span<const Gaussian3D> scene, std::span<const Camera> calib_views,
+                           double target_drop, const RenderConfig& cfg, const TUpperLUT& lut,
+                           bool worst_case = false);
+CalibrationResult search_k(const DeviceScene& scene, std::span<const Camera> calib_views, double target_drop,
+                           const RenderConfig& cfg, const TUpperLUT& lut, bool worst_case = false);
+
 }  // namespace ags
 
 // C entry points of libags.so for FFI callers (Python ctypes, bench).

@@ -209,6 +209,23 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
                 int32_t width, int32_t height, const agsx_config* cfg, float* image,
                 float* max_t);
 
+/* ---- calibration primitives (calibrate.cpp:14-155, analysis.cpp:14-29) - */
+/* Device memory owned by the caller (e.g. the calibration reference frames). */
+int agsx_device_alloc(agsx_ctx* ctx, size_t bytes, void** out);
+void agsx_device_free(agsx_ctx* ctx, void* p);
+/* One view of build_lut (calibrate.cpp:26-37): renders `cam` in the lossless
+ * Ellipse mode (cfg's mode is ignored) with glibc-exact alpha and
+ * max-transmittance recording, then folds every blended splat's max_t into
+ * the depth bin of lut_shape (bin_index, lut.hpp:16-23):
+ * folded[b] = max(folded[b], max_t), observed[b] = 1.  folded / observed:
+ * lut_shape->bin_count host entries, updated in place; lut_shape->bins is
+ * not read. */
+int agsx_fold_max_t(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                    const agsx_config* cfg, const agsx_lut* lut_shape, float* folded, uint8_t* observed);
+/* Sum over n floats of ((double)a[i] - b[i])^2 (the numerator of psnr,
+ * analysis.cpp:14-25) for two device arrays; a deterministic tree order. */
+int agsx_sq_err(agsx_ctx* ctx, const float* a, const float* b, uint64_t n, double* out);
+
 /* ---- device libm pinning (glibc-exact logf / expf used on the path) -- */
 int agsx_device_logf(agsx_ctx* ctx, const float* x, float* y, uint64_t n);
 int agsx_device_expf(agsx_ctx* ctx, const float* x, float* y, uint64_t n);

@@ -314,6 +314,28 @@ class Oracle:
             out["max_t"] = mt[: sc.value].copy()
         return out
 
+    def calibrate(self, scene: SoAScene, target_drop: float, calib_views: int = 16, thread_count: int = 0):
+        """Reference calibrate_scene (build_lut + search_k); reference build only."""
+        if not hasattr(self.lib, "ago_calibrate"):
+            raise OracleError(1, "calibrate: only the reference build exports it")
+        n = min(calib_views, len(scene.cameras))
+        cams = (Camera * max(n, 1))(*scene.cameras[:n])
+        k, ach = C.c_double(), C.c_double()
+        it = C.c_int32()
+        bins = np.zeros(64, np.float32)
+        dmin, dmax = C.c_float(), C.c_float()
+        d = scene.desc()
+        f = self.lib.ago_calibrate
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_int32, C.c_void_p, C.c_void_p,
+                      C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+        rc = f(C.addressof(d), C.addressof(cams), n, target_drop, thread_count, C.addressof(k), C.addressof(ach),
+               C.addressof(it), _p(bins), 64, C.addressof(dmin), C.addressof(dmax))
+        if rc:
+            raise OracleError(rc, "calibrate")
+        return {"k": k.value, "achieved_drop": ach.value, "iterations": it.value, "lut_bins": bins[:20].tolist(),
+                "lut_depth_min": dmin.value, "lut_depth_max": dmax.value}
+
     def psnr(self, a, b) -> float:
         a = np.ascontiguousarray(a, np.float32).ravel()
         b = np.ascontiguousarray(b, np.float32).ravel()

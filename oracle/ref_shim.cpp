@@ -21,9 +21,11 @@
 #include <vector>
 
 #include "adagscale/analysis.hpp"
+#include "adagscale/calibrate.hpp"
 #include "adagscale/pair_gen.hpp"
 #include "adagscale/pair_sort.hpp"
 #include "adagscale/preprocess.hpp"
+#include "adagscale/calibrate.hpp"
 #include "adagscale/rasterizer.hpp"
 #include "adagscale/synth.hpp"
 #include "ags_oracle.h"
@@ -318,6 +320,30 @@ int ago_render(const ago_scene* scene, const ago_camera* cam,
             stage_s[2] = rep.stage_times.at("sort");
             stage_s[3] = rep.stage_times.at("raster");
         }
+        return AGO_OK;
+    });
+}
+
+// calibrate_scene of the reference binding (bindings.cpp:104-127):
+// build_lut + search_k (calibrate.cpp:14-155) with a default RenderConfig.
+int ago_calibrate(const ago_scene* scene, const ago_camera* views, int32_t n_views, double target_drop,
+                  int32_t thread_count, double* k, double* achieved, int32_t* iterations, float* bins,
+                  int32_t bin_capacity, float* depth_min, float* depth_max) {
+    return guarded([&] {
+        const auto g = to_scene(scene);
+        std::vector<ags::Camera> cams;
+        for (int i = 0; i < n_views; ++i) cams.push_back(to_cam(&views[i]));
+        ags::RenderConfig cfg;
+        cfg.thread_count = thread_count;
+        const ags::TUpperLUT lut = ags::build_lut(g, cams, cfg);
+        const ags::CalibrationResult r = ags::search_k(g, cams, target_drop, cfg, lut);
+        *k = r.k;
+        *achieved = r.achieved_drop;
+        *iterations = r.iterations;
+        if (static_cast<int>(r.lut.bins.size()) > bin_capacity) return AGO_ECAPACITY;
+        std::memcpy(bins, r.lut.bins.data(), r.lut.bins.size() * sizeof(float));
+        *depth_min = r.lut.depth_min;
+        *depth_max = r.lut.depth_max;
         return AGO_OK;
     });
 }

@@ -10,6 +10,7 @@ from ._core import (  # noqa: F401
     PairBudgetError,
     Renderer,
     Scene,
+    calibrate,
     default_renderer,
     pack_pair_key,
     peripheral_score_closed,
@@ -23,6 +24,7 @@ __all__ = [
     "PairBudgetError",
     "Renderer",
     "Scene",
+    "calibrate",
     "default_renderer",
     "pack_pair_key",
     "peripheral_score_closed",

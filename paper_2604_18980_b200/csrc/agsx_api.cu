@@ -79,7 +79,7 @@ struct agsx_ctx {
     // device arenas (grow-only)
     Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2;
     Buf tkeys, pvals, tkeys2, pvals2;
-    Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext, tile_pit;
+    Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext, tile_pit, calib;
     Buf tmp0, tmp1, tmp2, tmp3, tmp4;
     uint64_t pair_capacity = 0;
 
@@ -578,7 +578,7 @@ void agsx_destroy(agsx_ctx* ctx) {
     for (Buf* b : {&ctx->status, &ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4, &ctx->dkeys,
                    &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
                    &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
-                   &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tile_pit, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
+                   &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tile_pit, &ctx->calib, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
                    &ctx->tmp3, &ctx->tmp4})
         release(*b);
     for (auto& set : ctx->ev_ring)
@@ -1012,6 +1012,77 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
             AGSX_CUDA(cudaMemcpyAsync(max_t, ctx->maxt.p, n_splats * 4, cudaMemcpyDeviceToHost, st));
         AGSX_CUDA(cudaStreamSynchronize(st));
         ctx->have_frame = false;
+        return AGSX_OK;
+    });
+}
+
+int agsx_device_alloc(agsx_ctx* ctx, size_t bytes, void** out) {
+    if (!ctx || !out) return AGSX_EINVAL;
+    *out = nullptr;
+    return guarded(ctx, [&]() -> int {
+        AGSX_CUDA(cudaMalloc(out, std::max<size_t>(bytes, 1)));
+        return AGSX_OK;
+    });
+}
+
+void agsx_device_free(agsx_ctx* ctx, void* p) {
+    if (!ctx || !p) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(p);
+}
+
+int agsx_fold_max_t(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam, const agsx_config* cfg,
+                    const agsx_lut* lut_shape, float* folded, uint8_t* observed) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!cfg || !lut_shape || lut_shape->bin_count < 1 || !folded || !observed)
+            return fail(ctx, AGSX_EINVAL, "fold_max_t: bad arguments");
+        agsx_config c = *cfg;
+        c.mode = AGSX_MODE_ELLIPSE;  // build_lut renders losslessly (calibrate.cpp:22-23)
+        c.flags |= AGSX_FLAG_EXACT_ALPHA;
+        int rc = start_frame(ctx, scene, cam, &c, nullptr, true);
+        if (rc) return rc;
+        rc = finish_frame(ctx, nullptr);
+        if (rc) return rc;
+        const int nb = lut_shape->bin_count;
+        ensure(ctx->calib, static_cast<size_t>(2 * nb) * 4 + 4096 * 8 + 8);
+        uint32_t* dfold = ptr<uint32_t>(ctx->calib);
+        AGSX_CUDA(cudaMemsetAsync(dfold, 0, static_cast<size_t>(2 * nb) * 4, ctx->stream));
+        if (scene->n) {
+            k_fold_max_t<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
+                ptr<uint32_t>(ctx->dvals), ptr<uint32_t>(ctx->dkeys), &ptr<Counters>(ctx->ctr)->m,
+                ptr<uint32_t>(ctx->maxt), lut_shape->depth_min, lut_shape->depth_max, nb, dfold, dfold + nb);
+            check_launch(ctx);
+        }
+        std::vector<uint32_t> h(static_cast<size_t>(2 * nb));
+        AGSX_CUDA(cudaMemcpyAsync(h.data(), dfold, h.size() * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int b = 0; b < nb; ++b) {
+            float v;
+            std::memcpy(&v, &h[b], 4);
+            if (h[nb + b]) {
+                observed[b] = 1;
+                folded[b] = std::max(folded[b], v);
+            }
+        }
+        return AGSX_OK;
+    });
+}
+
+int agsx_sq_err(agsx_ctx* ctx, const float* a, const float* b, uint64_t n, double* out) {
+    if (!ctx || !out) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        constexpr int kBlocks = 1024;  // fixed: the summation order is the same every call
+        ensure(ctx->calib, 4096 * 8 + 8 + 1024);
+        double* part = reinterpret_cast<double*>(static_cast<char*>(ctx->calib.p) + 1024);
+        double* res = part + kBlocks;
+        k_sq_err_partial<<<kBlocks, 256, 0, ctx->stream>>>(a, b, n, part);
+        check_launch(ctx);
+        k_sq_err_final<<<1, 32, 0, ctx->stream>>>(part, kBlocks, res);
+        check_launch(ctx);
+        AGSX_CUDA(cudaMemcpyAsync(out, res, 8, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         return AGSX_OK;
     });
 }

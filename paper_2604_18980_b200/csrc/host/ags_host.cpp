@@ -14,6 +14,7 @@
 
 #include "agsx.h"
 #include "ags/ags.hpp"
+#include "ags_internal.hpp"
 
 namespace ags {
 
@@ -390,7 +391,7 @@ SynthScene synth_scene(std::uint64_t seed, int count, const SynthSpec& spec) {
 }
 
 // ----------------------------------------------------- device plumbing
-namespace {
+namespace detail {
 
 struct CtxHolder {
     agsx_ctx* ctx = nullptr;
@@ -516,7 +517,9 @@ PackedScene pack(std::span<const Gaussian3D> scene) {
     return p;
 }
 
-}  // namespace
+}  // namespace detail
+
+using namespace detail;
 
 DeviceScene::DeviceScene(std::span<const Gaussian3D> scene) {
     const PackedScene p = pack(scene);

@@ -56,6 +56,12 @@ void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const 
                          unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg);
 cudaError_t raster_units_occupancy(int* occ);
 
+__global__ void k_fold_max_t(const uint32_t* order, const uint32_t* dkeys, const uint32_t* m_dev,
+                             const uint32_t* maxt, float dmin, float dmax, int nbins, uint32_t* folded,
+                             uint32_t* observed);
+__global__ void k_sq_err_partial(const float* a, const float* b, uint64_t n, double* partial);
+__global__ void k_sq_err_final(const double* partial, int n, double* out);
+
 __global__ void k_logf(const float* x, float* y, uint64_t n);
 __global__ void k_expf(const float* x, float* y, uint64_t n);
 

@@ -24,6 +24,7 @@
 
 #include "agsx.h"
 #include "ags/ags.hpp"
+#include "ags_internal.hpp"
 
 namespace py = pybind11;
 
@@ -286,6 +287,33 @@ public:
         return out;
     }
 
+    // calibrate_scene (bindings.cpp:104-127 of the reference): LUT from the
+    // first min(calib_views, cameras) views, then the K search; on the GPU.
+    py::dict calibrate(Scene& scene, double target_drop, int calib_views, int threads) {
+        const int n = std::min<int>(calib_views, static_cast<int>(scene.cameras.size()));
+        if (n < 1) throw py::value_error("scene has no cameras");
+        ags::RenderConfig def;
+        def.thread_count = threads;
+        const agsx_config cfg = ags::detail::to_c(def);
+        agsx_scene* dev = device_scene(scene);
+        ags::CalibrationResult res;
+        {
+            py::gil_scoped_release nogil;
+            std::lock_guard<std::mutex> g(mu_);
+            const ags::TUpperLUT lut = ags::detail::build_lut_device(ctx_, dev, scene.cameras.data(), n, cfg);
+            res = ags::detail::search_k_device(ctx_, dev, scene.cameras.data(), n, target_drop, cfg, lut, false);
+        }
+        py::dict out;
+        out["k"] = res.k;
+        out["target_drop"] = res.target_drop;
+        out["achieved_drop"] = res.achieved_drop;
+        out["iterations"] = res.iterations;
+        out["lut_bins"] = res.lut.bins;
+        out["lut_depth_min"] = res.lut.depth_min;
+        out["lut_depth_max"] = res.lut.depth_max;
+        return out;
+    }
+
     py::array_t<float> stage_history(int max_frames) {
         std::vector<float> ms(static_cast<std::size_t>(std::max(max_frames, 0)) * 4);
         int32_t n = 0;
@@ -510,6 +538,14 @@ PYBIND11_MODULE(_core, m) {
         "Render one view on the GPU; returns dict with image, pair_count, splat_count, stage_times");
 
     m.def(
+        "calibrate",
+        [](Scene& scene, double target_drop, int calib_views, int threads) {
+            return default_renderer().calibrate(scene, target_drop, calib_views, threads);
+        },
+        py::arg("scene"), py::arg("target_drop"), py::arg("calib_views") = 16, py::arg("threads") = 0,
+        "Fit the T-upper LUT and binary-search K for a PSNR-drop budget (on the GPU)");
+
+    m.def(
         "psnr",
         [](const f32arr& a, const f32arr& b) {
             check_image(a);
@@ -570,6 +606,8 @@ PYBIND11_MODULE(_core, m) {
              py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27,
              py::arg("camera") = py::none())
         .def("wait", &Renderer::wait)
+        .def("calibrate", &Renderer::calibrate, py::arg("scene"), py::arg("target_drop"), py::arg("calib_views") = 16,
+             py::arg("threads") = 0)
         .def("device_image", &Renderer::device_image)
         .def("stage_history", &Renderer::stage_history, py::arg("max_frames") = 64)
         .def("frame_stats", &Renderer::frame_stats)

@@ -388,3 +388,44 @@ def test_multiview_single_rank_gpu(port):
     want = port.render(o, camera_from_dict(right), port.config("ellipse"))
     assert st["pair_count"] == want["pair_count"]
     assert np.max(np.abs(slot.cpu().numpy() - want["image"])) <= IMG_MAX_ABS
+
+
+def test_calibrate_matches_reference_golden():
+    """GPU calibration (next row f1) against the reference's build_lut +
+    search_k (calibrate.cpp:14-155) on tests/golden/calibration_veil3000.json
+    (made by tests/golden/gen_calibration.py from the reference build).  The
+    renders are glibc-exact, so the LUT (max_t folds) is bit-identical; K and
+    the achieved drop come from the same 22-step bisection."""
+    import json
+    import os
+
+    import paper_2604_18980_b200 as P
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "calibration_veil3000.json")))
+    s = P.synth_scene(**g["spec"])
+    out = P.calibrate(s, g["target_drop"], g["calib_views"])
+    assert np.array_equal(np.float32(out["lut_bins"]).view(np.uint32), np.float32(g["lut_bins"]).view(np.uint32))
+    assert out["iterations"] == g["iterations"]
+    assert out["k"] == g["k"]
+    assert abs(out["achieved_drop"] - g["achieved_drop"]) < 1e-9
+    assert (out["lut_depth_min"], out["lut_depth_max"]) == (g["lut_depth_min"], g["lut_depth_max"])
+
+
+def test_calibrate_config1_veil_reproduces_survey_parameters():
+    """Full-size calibration (veil 100K, 1920x1080, 16 views, 0.5 dB): the
+    reference produced K = 0.3985099792480469 with LUT bins[7] =
+    0.003038157941773534, bins[8] = 0.007012989837676287 and every other bin
+    1.0 (SURVEY.md §8(d), 176 s on 8 CPU threads).  The GPU run must land on
+    the same parameters."""
+    import time
+
+    import paper_2604_18980_b200 as P
+
+    s = P.synth_scene(1, 100_000, "veil", cameras=16, width=1920, height=1080, focal=1500.0)
+    t = time.time()
+    out = P.calibrate(s, 0.5, 16)
+    dt = time.time() - t
+    assert out["k"] == K1080
+    assert np.array_equal(np.float32(out["lut_bins"]), np.float32(LUT_BINS))
+    assert abs(out["achieved_drop"] - 0.499) < 1e-3
+    print(f"GPU calibration: {dt:.2f} s, {out['iterations']} drop evaluations")

@@ -136,3 +136,14 @@ def test_psnr(port):
     a = np.zeros((8, 8, 3), np.float32) + 0.5
     assert math.isinf(port.psnr(a, a))
     assert abs(port.psnr(a, a + np.float32(0.1)) - 20.0) < 1e-4
+
+
+def test_calibration_golden_is_reference(ref):
+    """The calibration golden fixture reproduces from the reference build."""
+    import json
+    import os
+
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "calibration_veil3000.json")))
+    s = ref.synth_scene(**g["spec"])
+    out = ref.calibrate(s, g["target_drop"], g["calib_views"])
+    assert out["k"] == g["k"] and out["lut_bins"] == g["lut_bins"] and out["iterations"] == g["iterations"]
