@@ -27,7 +27,8 @@ EXPORTS = (
     "agsx_dump_sorted_pairs", "agsx_dump_ranges", "agsx_preprocess_view",
     "agsx_generate_pairs", "agsx_sort_pairs", "agsx_raster", "agsx_device_logf",
     "agsx_device_expf", "agsx_kernel_launches", "agsx_stage_history",
-    "agsx_frame_stats", "agsx_host_alloc", "agsx_host_free",
+    "agsx_frame_stats", "agsx_host_alloc", "agsx_host_free", "agsx_device_alloc", "agsx_device_free",
+    "agsx_fold_max_t", "agsx_sq_err",
 )
 
 SPLAT_DTYPE = np.dtype(
