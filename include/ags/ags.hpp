@@ -20,6 +20,7 @@
 #pragma once
 
 #include <array>
+#include <iosfwd>
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
@@ -297,6 +298,42 @@ RenderReport render(std::span<const Gaussian3D> scene, const Camera& cam, const 
                     const TUpperLUT* lut = nullptr, const RecordOptions& rec = {});
 RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderConfig& cfg,
                     const TUpperLUT* lut = nullptr, const RecordOptions& rec = {});
+
+// ------------------------------------------------ scene ingest (gsio.hpp)
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+struct PlyLoadResult {
+    std::vector<Gaussian3D> gaussians;
+    std::size_t rejected = 0;  // elements dropped for non-finite values
+};
+
+// Binary little-endian 3DGS PLY (gsio.cpp:80-152): sigmoid opacity, exp
+// scales, normalised rotation, channel-major f_rest -> coefficient-major SH.
+PlyLoadResult load_ply(std::istream& in);
+PlyLoadResult load_ply_file(const std::string& path);
+
+// Struct-of-arrays form of load_ply_file for the device upload path: the same
+// values, decoded by `threads` host threads (0 = hardware_concurrency) with
+// no per-Gaussian heap allocation.  sh: 3 * sh_coeffs floats per Gaussian.
+struct PlySoA {
+    std::uint64_t count = 0;
+    int sh_coeffs = 1;
+    std::size_t rejected = 0;
+    std::vector<float> mean, scale, rotation, opacity, sh;
+};
+PlySoA load_ply_soa(const std::string& path, int threads = 0);
+
+// synth.cpp:254-281: `count` cameras on a circle of twice the bounding-box
+// diagonal around the scene centre.
+std::vector<Camera> orbit_cameras(const std::vector<Gaussian3D>& gaussians, int count, int width, int height,
+                                  float fx, float fy, std::uint64_t seed);
+std::vector<Camera> orbit_cameras(const float* mean, std::uint64_t n, int count, int width, int height, float fx,
+                                  float fy, std::uint64_t seed);
+
+// gsio.cpp:265-281: binary PPM, clamp to [0,1], lround(v * 255).
+void write_image(const Image& img, const std::string& path);
 
 // ---------------------------------------------------------- synthetic
 struct SynthSpec {

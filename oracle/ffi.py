@@ -336,6 +336,40 @@ class Oracle:
         return {"k": k.value, "achieved_drop": ach.value, "iterations": it.value, "lut_bins": bins[:20].tolist(),
                 "lut_depth_min": dmin.value, "lut_depth_max": dmax.value}
 
+    def load_ply(self, path: str):
+        """Reference load_ply_file (gsio.cpp:80-157) -> (SoAScene without cameras, rejected)."""
+        if not hasattr(self.lib, "ago_load_ply"):
+            raise OracleError(1, "load_ply: only the reference build exports it")
+        f = self.lib.ago_load_ply
+        f.restype = C.c_int
+        f.argtypes = [C.c_char_p] + [C.c_void_p] * 8
+        n, co, rej = C.c_uint64(), C.c_int32(), C.c_uint64()
+        rc = f(path.encode(), C.addressof(n), C.addressof(co), C.addressof(rej), None, None, None, None, None)
+        if rc:
+            raise OracleError(rc, "load_ply")
+        cnt, D = n.value, co.value
+        mean = np.zeros((cnt, 3), np.float32)
+        scale = np.zeros((cnt, 3), np.float32)
+        rot = np.zeros((cnt, 4), np.float32)
+        op = np.zeros(cnt, np.float32)
+        sh = np.zeros((cnt, D, 3), np.float32)
+        rc = f(path.encode(), C.addressof(n), C.addressof(co), C.addressof(rej), _p(mean), _p(scale), _p(rot),
+               _p(op), _p(sh))
+        if rc:
+            raise OracleError(rc, "load_ply")
+        return SoAScene(mean, scale, rot, op, sh, []), rej.value
+
+    def orbit_cameras(self, path: str, count, width, height, fx, fy, seed):
+        """Reference orbit_cameras (synth.cpp:254-281) around the PLY scene at `path`."""
+        f = self.lib.ago_orbit_cameras
+        f.restype = C.c_int
+        f.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_float, C.c_uint64, C.c_void_p]
+        cams = (Camera * max(count, 1))()
+        rc = f(path.encode(), count, width, height, fx, fy, seed, C.cast(cams, C.c_void_p))
+        if rc:
+            raise OracleError(rc, "orbit_cameras")
+        return [cams[i] for i in range(count)]
+
     def psnr(self, a, b) -> float:
         a = np.ascontiguousarray(a, np.float32).ravel()
         b = np.ascontiguousarray(b, np.float32).ravel()

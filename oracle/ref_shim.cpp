@@ -22,6 +22,8 @@
 
 #include "adagscale/analysis.hpp"
 #include "adagscale/calibrate.hpp"
+#include "adagscale/gsio.hpp"
+#include "adagscale/synth.hpp"
 #include "adagscale/pair_gen.hpp"
 #include "adagscale/pair_sort.hpp"
 #include "adagscale/preprocess.hpp"
@@ -344,6 +346,55 @@ int ago_calibrate(const ago_scene* scene, const ago_camera* views, int32_t n_vie
         std::memcpy(bins, r.lut.bins.data(), r.lut.bins.size() * sizeof(float));
         *depth_min = r.lut.depth_min;
         *depth_max = r.lut.depth_max;
+        return AGO_OK;
+    });
+}
+
+// load_ply_file (gsio.cpp:80-157) into SoA; first call with mean == NULL
+// returns the count / SH coefficients / rejected rows.
+int ago_load_ply(const char* path, uint64_t* count, int32_t* coeffs, uint64_t* rejected, float* mean, float* scale,
+                 float* rotation, float* opacity, float* sh) {
+    return guarded([&] {
+        const ags::PlyLoadResult r = ags::load_ply_file(path);
+        *count = r.gaussians.size();
+        *rejected = r.rejected;
+        *coeffs = r.gaussians.empty() ? 1 : static_cast<int32_t>(r.gaussians.front().sh.size() / 3);
+        if (!mean) return AGO_OK;
+        for (std::size_t i = 0; i < r.gaussians.size(); ++i) {
+            const ags::Gaussian3D& g = r.gaussians[i];
+            mean[3 * i] = g.mean.x;
+            mean[3 * i + 1] = g.mean.y;
+            mean[3 * i + 2] = g.mean.z;
+            scale[3 * i] = g.scale.x;
+            scale[3 * i + 1] = g.scale.y;
+            scale[3 * i + 2] = g.scale.z;
+            rotation[4 * i] = g.rotation.w;
+            rotation[4 * i + 1] = g.rotation.x;
+            rotation[4 * i + 2] = g.rotation.y;
+            rotation[4 * i + 3] = g.rotation.z;
+            opacity[i] = g.opacity;
+            std::memcpy(sh + i * g.sh.size(), g.sh.data(), g.sh.size() * sizeof(float));
+        }
+        return AGO_OK;
+    });
+}
+
+// orbit_cameras (synth.cpp:254-281) around the loaded scene of `path`.
+int ago_orbit_cameras(const char* path, int32_t count, int32_t width, int32_t height, float fx, float fy,
+                      uint64_t seed, ago_camera* cams) {
+    return guarded([&] {
+        const ags::PlyLoadResult r = ags::load_ply_file(path);
+        const std::vector<ags::Camera> c = ags::orbit_cameras(r.gaussians, count, width, height, fx, fy, seed);
+        for (std::size_t i = 0; i < c.size(); ++i) {
+            cams[i].position[0] = c[i].position.x;
+            cams[i].position[1] = c[i].position.y;
+            cams[i].position[2] = c[i].position.z;
+            for (int k = 0; k < 9; ++k) cams[i].rotation[k] = c[i].rotation.m[k];
+            cams[i].fx = c[i].fx;
+            cams[i].fy = c[i].fy;
+            cams[i].width = c[i].width;
+            cams[i].height = c[i].height;
+        }
         return AGO_OK;
     });
 }

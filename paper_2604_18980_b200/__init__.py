@@ -12,6 +12,7 @@ from ._core import (  # noqa: F401
     Scene,
     calibrate,
     default_renderer,
+    load_ply,
     pack_pair_key,
     peripheral_score_closed,
     psnr,
@@ -26,6 +27,7 @@ __all__ = [
     "Scene",
     "calibrate",
     "default_renderer",
+    "load_ply",
     "pack_pair_key",
     "peripheral_score_closed",
     "psnr",

@@ -444,6 +444,29 @@ std::shared_ptr<Scene> scene_from_arrays(f32arr mean, f32arr scale, f32arr rotat
     return s;
 }
 
+// load_ply_scene (bindings.cpp:35-42 of the reference): the PLY's Gaussians
+// plus a generated camera orbit; decoded by host threads into the SoA arrays
+// the device upload takes.
+std::shared_ptr<Scene> load_ply_scene(const std::string& path, int orbit_views, int width, int height, float focal,
+                                      std::uint64_t seed) {
+    auto s = std::make_shared<Scene>();
+    std::vector<ags::Camera> cams;
+    {
+        py::gil_scoped_release nogil;
+        ags::PlySoA p = ags::load_ply_soa(path);
+        cams = ags::orbit_cameras(p.mean.data(), p.count, orbit_views, width, height, focal, focal, seed);
+        s->n = p.count;
+        s->D = p.sh_coeffs;
+        s->mean = std::move(p.mean);
+        s->scale = std::move(p.scale);
+        s->rot = std::move(p.rotation);
+        s->op = std::move(p.opacity);
+        s->sh = std::move(p.sh);
+    }
+    for (const ags::Camera& c : cams) s->cameras.push_back(ags::detail::to_c(c));
+    return s;
+}
+
 py::dict camera_dict(const agsx_camera& c) {
     py::dict d;
     d["position"] = std::vector<float>(c.position, c.position + 3);
@@ -536,6 +559,11 @@ PYBIND11_MODULE(_core, m) {
         py::arg("exact") = false, py::arg("max_t") = false,
         py::arg("pair_budget") = std::size_t{1} << 27,
         "Render one view on the GPU; returns dict with image, pair_count, splat_count, stage_times");
+
+    m.def("load_ply", &load_ply_scene, py::arg("path"), py::arg("orbit_views") = 24, py::arg("width") = 640,
+          py::arg("height") = 480, py::arg("focal") = 500.0f, py::arg("seed") = 1,
+          "Trained splat model plus a generated camera orbit");
+    py::register_exception<ags::IoError>(m, "IoError", PyExc_RuntimeError);
 
     m.def(
         "calibrate",

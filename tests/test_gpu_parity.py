@@ -6,6 +6,8 @@ with AGSX_FLAG_EXACT_ALPHA and within max-abs 1e-3 / PSNR >= 50 dB on the
 default (hardware-exp, guard-banded) path.  Known-answer cases follow the
 reference unit suites (file:line cited per test).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -429,3 +431,31 @@ def test_calibrate_config1_veil_reproduces_survey_parameters():
     assert np.array_equal(np.float32(out["lut_bins"]), np.float32(LUT_BINS))
     assert abs(out["achieved_drop"] - 0.499) < 1e-3
     print(f"GPU calibration: {dt:.2f} s, {out['iterations']} drop evaluations")
+
+
+@pytest.mark.parametrize("degree", [1, 3])
+def test_ply_scene_sh_degrees_render(tmp_path, port, degree):
+    """A PLY-ingested scene (row f2) with SH degree 1 / 3 through the device
+    path vs the oracle: counts and keys bit-exact, image within tolerance."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    from plyfixture import write_ply
+
+    import paper_2604_18980_b200 as P
+    from oracle.ffi import SoAScene, camera_from_dict
+
+    path = str(tmp_path / "s.ply")
+    write_ply(path, n=4000, degree=degree, seed=degree)
+    s = P.load_ply(path, orbit_views=3, width=256, height=192, focal=200.0, seed=2)
+    a = s.arrays()
+    o = SoAScene(a["mean"].copy(), a["scale"].copy(), a["rotation"].copy(), a["opacity"].copy(), a["sh"].copy(), [])
+    r = P.Renderer(0)
+    for v in range(3):
+        cam = s.camera(v)
+        got = r.render(s, v, "ellipse")
+        want = port.render(o, camera_from_dict(cam), port.config("ellipse"))
+        assert got["pair_count"] == want["pair_count"] and got["splat_count"] == want["splat_count"]
+        assert np.max(np.abs(got["image"] - want["image"])) <= IMG_MAX_ABS
+        ex = r.render(s, v, "ellipse", exact=True)["image"]
+        assert np.array_equal(ex.view(np.uint32), want["image"].view(np.uint32))
