@@ -342,7 +342,23 @@ def run_ours(args, rank, world, local_rank):
         h2d = ctypes.sizeof(capi.Camera) + ctypes.sizeof(capi.Config) + 4 * len(bins)
         e2e = {"value": world / float(tt.item()), "unit": "frames/s", "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": int(out["image"].nbytes) + 128,
-               "api": "paper_2604_18980_b200.render(scene, view, ...) -> host numpy image (scene resident)"}
+               "api": "paper_2604_18980_b200.render(scene, view, ...) -> host numpy float32 image "
+                      "(scene resident; the rasterizer streams the frame into a pinned host buffer)"}
+        # row f3: the same call with the frame quantised to PPM bytes on the device
+        for _ in range(3):
+            out8 = P.render(scene, view, mode, k, bins, exact=args.exact, image_u8=True)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(steps_e2e):
+            out8 = P.render(scene, view, mode, k, bins, exact=args.exact, image_u8=True)
+        barrier()
+        t8 = torch.tensor([(time.perf_counter() - t0) / steps_e2e], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(t8, op=dist.ReduceOp.MAX)
+        e2e["u8_egress"] = {"value": world / float(t8.item()), "unit": "frames/s",
+                            "d2h_bytes_per_step": int(out8["image"].nbytes) + 128,
+                            "api": "render(..., image_u8=True) -> host uint8 PPM pixels (write_image quantisation "
+                                   "on the GPU)"}
 
     # ---- AdaGScale off, same scene (pairs + FPS) --------------------------
     off = None

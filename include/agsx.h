@@ -145,6 +145,14 @@ uint64_t agsx_scene_count(const agsx_scene* scene);
 int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
                 const agsx_config* cfg, const agsx_lut* lut, agsx_frame* out);
 
+/* ags::render + write_image fused on the device (next row f3): the frame is
+ * quantised to the PPM byte image clamp(v, 0, 1) -> lround(v * 255)
+ * (gsio.cpp:265-281) before it leaves the GPU, so 3 B/pixel cross PCIe
+ * instead of 12.  image_u8: host H*W*3 bytes (written directly when
+ * page-locked); out->image is ignored. */
+int agsx_render_u8(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                   const agsx_config* cfg, const agsx_lut* lut, uint8_t* image_u8, agsx_frame* out);
+
 /* Asynchronous form for benchmarking / batching: enqueues one frame on the
  * ctx stream and returns.  Results stay on the device; agsx_render_wait()
  * synchronises, checks the budget/overflow status and fills counts and

@@ -28,7 +28,7 @@ EXPORTS = (
     "agsx_generate_pairs", "agsx_sort_pairs", "agsx_raster", "agsx_device_logf",
     "agsx_device_expf", "agsx_kernel_launches", "agsx_stage_history",
     "agsx_frame_stats", "agsx_host_alloc", "agsx_host_free", "agsx_device_alloc", "agsx_device_free",
-    "agsx_fold_max_t", "agsx_sq_err",
+    "agsx_fold_max_t", "agsx_sq_err", "agsx_render_u8",
 )
 
 SPLAT_DTYPE = np.dtype(
@@ -183,6 +183,8 @@ class Lib:
         L.agsx_render.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), C.POINTER(Frame)]
         L.agsx_render_async.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut)]
         L.agsx_render_async_to.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp]
+        L.agsx_render_u8.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp,
+                                     C.POINTER(Frame)]
         L.agsx_render_wait.argtypes = [vp, C.POINTER(Frame)]
         L.agsx_device_image.argtypes = [vp, C.POINTER(vp), C.POINTER(i32), C.POINTER(i32)]
         L.agsx_dump_tile_counts.argtypes = [vp, vp, vp, u64]

@@ -700,6 +700,44 @@ int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
     });
 }
 
+int agsx_render_u8(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam, const agsx_config* cfg,
+                   const agsx_lut* lut, uint8_t* image_u8, agsx_frame* out) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!image_u8) return fail(ctx, AGSX_EINVAL, "render_u8: null image");
+        int rc = start_frame(ctx, scene, cam, cfg, lut, false);
+        if (rc) return rc;
+        rc = finish_frame(ctx, out);
+        if (rc) return rc;
+        const uint64_t n = static_cast<uint64_t>(cam->width) * cam->height * 3;
+        uint8_t* dst = nullptr;  // device-visible destination
+        cudaPointerAttributes at{};
+        const bool mapped = cudaPointerGetAttributes(&at, image_u8) == cudaSuccess &&
+                            at.type == cudaMemoryTypeHost && at.devicePointer != nullptr &&
+                            (reinterpret_cast<uintptr_t>(at.devicePointer) & 15u) == 0;
+        cudaGetLastError();
+        if (mapped) {
+            dst = static_cast<uint8_t*>(at.devicePointer);
+        } else {
+            ensure(ctx->tmp0, std::max<uint64_t>(n, 16));
+            dst = ptr<uint8_t>(ctx->tmp0);
+        }
+        const uint64_t n16 = n / 16;
+        if (n16) {
+            const int grid = static_cast<int>(std::min<uint64_t>((n16 + 255) / 256, ctx->num_sms * 8));
+            k_quantize_u8<<<grid, 256, 0, ctx->stream>>>(ptr<float4>(ctx->image), reinterpret_cast<uint4*>(dst), n16);
+            check_launch(ctx);
+        }
+        if (n % 16) {
+            k_quantize_u8_tail<<<1, 16, 0, ctx->stream>>>(ptr<float>(ctx->image), dst, n16 * 16, n);
+            check_launch(ctx);
+        }
+        if (!mapped) AGSX_CUDA(cudaMemcpyAsync(image_u8, dst, n, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return AGSX_OK;
+    });
+}
+
 int agsx_stage_history(agsx_ctx* ctx, float* stage_ms, int32_t max_frames, int32_t* out_frames) {
     if (!ctx || !stage_ms || !out_frames) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {

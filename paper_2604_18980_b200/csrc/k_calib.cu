@@ -56,4 +56,35 @@ __global__ void k_sq_err_final(const double* __restrict__ partial, int n, double
     }
 }
 
+// PPM quantisation of an f32 HWC frame (write_image, gsio.cpp:265-281):
+// clamp to [0, 1], then lround(v * 255) = floor(v * 255 + 0.5) (v * 255 is
+// exact in double).  16 bytes per thread, one 16-byte store.
+__global__ void __launch_bounds__(256)
+k_quantize_u8(const float4* __restrict__ img, uint4* __restrict__ dst, uint64_t n16) {
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float4 v = img[4 * i + q];
+            const float c[4] = {v.x, v.y, v.z, v.w};
+            uint32_t word = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float x = sclamp(c[k], 0.0f, 1.0f);
+                const uint32_t b = static_cast<uint32_t>(floor(static_cast<double>(x) * 255.0 + 0.5));
+                word |= b << (8 * k);
+            }
+            w[q] = word;
+        }
+        dst[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// Tail (n % 16 bytes) of the same quantisation.
+__global__ void k_quantize_u8_tail(const float* __restrict__ img, uint8_t* __restrict__ dst, uint64_t lo, uint64_t n) {
+    const uint64_t i = lo + threadIdx.x;
+    if (i < n) dst[i] = static_cast<uint8_t>(floor(static_cast<double>(sclamp(img[i], 0.0f, 1.0f)) * 255.0 + 0.5));
+}
+
 }  // namespace agsx

@@ -62,6 +62,9 @@ __global__ void k_fold_max_t(const uint32_t* order, const uint32_t* dkeys, const
 __global__ void k_sq_err_partial(const float* a, const float* b, uint64_t n, double* partial);
 __global__ void k_sq_err_final(const double* partial, int n, double* out);
 
+__global__ void k_quantize_u8(const float4* img, uint4* dst, uint64_t n16);
+__global__ void k_quantize_u8_tail(const float* img, uint8_t* dst, uint64_t lo, uint64_t n);
+
 __global__ void k_logf(const float* x, float* y, uint64_t n);
 __global__ void k_expf(const float* x, float* y, uint64_t n);
 

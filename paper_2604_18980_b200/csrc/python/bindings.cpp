@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstring>
 #include <fstream>
+#include <limits>
 #include <memory>
 #include <mutex>
 #include <numbers>
@@ -141,12 +142,13 @@ private:
     std::map<void*, std::size_t> sizes_;
 };
 
-py::array_t<float> pinned_image(int h, int w) {
-    const std::size_t bytes = static_cast<std::size_t>(h) * w * 3 * sizeof(float);
+template <typename T>
+py::array_t<T> pinned_image(int h, int w) {
+    const std::size_t bytes = static_cast<std::size_t>(h) * w * 3 * sizeof(T);
     void* p = PinnedPool::get().acquire(bytes);
-    if (!p) return py::array_t<float>({h, w, 3});  // pageable fallback for the host buffer only
+    if (!p) return py::array_t<T>({h, w, 3});  // pageable fallback for the host buffer only
     py::capsule owner(p, [](void* q) { PinnedPool::get().release(q); });
-    return py::array_t<float>({h, w, 3}, static_cast<float*>(p), owner);
+    return py::array_t<T>({h, w, 3}, static_cast<T*>(p), owner);
 }
 
 agsx_camera camera_from(const py::dict& d) {
@@ -195,13 +197,35 @@ public:
 
     py::dict render(Scene& scene, int view, const std::string& mode, double k,
                     const std::vector<float>& lut_bins, float dmin, float dmax, int threads,
-                    int tile_size, bool exact, bool max_t, std::size_t pair_budget, bool image) {
+                    int tile_size, bool exact, bool max_t, std::size_t pair_budget, bool image,
+                    bool image_u8 = false) {
         const agsx_camera cam = view_of(scene, view);
         const agsx_config cfg = make_config(mode, k, threads, tile_size, exact, pair_budget);
         const LutHolder lut(lut_bins, dmin, dmax);
         agsx_scene* dev = device_scene(scene);
+        if (image && image_u8 && !max_t) {  // frame quantised on the device (row f3)
+            py::array_t<std::uint8_t> img8 = pinned_image<std::uint8_t>(cam.height, cam.width);
+            agsx_frame f{};
+            int rc;
+            {
+                py::gil_scoped_release nogil;
+                std::lock_guard<std::mutex> g(mu_);
+                rc = agsx_render_u8(ctx_, dev, &cam, &cfg, cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr,
+                                    img8.mutable_data(), &f);
+            }
+            if (rc != AGSX_OK) raise_status(rc, ctx_);
+            py::dict out;
+            out["image"] = img8;
+            out["pair_count"] = f.pair_count;
+            out["splat_count"] = f.splat_count;
+            py::dict times;
+            const char* names[4] = {"preprocess", "pair_gen", "sort", "raster"};
+            for (int i = 0; i < 4; ++i) times[names[i]] = f.stage_ms[i] * 1e-3;
+            out["stage_times"] = times;
+            return out;
+        }
         py::array_t<float> img;
-        if (image) img = pinned_image(cam.height, cam.width);
+        if (image) img = pinned_image<float>(cam.height, cam.width);
         std::vector<float> mt;
         agsx_frame f{};
         if (image) f.image = img.mutable_data();
@@ -312,6 +336,21 @@ public:
         out["lut_depth_min"] = res.lut.depth_min;
         out["lut_depth_max"] = res.lut.depth_max;
         return out;
+    }
+
+    // psnr (analysis.cpp:14-25) of two device frames of n floats, numerator
+    // reduced on the GPU (row f3; e.g. torch tensors of a gathered path).
+    double psnr_device(std::uintptr_t a, std::uintptr_t b, std::uint64_t n) {
+        double se = 0.0;
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            std::lock_guard<std::mutex> g(mu_);
+            rc = agsx_sq_err(ctx_, reinterpret_cast<const float*>(a), reinterpret_cast<const float*>(b), n, &se);
+        }
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        if (se == 0.0) return std::numeric_limits<double>::infinity();
+        return 10.0 * std::log10(1.0 / (se / static_cast<double>(n)));
     }
 
     py::array_t<float> stage_history(int max_frames) {
@@ -549,15 +588,15 @@ PYBIND11_MODULE(_core, m) {
         "render",
         [](Scene& scene, int view, const std::string& mode, double k, const std::vector<float>& lut_bins,
            float lut_depth_min, float lut_depth_max, int threads, int tile_size, bool exact, bool max_t,
-           std::size_t pair_budget) {
+           std::size_t pair_budget, bool image_u8) {
             return default_renderer().render(scene, view, mode, k, lut_bins, lut_depth_min, lut_depth_max,
-                                             threads, tile_size, exact, max_t, pair_budget, true);
+                                             threads, tile_size, exact, max_t, pair_budget, true, image_u8);
         },
         py::arg("scene"), py::arg("view") = 0, py::arg("mode") = "ellipse", py::arg("k") = 0.0,
         py::arg("lut_bins") = std::vector<float>{}, py::arg("lut_depth_min") = 0.0f,
         py::arg("lut_depth_max") = 100.0f, py::arg("threads") = 0, py::arg("tile_size") = 16,
         py::arg("exact") = false, py::arg("max_t") = false,
-        py::arg("pair_budget") = std::size_t{1} << 27,
+        py::arg("pair_budget") = std::size_t{1} << 27, py::arg("image_u8") = false,
         "Render one view on the GPU; returns dict with image, pair_count, splat_count, stage_times");
 
     m.def("load_ply", &load_ply_scene, py::arg("path"), py::arg("orbit_views") = 24, py::arg("width") = 640,
@@ -584,6 +623,18 @@ PYBIND11_MODULE(_core, m) {
         },
         py::arg("a"), py::arg("b"));
 
+    m.def(
+        "write_image",
+        [](const py::array_t<std::uint8_t, py::array::c_style>& a, const std::string& path) {
+            // already-quantised PPM bytes (render(..., image_u8=True))
+            if (a.ndim() != 3 || a.shape(2) != 3) throw py::value_error("expected an (H, W, 3) uint8 array");
+            std::ofstream out(path, std::ios::binary);
+            if (!out) throw std::runtime_error("cannot open '" + path + "' for writing");
+            out << "P6\n" << a.shape(1) << " " << a.shape(0) << "\n255\n";
+            out.write(reinterpret_cast<const char*>(a.data()), static_cast<std::streamsize>(a.size()));
+            if (!out) throw std::runtime_error("write failure on '" + path + "'");
+        },
+        py::arg("image"), py::arg("path"));
     m.def(
         "write_image",
         [](const f32arr& a, const std::string& path) {
@@ -623,7 +674,7 @@ PYBIND11_MODULE(_core, m) {
              py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{}, py::arg("lut_depth_min") = 0.0f,
              py::arg("lut_depth_max") = 100.0f, py::arg("threads") = 0, py::arg("tile_size") = 16,
              py::arg("exact") = false, py::arg("max_t") = false, py::arg("pair_budget") = std::size_t{1} << 27,
-             py::arg("image") = true)
+             py::arg("image") = true, py::arg("image_u8") = false)
         .def("render_async", &Renderer::render_async, py::arg("scene"), py::arg("view") = 0,
              py::arg("mode") = "ellipse", py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{},
              py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("tile_size") = 16,
@@ -634,6 +685,7 @@ PYBIND11_MODULE(_core, m) {
              py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27,
              py::arg("camera") = py::none())
         .def("wait", &Renderer::wait)
+        .def("psnr_device", &Renderer::psnr_device, py::arg("a"), py::arg("b"), py::arg("n"))
         .def("calibrate", &Renderer::calibrate, py::arg("scene"), py::arg("target_drop"), py::arg("calib_views") = 16,
              py::arg("threads") = 0)
         .def("device_image", &Renderer::device_image)

@@ -459,3 +459,41 @@ def test_ply_scene_sh_degrees_render(tmp_path, port, degree):
         assert np.max(np.abs(got["image"] - want["image"])) <= IMG_MAX_ABS
         ex = r.render(s, v, "ellipse", exact=True)["image"]
         assert np.array_equal(ex.view(np.uint32), want["image"].view(np.uint32))
+
+
+def test_render_u8_egress_matches_host_quantisation(ctx, port):
+    """Row f3: the device-quantised PPM bytes equal write_image's
+    lround(clamp(v) * 255) of the f32 frame (gsio.cpp:265-281), through the
+    pinned zero-copy path and the pageable copy path."""
+    import ctypes as C
+
+    import paper_2604_18980_b200 as P
+
+    s = P.synth_scene(4, 5000, "veil", cameras=2, width=333, height=211, focal=260.0)  # n % 16 != 0
+    r = P.Renderer(0)
+    f32 = r.render(s, 1, "adagscale", 0.3, [0.7] * 20, exact=True)["image"]
+    want = np.floor(np.clip(f32, 0, 1).astype(np.float64) * 255.0 + 0.5).astype(np.uint8)
+    got = r.render(s, 1, "adagscale", 0.3, [0.7] * 20, exact=True, image_u8=True)["image"]
+    assert got.dtype == np.uint8 and np.array_equal(got, want)
+    a = s.arrays()
+    dev = ctx.upload(a["mean"], a["scale"], a["rotation"], a["opacity"], a["sh"])
+    cam = capi.Camera.from_dict(s.camera(1))
+    buf = np.zeros((211, 333, 3), np.uint8)  # pageable: staged copy
+    f = capi.Frame()
+    rc = ctx.L.agsx_render_u8(ctx.h, dev, C.byref(cam), C.byref(gpu_cfg("adagscale", 0.3, exact=True)),
+                              C.byref(capi.make_lut([0.7] * 20)), buf.ctypes.data, C.byref(f))
+    assert rc == 0 and np.array_equal(buf, want)
+
+
+def test_psnr_device_matches_reference_formula():
+    import torch
+
+    import paper_2604_18980_b200 as P
+
+    a = torch.rand(3 * 1000, device="cuda")
+    b = a + 0.01 * torch.randn(3 * 1000, device="cuda")
+    r = P.Renderer(0)
+    got = r.psnr_device(a.data_ptr(), b.data_ptr(), a.numel())
+    want = P.psnr(a.cpu().numpy().reshape(1, 1000, 3), b.cpu().numpy().reshape(1, 1000, 3))
+    assert abs(got - want) < 1e-9
+    assert r.psnr_device(a.data_ptr(), a.data_ptr(), a.numel()) == float("inf")
