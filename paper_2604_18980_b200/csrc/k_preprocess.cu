@@ -14,6 +14,10 @@
 #include "agsx_internal.cuh"
 #include "kernels.cuh"
 
+#ifndef AGSX_PRE_MINB
+#define AGSX_PRE_MINB 4
+#endif
+
 namespace agsx {
 
 namespace {
@@ -79,7 +83,7 @@ __device__ __forceinline__ void eval_color(const DevScene& sc, uint64_t i, float
 
 }  // namespace
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, AGSX_PRE_MINB)
 k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ status,
              uint32_t* __restrict__ dkeys, Counters* ctr, agsx_splat_view* __restrict__ dump) {
     const int lane = threadIdx.x & 31;

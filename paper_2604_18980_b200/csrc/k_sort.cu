@@ -170,14 +170,29 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         // warp multisplit: the lowest lane of each digit group bumps the
         // warp's counter and gets the old value back; shared-memory atomics
         // of one warp execute in issue order, so ranks follow (item, lane).
+        // all match groups first (independent, so their latencies overlap),
+        // then the in-order counter updates
+        // match groups from 8 ballots over the digit bits (VOTE latency,
+        // instead of MATCH.ANY's); invalid lanes form no group
+        uint32_t peers[kSortItems];
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
             const uint32_t d = digit_of(k[it], shift);
-            const uint32_t peers = __match_any_sync(0xffffffffu, ok[it] ? d : 0x100u + lane);
-            const int leader = __ffs(peers) - 1;
+            uint32_t pm = __ballot_sync(0xffffffffu, ok[it]);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+                pm &= ((d >> b) & 1u) ? bal : ~bal;
+            }
+            peers[it] = ok[it] ? pm : (1u << lane);
+        }
+#pragma unroll
+        for (int it = 0; it < kSortItems; ++it) {
+            const uint32_t d = digit_of(k[it], shift);
+            const int leader = __ffs(peers[it]) - 1;
             uint32_t old = 0;
-            if (ok[it] && leader == lane) old = atomicAdd(&s_whist[warp][d], __popc(peers));
-            rank[it] = __popc(peers & ((1u << lane) - 1u));
+            if (ok[it] && leader == lane) old = atomicAdd(&s_whist[warp][d], __popc(peers[it]));
+            rank[it] = __popc(peers[it] & ((1u << lane) - 1u));
             rank[it] += __shfl_sync(0xffffffffu, old, leader);
         }
         __syncthreads();
