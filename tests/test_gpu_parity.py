@@ -116,6 +116,25 @@ def test_render_config1_veil_adagscale(ctx, port, exact):
     assert out["pair_count"] == 2_357_743  # SURVEY.md §6 [measured] on the reference
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("mode,pairs", [("adagscale", 5_147_441), ("ellipse", 32_844_800)])
+def test_render_config3_full_size_vs_reference(ctx, ref, mode, pairs):
+    """Config 3 (veil 3M, 4608x3456) against the reference build itself
+    (oracle/_ref): survivors, per-Gaussian tile counts, the 5.1M / 32.8M
+    sorted (tile|depth) keys and tile ranges bit-exact; the glibc-exact image
+    bit-identical; the default image within max-abs 1e-3 / PSNR >= 50 dB."""
+    k = float(np.float32(K1080 * (3600.0 / 1500.0) ** 2))
+    oscene, dev = scene_pair(ref, ctx, 1, 3_000_000, "veil", 16, 4608, 3456, 3600.0)
+    bins = LUT_BINS if mode == "adagscale" else None
+    out, oimg = check_frame(ctx, ref, oscene, dev, 0, mode, k=k if mode == "adagscale" else 0.0, lut_bins=bins,
+                            exact=True)
+    assert out["pair_count"] == pairs  # SURVEY.md §8(a) [measured] on the reference
+    fast = ctx.render(dev, to_gpu_cam(oscene.cameras[0]), gpu_cfg(mode, k if mode == "adagscale" else 0.0),
+                      capi.make_lut(bins) if bins else None)["image"]
+    assert np.max(np.abs(fast - oimg)) <= IMG_MAX_ABS
+    assert psnr(fast, oimg) >= IMG_MIN_PSNR
+
+
 def test_fast_alpha_within_tolerance(ctx, port):
     oscene, dev = scene_pair(port, ctx, 9, 4000, "veil", 2, 480, 320, 375.0)
     check_frame(ctx, port, oscene, dev, 0, "ellipse", exact=False)
