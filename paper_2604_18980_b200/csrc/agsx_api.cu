@@ -77,7 +77,7 @@ struct agsx_ctx {
     Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
     // device arenas (grow-only)
-    Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2;
+    Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2, dcounts, chunks;
     Buf tkeys, pvals, tkeys2, pvals2;
     Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext, tile_pit, calib;
     Buf tmp0, tmp1, tmp2, tmp3, tmp4;
@@ -277,6 +277,8 @@ size_t sort_smem(bool k64) {
 }
 
 size_t counters_bytes() { return sizeof(Counters); }
+// 256-splat chunks of the depth order (K3 work units)
+uint64_t chunk_slots(uint64_t n) { return std::max<uint64_t>((n + 255) / 256, 1); }
 
 int sort_grid(agsx_ctx* ctx, bool k64) { return ctx->num_sms * (k64 ? ctx->occ_sort64 : ctx->occ_sort32); }
 
@@ -293,7 +295,7 @@ void sort_hist(agsx_ctx* ctx, const K* keys, const uint32_t* n_dev, uint64_t n_h
 // One stable LSD pass over at most n_host keys (three kernels).
 template <typename K>
 void sort_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, const uint32_t* n_dev,
-               uint64_t n_host, int shift, bool sentinel, uint32_t* n_out) {
+               uint64_t n_host, int shift, bool sentinel, uint32_t* n_out, SortCountOut co = {}) {
     const bool k64 = sizeof(K) == 8;
     const uint64_t tiles = (n_host + kSortTile - 1) / kSortTile;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(
@@ -301,7 +303,7 @@ void sort_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32
     ensure(ctx->sort_counts, static_cast<size_t>(grid) * 256 * 4 + 256 * 4);
     uint32_t* counts = ptr<uint32_t>(ctx->sort_counts);
     launch_sort_pass<K>(grid, sort_smem(k64), ctx->stream, kin, vin, kout, vout, n_dev, n_host, shift, sentinel,
-                        static_cast<K>(~K(0)), counts, counts + static_cast<size_t>(grid) * 256, n_out);
+                        static_cast<K>(~K(0)), counts, counts + static_cast<size_t>(grid) * 256, n_out, co);
     check_launch(ctx);
     ctx->launches += 2;  // three kernels per pass
 }
@@ -325,6 +327,8 @@ void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pi
     ensure(ctx->dvals, std::max<uint64_t>(n, 1) * 4);
     ensure(ctx->dkeys2, std::max<uint64_t>(n, 1) * 4);
     ensure(ctx->dvals2, std::max<uint64_t>(n, 1) * 4);
+    ensure(ctx->dcounts, std::max<uint64_t>(n, 1) * 4);
+    ensure(ctx->chunks, 2 * chunk_slots(n) * 4);
     ensure(ctx->ranges, std::max<uint64_t>(tiles, 1) * 8);
     ensure(ctx->image, std::max<uint64_t>(pixels, 1) * 12);
     ensure(ctx->ctr, counters_bytes());
@@ -401,20 +405,31 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     // compaction) and sets m.
     uint32_t* dk[2] = {ptr<uint32_t>(ctx->dkeys), ptr<uint32_t>(ctx->dkeys2)};
     uint32_t* dv[2] = {ptr<uint32_t>(ctx->dvals), ptr<uint32_t>(ctx->dvals2)};
+    uint32_t* chunk_sum = ptr<uint32_t>(ctx->chunks);
+    uint32_t* chunk_off = chunk_sum + chunk_slots(n);
     if (n > 0) {
+        AGSX_CUDA(cudaMemsetAsync(chunk_sum, 0, chunk_slots(n) * 4, st));
         sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m);
-        for (int ps = 1; ps < 4; ++ps)
+        for (int ps = 1; ps < 4; ++ps) {
+            SortCountOut co;
+            if (ps == 3) {  // the depth order's tile counts + per-chunk sums for K3
+                co.src = ptr<uint32_t>(ctx->status);
+                co.out = ptr<uint32_t>(ctx->dcounts);
+                co.chunk_sum = chunk_sum;
+            }
             sort_pass<uint32_t>(ctx, dk[ps & 1], dv[ps & 1], dk[(ps + 1) & 1], dv[(ps + 1) & 1], &ctr->m, n, 8 * ps,
-                                false, nullptr);
+                                false, nullptr, co);
+        }
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[2], st));
     // K3: scan + emit in depth order
     uint32_t* tk[2] = {ptr<uint32_t>(ctx->tkeys), ptr<uint32_t>(ctx->tkeys2)};
     uint32_t* pv[2] = {ptr<uint32_t>(ctx->pvals), ptr<uint32_t>(ctx->pvals2)};
     if (n > 0) {
-        k_emit<<<ctx->num_sms * ctx->occ_emit, 256, 0, st>>>(p, dv[0], ptr<uint32_t>(ctx->status), pl,
-                                                            tk[0], pv[0], ctx->pair_capacity,
-                                                            ptr<uint64_t>(ctx->lb), ctr, ctx->epoch++);
+        k_scan_chunks<<<1, 1024, 0, st>>>(chunk_sum, chunk_off, ctr, ctx->pair_capacity);
+        check_launch(ctx);
+        k_emit<<<ctx->num_sms * ctx->occ_emit, 256, 0, st>>>(p, dv[0], ptr<uint32_t>(ctx->dcounts), chunk_off, pl,
+                                                            tk[0], pv[0], ctx->pair_capacity, ctr);
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[3], st));
@@ -576,7 +591,7 @@ void agsx_destroy(agsx_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (Buf* b : {&ctx->status, &ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4, &ctx->dkeys,
-                   &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
+                   &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->dcounts, &ctx->chunks, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
                    &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
                    &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tile_pit, &ctx->calib, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
                    &ctx->tmp3, &ctx->tmp4})

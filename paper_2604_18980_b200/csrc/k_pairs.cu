@@ -9,8 +9,9 @@
 // id), so a stable sort on the tile field alone yields exactly the
 // reference's stable (tile, depth, emission order) permutation -- LSD radix
 // order with the 32 depth bits sorted once per splat instead of once per
-// pair.  The exclusive scan of the per-splat tile counts is
-// fused into the emit kernel with a decoupled look-back.
+// pair.  The last depth-sort pass writes the tile counts in
+// depth order and their per-chunk sums; a one-block scan turns those into
+// chunk offsets, so emission needs no look-back.
 #include "kernels.cuh"
 
 namespace agsx {
@@ -41,9 +42,6 @@ __device__ __forceinline__ TileTest planes_tile_test(const FrameParams& p, const
     return t;
 }
 
-// Persistent over the depth-sorted splat list; per 256-splat tile: block
-// scan of tile counts + look-back -> pair offsets, then emission of
-// (tile id, Gaussian id) for every intersected tile in row-major order.
 // Emits f(tx, ty) for the intersected tiles of splat g in row-major order
 // from its P3 hit record (mask) or, for spans over 64 tiles, by re-running
 // the tile test.
@@ -65,27 +63,73 @@ __device__ __forceinline__ void emit_hits(const FrameParams& p, const SplatPlane
     for_each_tile_hit(t, p, f);
 }
 
+// Exclusive scan of the per-chunk sums of tile counts (chunk = 256 splats
+// of the depth order; written by the last depth-sort pass), the serial
+// prefix of generate_pairs (pair_gen.cpp:177-180): chunk offsets, total P
+// (saturating at 2^32 - 1) and the capacity flags.  One block.
+__global__ void __launch_bounds__(1024)
+k_scan_chunks(const uint32_t* __restrict__ chunk_sum, uint32_t* __restrict__ chunk_off, Counters* ctr,
+              uint64_t capacity) {
+    __shared__ unsigned long long s_warp[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = (ctr->m + 255u) / 256u;
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t lo = min(n, tid * per), hi = min(n, lo + per);
+    unsigned long long mine = 0;
+    for (uint32_t c = lo; c < hi; ++c) mine += chunk_sum[c];
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned long long v = s_warp[lane];
+        unsigned long long vi = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) vi += t;
+        }
+        s_warp[lane] = vi - v;
+        if (lane == 31) {
+            const uint32_t pt = vi >= 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(vi);
+            ctr->p = pt;
+            const bool fits = pt != 0xffffffffu && pt <= capacity;
+            ctr->p_eff = fits ? pt : 0u;
+            if (!fits) ctr->overflow = 1u;
+        }
+    }
+    __syncthreads();
+    unsigned long long run = s_warp[warp] + incl - mine;
+    for (uint32_t c = lo; c < hi; ++c) {
+        chunk_off[c] = run >= 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(run);
+        run += chunk_sum[c];
+    }
+}
+
+// Emission in depth order (pair_gen.cpp:187-201): one CTA per 256-splat
+// chunk; block scan of the (sorted) tile counts + the chunk offset give each
+// splat's first pair; pairs (tile id, Gaussian id) are staged in shared memory
+// and written as one contiguous run of the chunk when they fit.
 __global__ void __launch_bounds__(256)
-k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __restrict__ status,
-       SplatPlanes pl, uint32_t* __restrict__ tkeys, uint32_t* __restrict__ pvals,
-       uint64_t capacity, uint64_t* lb_states, Counters* ctr, uint32_t epoch) {
-    __shared__ uint32_t s_tile, s_prefix;
+k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts_sorted,
+       const uint32_t* __restrict__ chunk_off, SplatPlanes pl, uint32_t* __restrict__ tkeys,
+       uint32_t* __restrict__ pvals, uint64_t capacity, const Counters* ctr) {
+    constexpr int kStage = 3072;  // pairs staged per chunk
+    __shared__ uint32_t s_tile[kStage], s_gid[kStage];
     __shared__ uint32_t s_warp[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t n = ctr->m;
-    const uint32_t ntiles = (n + 255u) / 256u;
-    while (true) {
-        if (tid == 0) s_tile = atomicAdd(&ctr->tile_ctr[1], 1u);
-        __syncthreads();
-        const uint32_t tile = s_tile;
-        if (tile >= ntiles) break;
-        const uint32_t j = tile * 256u + tid;
+    const uint32_t m = ctr->m;
+    if (ctr->p_eff == 0u) return;  // nothing fits (overflow: the host grows the arena and re-runs)
+    const uint32_t nchunks = (m + 255u) / 256u;
+    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint32_t j = c * 256u + tid;
         uint32_t g = 0, cnt = 0;
-        if (j < n) {
+        if (j < m) {
             g = order[j];
-            cnt = status[g] & kCountMask;
+            cnt = counts_sorted[j];
         }
-        // block exclusive scan of cnt
         uint32_t incl = cnt;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -93,39 +137,36 @@ k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __rest
         }
         if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
-        if (warp == 0) {
-            const uint32_t v = lane < 8 ? s_warp[lane] : 0u;
-            uint32_t wi = v;
-            for (int o = 1; o < 8; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += t;
-            }
-            const uint32_t total = __shfl_sync(0xffffffffu, wi, 7);
-            if (lane < 8) s_warp[lane] = wi - v;
-            const uint32_t prefix = lookback_warp(lb_states, tile, total, epoch);
-            if (lane == 0) {
-                s_prefix = prefix;
-                if (tile == ntiles - 1) {
-                    const uint32_t pt = sat_add(prefix, total);
-                    ctr->p = pt;
-                    ctr->p_eff = (pt != 0xffffffffu && pt <= capacity) ? pt : 0u;
+        uint32_t wbase = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t v = s_warp[w];
+            wbase += w < warp ? v : 0u;
+            total += v;
+        }
+        const uint32_t local = wbase + incl - cnt;
+        const uint64_t base = chunk_off[c];
+        const bool staged = total <= static_cast<uint32_t>(kStage);
+        if (cnt) {
+            uint32_t at = local;
+            emit_hits(p, pl, g, [&](int tx, int ty) {
+                const uint32_t tile = static_cast<uint32_t>(ty * p.tiles_x + tx);
+                if (staged) {
+                    s_tile[at] = tile;
+                    s_gid[at] = g;
+                } else {
+                    tkeys[base + at] = tile;
+                    pvals[base + at] = g;
                 }
-            }
+                ++at;
+            });
         }
         __syncthreads();
-        if (cnt) {
-            const uint64_t off = static_cast<uint64_t>(s_prefix) + s_warp[warp] + (incl - cnt);
-            if (off + cnt > capacity || s_prefix == 0xffffffffu) {
-                atomicOr(&ctr->overflow, 1u);
-            } else {
-                uint64_t at = off;
-                emit_hits(p, pl, g, [&](int tx, int ty) {
-                    tkeys[at] = static_cast<uint32_t>(ty * p.tiles_x + tx);
-                    pvals[at] = g;
-                    ++at;
-                });
+        if (staged)
+            for (uint32_t i = tid; i < total; i += 256) {
+                tkeys[base + i] = s_tile[i];
+                pvals[base + i] = s_gid[i];
             }
-        }
         __syncthreads();
     }
 }

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kSortThreads, 3)
 k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
             uint32_t* __restrict__ vout, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
             K sentinel, const uint32_t* __restrict__ counts_excl, const uint32_t* __restrict__ totals,
-            uint32_t* n_out) {
+            uint32_t* n_out, SortCountOut co) {
     constexpr int W = kSortThreads / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s_keys = reinterpret_cast<K*>(smem_raw);
@@ -219,11 +219,26 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         }
         __syncthreads();
         const uint32_t tn = s_tile_n;
-        for (uint32_t i = tid; i < tn; i += kSortThreads) {
-            const K key = s_keys[i];
-            const uint32_t pos = s_pos[digit_of(key, shift)] + i;
-            kout[pos] = key;
-            vout[pos] = s_vals[i];
+        const uint32_t tn_round = (tn + 31u) & ~31u;  // whole warps for the aggregated atomics
+        for (uint32_t i = tid; i < tn_round; i += kSortThreads) {
+            const bool act = i < tn;
+            uint32_t pos = 0, val = 0;
+            if (act) {
+                const K key = s_keys[i];
+                pos = s_pos[digit_of(key, shift)] + i;
+                kout[pos] = key;
+                val = s_vals[i];
+                vout[pos] = val;
+            }
+            if (co.src) {  // warp-uniform
+                const uint32_t c = act ? co.src[val] & kCountMask : 0u;
+                if (act) co.out[pos] = c;
+                // consecutive i land in a few 256-splat chunks: one atomic per chunk group
+                const uint32_t chunk = act ? pos >> 8 : 0xffffffffu;
+                const uint32_t peers = __match_any_sync(0xffffffffu, chunk);
+                const uint32_t sum = __reduce_add_sync(peers, c);
+                if (act && (__ffs(peers) - 1) == lane) atomicAdd(&co.chunk_sum[chunk], sum);
+            }
         }
         s_base[tid] += count;
         __syncthreads();
@@ -233,11 +248,11 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
 template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
                       uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift, bool use_sentinel,
-                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out) {
+                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out, SortCountOut co) {
     k_upsweep<K><<<grid, kSortThreads, 0, st>>>(kin, n_dev, n_host, shift, use_sentinel ? 1 : 0, sentinel, counts);
     k_scan_counts<<<256, (grid + 31) / 32 * 32, 0, st>>>(counts, grid, totals);
     k_downsweep<K><<<grid, kSortThreads, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, shift,
-                                                     use_sentinel ? 1 : 0, sentinel, counts, totals, n_out);
+                                                     use_sentinel ? 1 : 0, sentinel, counts, totals, n_out, co);
 }
 
 template <typename K>
@@ -250,10 +265,10 @@ cudaError_t sort_configure(size_t smem, int* occupancy) {
 
 template void launch_sort_pass<uint32_t>(int, size_t, cudaStream_t, const uint32_t*, const uint32_t*, uint32_t*,
                                          uint32_t*, const uint32_t*, uint64_t, int, bool, uint32_t, uint32_t*,
-                                         uint32_t*, uint32_t*);
+                                         uint32_t*, uint32_t*, SortCountOut);
 template void launch_sort_pass<uint64_t>(int, size_t, cudaStream_t, const uint64_t*, const uint32_t*, uint64_t*,
                                          uint32_t*, const uint32_t*, uint64_t, int, bool, uint64_t, uint32_t*,
-                                         uint32_t*, uint32_t*);
+                                         uint32_t*, uint32_t*, SortCountOut);
 template cudaError_t sort_configure<uint32_t>(size_t, int*);
 template cudaError_t sort_configure<uint64_t>(size_t, int*);
 

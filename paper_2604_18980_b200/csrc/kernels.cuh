@@ -14,9 +14,13 @@ __global__ void k_pack_scene(uint64_t n, int D, const float* mean, const float* 
                              const float* rot, const float* op, const float* sh, float4* pos_op,
                              float4* rotq, float4* scale_r, float2* sh_gb, float* sh_rest);
 
-__global__ void k_emit(FrameParams p, const uint32_t* order, const uint32_t* status,
-                       SplatPlanes pl, uint32_t* tkeys, uint32_t* pvals, uint64_t capacity,
-                       uint64_t* lb_states, Counters* ctr, uint32_t epoch);
+// K3 scan: exclusive scan of the per-chunk tile-count sums -> chunk offsets,
+// total P, capacity check (single block).
+__global__ void k_scan_chunks(const uint32_t* chunk_sum, uint32_t* chunk_off, Counters* ctr, uint64_t capacity);
+// K3 emit: one CTA per 256-splat chunk of the depth order.
+__global__ void k_emit(FrameParams p, const uint32_t* order, const uint32_t* counts_sorted,
+                       const uint32_t* chunk_off, SplatPlanes pl, uint32_t* tkeys, uint32_t* pvals,
+                       uint64_t capacity, const Counters* ctr);
 __global__ void k_splats_to_planes(FrameParams p, const agsx_splat_view* splats, uint64_t n,
                                    SplatPlanes pl, uint32_t* counts, uint32_t* depth_bits);
 __global__ void k_emit_list(FrameParams p, uint64_t n, SplatPlanes pl, const uint32_t* counts,
@@ -32,10 +36,18 @@ __global__ void k_ranges_u64(const uint64_t* keys, uint64_t n, uint32_t tile_cou
 // scan + downsweep over `grid` (<= 1024) chunks.  counts: grid*256 u32
 // scratch; totals: 256 u32 scratch.  n_out (optional) receives the number of
 // keys kept (sentinels dropped).
+// Optional by-product of a pass: out[pos] = src[value] & kCountMask for every
+// key written, and chunk_sum[pos >> 8] += that (the per-256-splat sums K3's
+// scan needs).  All null = off.
+struct SortCountOut {
+    const uint32_t* src = nullptr;
+    uint32_t* out = nullptr;
+    uint32_t* chunk_sum = nullptr;
+};
 template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
                       uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift, bool use_sentinel,
-                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out);
+                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out, SortCountOut co = {});
 template <typename K>
 cudaError_t sort_configure(size_t smem, int* occupancy);
 // Histograms of the low `npasses` 8-bit digits into hist[npasses][256]
