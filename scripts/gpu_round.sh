@@ -16,8 +16,8 @@ if [ "${BENCH:-1}" = "1" ]; then
 fi
 if [ "${NCU:-1}" = "1" ]; then
   timeout 240 ncu --metrics gpu__time_duration.sum --clock-control none -c 120 --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-off > /dev/null 2>&1; echo "ncu list rc=$?"
+    python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-off --no-inflight > /dev/null 2>&1; echo "ncu list rc=$?"
   timeout ${NCU_TIMEOUT:-420} ncu --set full --clock-control none --import-source on -k "regex:${NCU_KERNELS:-k_raster|k_preprocess|k_upsweep|k_downsweep|k_scan|k_emit|k_ranges}" \
-    -s ${NCU_SKIP:-23} -c ${NCU_COUNT:-23} -o $OUT/prof -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-off > $OUT/ncu_full.log 2>&1
+    -s ${NCU_SKIP:-23} -c ${NCU_COUNT:-23} -o $OUT/prof -f python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-off --no-inflight > $OUT/ncu_full.log 2>&1
   echo "ncu full rc=$?"; tail -3 $OUT/ncu_full.log
 fi
