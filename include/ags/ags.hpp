@@ -299,6 +299,35 @@ RenderReport render(std::span<const Gaussian3D> scene, const Camera& cam, const 
 RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderConfig& cfg,
                     const TUpperLUT* lut = nullptr, const RecordOptions& rec = {});
 
+// ------------------------------------------- pair report (analysis.hpp:59-82)
+struct ReportSpec {
+    Mode mode;
+    double k = 0.0;  // used only in AdaGScale mode
+};
+
+struct PairReportRow {
+    std::string mode;
+    double k;
+    std::size_t pair_count;      // summed over views
+    double reduction_pct;        // vs ELLIPSE, mean of per-view ratios
+    double psnr_drop_db;         // vs ELLIPSE renders, mean over views
+    double t_preprocess, t_pair_gen, t_sort, t_raster;  // summed seconds (device time)
+};
+
+// analysis.cpp:259-312 (the Table IV methodology) with every render on the
+// GPU: glibc-exact alpha (frames bit-identical to the reference's), lossless
+// reference frames kept in HBM, PSNR numerators reduced on the device.  A
+// missing LUT is built from `views` like the reference does.
+std::vector<PairReportRow> pair_report(const DeviceScene& scene, std::span<const Camera> views,
+                                       std::span<const ReportSpec> specs, const RenderConfig& cfg,
+                                       const TUpperLUT* lut = nullptr);
+std::vector<PairReportRow> pair_report(std::span<const Gaussian3D> scene, std::span<const Camera> views,
+                                       std::span<const ReportSpec> specs, const RenderConfig& cfg,
+                                       const TUpperLUT* lut = nullptr);
+std::string pair_report_csv(std::span<const PairReportRow> rows);
+// Shortest round-trip formatting (std::to_chars), analysis.cpp:314-318.
+std::string format_double(double v);
+
 // ------------------------------------------------ scene ingest (gsio.hpp)
 struct IoError : std::runtime_error {
     using std::runtime_error::runtime_error;

@@ -370,6 +370,22 @@ class Oracle:
             raise OracleError(rc, "orbit_cameras")
         return [cams[i] for i in range(count)]
 
+    def pair_report(self, scene: SoAScene, n_views, specs, lut=None):
+        """Reference pair_report over views [0, n_views): rows of (pair_count, reduction_pct, psnr_drop_db)."""
+        f = self.lib.ago_pair_report
+        f.restype = C.c_int
+        f.argtypes = [C.c_void_p] * 2 + [C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+        cams = (Camera * n_views)(*scene.cameras[:n_views])
+        modes = np.array([MODES[m] for m, _ in specs], np.int32)
+        ks = np.array([k for _, k in specs], np.float64)
+        rows = np.zeros((len(specs), 3), np.float64)
+        d = scene.desc()
+        rc = f(C.addressof(d), C.addressof(cams), n_views, _p(modes), _p(ks), len(specs),
+               C.addressof(lut) if lut is not None else None, _p(rows))
+        if rc:
+            raise OracleError(rc, "pair_report")
+        return rows
+
     def psnr(self, a, b) -> float:
         a = np.ascontiguousarray(a, np.float32).ravel()
         b = np.ascontiguousarray(b, np.float32).ravel()

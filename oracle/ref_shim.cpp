@@ -399,6 +399,28 @@ int ago_orbit_cameras(const char* path, int32_t count, int32_t width, int32_t he
     });
 }
 
+// pair_report (analysis.cpp:259-312) with the given LUT (or a built one when
+// lut is NULL); rows: n_specs x {pair_count, reduction_pct, psnr_drop_db}.
+int ago_pair_report(const ago_scene* scene, const ago_camera* views, int32_t n_views, const int32_t* modes,
+                    const double* ks, int32_t n_specs, const ago_lut* lut, double* rows) {
+    return guarded([&] {
+        const auto g = to_scene(scene);
+        std::vector<ags::Camera> cams;
+        for (int i = 0; i < n_views; ++i) cams.push_back(to_cam(&views[i]));
+        std::vector<ags::ReportSpec> specs;
+        for (int i = 0; i < n_specs; ++i) specs.push_back({static_cast<ags::Mode>(modes[i]), ks[i]});
+        ags::RenderConfig cfg;
+        const ags::TUpperLUT l = to_lut(lut);
+        const auto r = ags::pair_report(g, cams, specs, cfg, lut ? &l : nullptr);
+        for (int i = 0; i < n_specs; ++i) {
+            rows[3 * i] = static_cast<double>(r[i].pair_count);
+            rows[3 * i + 1] = r[i].reduction_pct;
+            rows[3 * i + 2] = r[i].psnr_drop_db;
+        }
+        return AGO_OK;
+    });
+}
+
 double ago_psnr(const float* a, const float* b, uint64_t n) {
     // analysis.cpp:14-25 operates on Image; wrap the flat buffers as 1 x n/3.
     ags::Image ia(static_cast<int>(n / 3), 1), ib(static_cast<int>(n / 3), 1);

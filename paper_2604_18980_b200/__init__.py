@@ -12,8 +12,10 @@ from ._core import (  # noqa: F401
     Scene,
     calibrate,
     default_renderer,
+    format_double,
     load_ply,
     pack_pair_key,
+    pair_report_csv,
     peripheral_score_closed,
     psnr,
     render,
@@ -27,8 +29,10 @@ __all__ = [
     "Scene",
     "calibrate",
     "default_renderer",
+    "format_double",
     "load_ply",
     "pack_pair_key",
+    "pair_report_csv",
     "peripheral_score_closed",
     "psnr",
     "render",

@@ -22,4 +22,8 @@ CalibrationResult search_k_device(agsx_ctx* ctx, const agsx_scene* scene, const 
                                   double target_drop, const agsx_config& cfg, const TUpperLUT& lut,
                                   bool worst_case);
 
+std::vector<PairReportRow> pair_report_device(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* views,
+                                              int n_views, std::span<const ReportSpec> specs,
+                                              const agsx_config& cfg, const TUpperLUT* lut);
+
 }  // namespace ags::detail

@@ -353,6 +353,54 @@ public:
         return 10.0 * std::log10(1.0 / (se / static_cast<double>(n)));
     }
 
+    // pair_report (analysis.cpp:259-312) over views of the scene (row f4).
+    py::list pair_report(Scene& scene, const std::vector<py::tuple>& specs, std::vector<int> views,
+                         const std::vector<float>& lut_bins, float dmin, float dmax, int threads) {
+        if (views.empty())
+            for (int v = 0; v < static_cast<int>(scene.cameras.size()); ++v) views.push_back(v);
+        std::vector<agsx_camera> cams;
+        for (int v : views) cams.push_back(view_of(scene, v));
+        std::vector<ags::ReportSpec> sp;
+        for (const py::tuple& t : specs) {
+            ags::Mode m;
+            if (!ags::parse_mode(t[0].cast<std::string>(), m)) throw py::value_error("unknown mode");
+            sp.push_back({m, t.size() > 1 ? t[1].cast<double>() : 0.0});
+        }
+        ags::RenderConfig def;
+        def.thread_count = threads;
+        const agsx_config cfg = ags::detail::to_c(def);
+        ags::TUpperLUT lut;
+        if (!lut_bins.empty()) {
+            lut.bins = lut_bins;
+            lut.depth_min = dmin;
+            lut.depth_max = dmax;
+        }
+        agsx_scene* dev = device_scene(scene);
+        std::vector<ags::PairReportRow> rows;
+        {
+            py::gil_scoped_release nogil;
+            std::lock_guard<std::mutex> g(mu_);
+            rows = ags::detail::pair_report_device(ctx_, dev, cams.data(), static_cast<int>(cams.size()), sp, cfg,
+                                                   lut_bins.empty() ? nullptr : &lut);
+        }
+        py::list out;
+        for (const auto& r : rows) {
+            py::dict d;
+            d["mode"] = r.mode;
+            d["k"] = r.k;
+            d["pair_count"] = r.pair_count;
+            d["reduction_pct"] = r.reduction_pct;
+            d["psnr_drop_db"] = r.psnr_drop_db;
+            d["t_preprocess"] = r.t_preprocess;
+            d["t_pair_gen"] = r.t_pair_gen;
+            d["t_sort"] = r.t_sort;
+            d["t_raster"] = r.t_raster;
+            d["views"] = cams.size();
+            out.append(d);
+        }
+        return out;
+    }
+
     py::array_t<float> stage_history(int max_frames) {
         std::vector<float> ms(static_cast<std::size_t>(std::max(max_frames, 0)) * 4);
         int32_t n = 0;
@@ -667,6 +715,19 @@ PYBIND11_MODULE(_core, m) {
         py::arg("tau") = 1.0f / 255.0f);
 
     m.def("pack_pair_key", &ags::pack_pair_key, py::arg("tile"), py::arg("depth"));
+    m.def("format_double", &ags::format_double, py::arg("v"), "shortest round-trip (std::to_chars)");
+    m.def(
+        "pair_report_csv",
+        [](const std::vector<py::dict>& rows) {
+            std::vector<ags::PairReportRow> r;
+            for (const py::dict& d : rows)
+                r.push_back({d["mode"].cast<std::string>(), d["k"].cast<double>(), d["pair_count"].cast<std::size_t>(),
+                             d["reduction_pct"].cast<double>(), d["psnr_drop_db"].cast<double>(),
+                             d["t_preprocess"].cast<double>(), d["t_pair_gen"].cast<double>(),
+                             d["t_sort"].cast<double>(), d["t_raster"].cast<double>()});
+            return ags::pair_report_csv(r);
+        },
+        py::arg("rows"));
 
     py::class_<Renderer>(m, "Renderer")
         .def(py::init<int>(), py::arg("device") = 0)
@@ -685,6 +746,9 @@ PYBIND11_MODULE(_core, m) {
              py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27,
              py::arg("camera") = py::none())
         .def("wait", &Renderer::wait)
+        .def("pair_report", &Renderer::pair_report, py::arg("scene"), py::arg("specs"),
+             py::arg("views") = std::vector<int>{}, py::arg("lut_bins") = std::vector<float>{},
+             py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("threads") = 0)
         .def("psnr_device", &Renderer::psnr_device, py::arg("a"), py::arg("b"), py::arg("n"))
         .def("calibrate", &Renderer::calibrate, py::arg("scene"), py::arg("target_drop"), py::arg("calib_views") = 16,
              py::arg("threads") = 0)

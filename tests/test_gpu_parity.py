@@ -516,3 +516,25 @@ def test_psnr_device_matches_reference_formula():
     want = P.psnr(a.cpu().numpy().reshape(1, 1000, 3), b.cpu().numpy().reshape(1, 1000, 3))
     assert abs(got - want) < 1e-9
     assert r.psnr_device(a.data_ptr(), a.data_ptr(), a.numel()) == float("inf")
+
+
+def test_pair_report_matches_reference(ref):
+    """Row f4: pair_report (analysis.cpp:259-312) on the device vs the
+    reference build: pair counts and reductions exact, PSNR drops equal up to
+    the summation order of the squared errors."""
+    import paper_2604_18980_b200 as P
+
+    spec = dict(seed=6, count=4000, layout="veil", cameras=3, width=320, height=240, focal=250.0)
+    s = P.synth_scene(**spec)
+    o = ref.synth_scene(**spec)
+    specs = [("ellipse", 0.0), ("aabb", 0.0), ("adagscale", 0.3), ("adagscale", 0.8)]
+    bins = [0.6] * 20
+    got = P.Renderer(0).pair_report(s, specs, views=[0, 1, 2], lut_bins=bins)
+    want = ref.pair_report(o, 3, specs, ref.lut(bins))
+    for g, (pc, red, drop) in zip(got, want):
+        assert g["pair_count"] == int(pc)
+        assert g["reduction_pct"] == red
+        assert abs(g["psnr_drop_db"] - drop) < 1e-9
+    csv = P.pair_report_csv(got)
+    assert csv.splitlines()[0].startswith("mode,k,pair_count,reduction_vs_ellipse_pct")
+    assert P.format_double(100.0) == "100" and P.format_double(0.5) == "0.5"

@@ -106,3 +106,41 @@ def test_gather_camera_path_world2_gloo():
         assert results[r][1] == SCENE["cameras"]
         assert results[r][2] == sum(w["pair_count"] for w in want)
         assert results[r][3][0] == 1.0 + (SCENE["cameras"] - 1)
+
+
+def _report_worker(rank, world, port_no, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_18980_b200.batch import pair_report
+
+        def local(views):  # stand-in device report: deterministic per-view values
+            return [{"mode": m, "k": k, "views": len(views), "pair_count": sum(100 * v + i for v in views),
+                     "reduction_pct": sum(float(v) for v in views) / len(views),
+                     "psnr_drop_db": sum(0.1 * v for v in views) / len(views),
+                     "t_preprocess": 0.001 * len(views), "t_pair_gen": 0.0, "t_sort": 0.0, "t_raster": 0.0}
+                    for i, (m, k) in enumerate((("ellipse", 0.0), ("adagscale", 0.5)))]
+
+        q.put((rank, pair_report(local, 7)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_pair_report_merges_view_blocks_world2_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_report_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rows in res.values():  # same merged rows on both ranks
+        assert [r["mode"] for r in rows] == ["ellipse", "adagscale"]
+        assert rows[0]["views"] == 7
+        assert rows[0]["pair_count"] == sum(100 * v for v in range(7))
+        assert rows[1]["pair_count"] == sum(100 * v + 1 for v in range(7))
+        assert abs(rows[0]["reduction_pct"] - 3.0) < 1e-12  # mean of 0..6
+        assert abs(rows[0]["psnr_drop_db"] - 0.3) < 1e-12
