@@ -149,51 +149,62 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
     if (c == 0 && tid == 255 && n_out) *n_out = dexcl + total;  // keys kept
     __syncthreads();
 
-    uint64_t lo, hi;
-    chunk_of(n, gridDim.x, c, lo, hi);
-    for (uint64_t tbase = lo; tbase < hi; tbase += kSortTile) {
+    uint64_t lo64, hi64;
+    chunk_of(n, gridDim.x, c, lo64, hi64);
+    const uint32_t lo = static_cast<uint32_t>(lo64), hi = static_cast<uint32_t>(hi64);  // n < 2^32
+    const uint32_t lanemask_lt = (1u << lane) - 1u;
+    for (uint32_t tbase = lo; tbase < hi; tbase += kSortTile) {
         K k[kSortItems];
         uint32_t v[kSortItems];
         uint32_t rank[kSortItems];
         bool ok[kSortItems];
-        const uint64_t wbase = tbase + static_cast<uint64_t>(warp) * 32 * kSortItems;
+        // a full tile without sentinels (the common case) skips every
+        // per-item validity test
+        const bool full = !use_sentinel && hi - tbase >= static_cast<uint32_t>(kSortTile);
+        const uint32_t wbase = tbase + static_cast<uint32_t>(warp) * 32u * kSortItems + lane;
+        if (full) {
 #pragma unroll
-        for (int it = 0; it < kSortItems; ++it) {
-            const uint64_t idx = wbase + it * 32 + lane;
-            ok[it] = idx < hi;
-            k[it] = ok[it] ? kin[idx] : K(0);
-            v[it] = ok[it] ? (vin ? vin[idx] : static_cast<uint32_t>(idx)) : 0u;
-            if (use_sentinel && k[it] == sentinel) ok[it] = false;
+            for (int it = 0; it < kSortItems; ++it) {
+                k[it] = kin[wbase + it * 32];
+                v[it] = vin ? vin[wbase + it * 32] : wbase + it * 32;
+                ok[it] = true;
+            }
+        } else {
+#pragma unroll
+            for (int it = 0; it < kSortItems; ++it) {
+                const uint32_t idx = wbase + it * 32;
+                ok[it] = idx < hi;
+                k[it] = ok[it] ? kin[idx] : K(0);
+                v[it] = ok[it] ? (vin ? vin[idx] : idx) : 0u;
+                if (use_sentinel && k[it] == sentinel) ok[it] = false;
+            }
         }
         for (int d = lane; d < 256; d += 32) s_whist[warp][d] = 0;
         __syncwarp();
-        // warp multisplit: the lowest lane of each digit group bumps the
-        // warp's counter and gets the old value back; shared-memory atomics
-        // of one warp execute in issue order, so ranks follow (item, lane).
-        // all match groups first (independent, so their latencies overlap),
-        // then the in-order counter updates
-        // match groups from 8 ballots over the digit bits (VOTE latency,
-        // instead of MATCH.ANY's); invalid lanes form no group
+        // Warp multisplit, stable in (item, lane) order: the match group of
+        // each item from 8 ballots over its digit bits (VOTE latency instead
+        // of MATCH.ANY's); each lane reads its digit's running warp count,
+        // the group's lowest lane advances it (ordered by __syncwarp).
         uint32_t peers[kSortItems];
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
             const uint32_t d = digit_of(k[it], shift);
-            uint32_t pm = __ballot_sync(0xffffffffu, ok[it]);
+            uint32_t pm = full ? 0xffffffffu : __ballot_sync(0xffffffffu, ok[it]);
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
                 const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
                 pm &= ((d >> b) & 1u) ? bal : ~bal;
             }
-            peers[it] = ok[it] ? pm : (1u << lane);
+            peers[it] = pm;
         }
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
             const uint32_t d = digit_of(k[it], shift);
-            const int leader = __ffs(peers[it]) - 1;
-            uint32_t old = 0;
-            if (ok[it] && leader == lane) old = atomicAdd(&s_whist[warp][d], __popc(peers[it]));
-            rank[it] = __popc(peers[it] & ((1u << lane) - 1u));
-            rank[it] += __shfl_sync(0xffffffffu, old, leader);
+            const uint32_t lt = peers[it] & lanemask_lt;
+            const uint32_t before = s_whist[warp][d];
+            rank[it] = before + __popc(lt);
+            if (ok[it] && lt == 0u) s_whist[warp][d] = before + __popc(peers[it]);
+            __syncwarp();
         }
         __syncthreads();
         uint32_t count = 0;
@@ -210,7 +221,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         __syncthreads();
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
-            if (ok[it]) {
+            if (full || ok[it]) {
                 const uint32_t d = digit_of(k[it], shift);
                 const uint32_t lsi = s_texcl[d] + s_whist[warp][d] + rank[it];
                 s_keys[lsi] = k[it];
