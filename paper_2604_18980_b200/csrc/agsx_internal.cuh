@@ -465,7 +465,7 @@ struct Counters {
     uint32_t p_eff;         // p if it fits the pair buffers, else 0 (memory safety)
     uint32_t pad0;
     unsigned long long p_it;  // pairs iterated before tile saturation (raster work)
-    unsigned long long dbg[4];  // raster work counters (AGSX_RASTER_STATS=1)
+    unsigned long long dbg[8];  // raster work counters (AGSX_RASTER_STATS=1)
 };
 
 }  // namespace agsx

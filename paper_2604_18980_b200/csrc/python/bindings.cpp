@@ -412,13 +412,14 @@ public:
     }
 
     py::dict frame_stats() {
-        std::uint64_t v[10] = {};
-        const int rc = agsx_frame_stats(ctx_, v, 10);
+        std::uint64_t v[12] = {};
+        const int rc = agsx_frame_stats(ctx_, v, 12);
         if (rc != AGSX_OK) raise_status(rc, ctx_);
         py::dict d;
-        const char* names[10] = {"splat_count", "splats_with_tiles", "pair_count", "p_it", "overflow", "tiles",
-                                 "raster_iters", "raster_evals", "raster_fast", "raster_exact"};
-        for (int i = 0; i < 10; ++i) d[names[i]] = v[i];
+        const char* names[12] = {"splat_count", "splats_with_tiles", "pair_count", "p_it", "overflow", "tiles",
+                                 "raster_iters", "raster_evals", "raster_fast", "raster_exact",
+                                 "raster_iters_live_le32", "raster_iters_live_le64"};
+        for (int i = 0; i < 12; ++i) d[names[i]] = v[i];
         return d;
     }
 
