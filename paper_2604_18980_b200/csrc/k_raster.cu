@@ -364,7 +364,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                unsigned long long* __restrict__ pit, unsigned long long* dbg) {
     // STATS: dbg[0] += splat iterations per warp, dbg[1] += live pixel
     // evaluations, dbg[2] += fast blends, dbg[3] += exact re-evaluations
-    unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0;
+    unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0, st_lo32 = 0, st_lo64 = 0;
     constexpr int PPT = 4;
     constexpr int NWB = 8;  // warps per block
     __shared__ __align__(16) float4 sA[NWB][32];
@@ -441,8 +441,13 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 const float qcut = sb.z, qsafe = sb.w;
                 if (STATS) {
                     ++st_it;
+                    uint32_t mine = 0;
 #pragma unroll
-                    for (int k = 0; k < PPT; ++k) st_on += T[k] >= tfloor;
+                    for (int k = 0; k < PPT; ++k) mine += T[k] >= tfloor;
+                    st_on += mine;
+                    const uint32_t live_w = __reduce_add_sync(0xffffffffu, mine);
+                    st_lo32 += live_w <= 32u;
+                    st_lo64 += live_w <= 64u;
                 }
                 // Pixels are not masked once saturated (T < floor): their
                 // remaining blend weights sum to less than T <= floor = 1e-4,
@@ -558,6 +563,8 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             atomicAdd(&dbg[1], st_on);
             atomicAdd(&dbg[2], st_fast);
             atomicAdd(&dbg[3], st_need);
+            atomicAdd(&dbg[4], st_lo32);
+            atomicAdd(&dbg[5], st_lo64);
         }
     }
 }
