@@ -183,6 +183,26 @@ def test_pair_budget_error(ctx, port):
     assert out["pair_count"] > 4
 
 
+def test_pair_arena_regrows_and_budget_boundary(port):
+    """More pairs than the first-guess pair arena (max(12 N, 2^20)): the frame
+    is re-run with a grown arena and still matches the oracle; a budget of
+    exactly P passes, P - 1 raises (pair_gen.cpp:181-184: P > budget)."""
+    ctx = capi.Context(0)  # fresh context: arena at its first guess
+    try:
+        o = port.synth_scene(2, 2000, "slab", cameras=2, width=640, height=480, focal=500.0)
+        o.scale[:] *= 40.0  # every splat covers most of the 1200 tiles -> P >> 2^20
+        dev = ctx.upload(o.mean, o.scale, o.rotation, o.opacity, o.sh)
+        out, _ = check_frame(ctx, port, o, dev, 0, "aabb", exact=True)
+        p = out["pair_count"]
+        assert p > (1 << 20)
+        cam = to_gpu_cam(o.cameras[0])
+        assert ctx.render(dev, cam, gpu_cfg("aabb", pair_budget=p))["pair_count"] == p
+        with pytest.raises(capi.PairBudgetError):
+            ctx.render(dev, cam, gpu_cfg("aabb", pair_budget=p - 1))
+    finally:
+        ctx.close()
+
+
 def test_invalid_config_and_camera(ctx, port):
     oscene, dev = scene_pair(port, ctx, 5, 100, "slab", 2, 64, 48, 100.0)
     cam = to_gpu_cam(oscene.cameras[0])
