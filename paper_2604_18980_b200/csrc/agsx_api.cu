@@ -251,16 +251,19 @@ int raster_ppt(int tile_size) {
     return 16;
 }
 
+bool raster_uses_units(const FrameParams& p, bool maxt) {
+    return p.tile_size == 16 && (p.flags & AGSX_FLAG_EXACT_ALPHA) == 0 && !maxt && p.raster_ppt == 4;
+}
+
 void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
                    const float4* P0, const float4* P1, const float4* P2, float* image,
                    uint32_t* maxt, Counters* ctr) {
     const int grid = p.tiles_x * p.tiles_y;
     if (grid == 0) return;
     const bool exact = (p.flags & AGSX_FLAG_EXACT_ALPHA) != 0;
-    if (p.tile_size == 16 && !exact && maxt == nullptr && p.raster_ppt == 4) {
-        // default path: warp-persistent units (half tiles); per-tile P_it words
-        ensure(ctx->tile_pit, static_cast<size_t>(grid) * 8);
-        AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, static_cast<size_t>(grid) * 8, ctx->stream));
+    if (raster_uses_units(p, maxt != nullptr)) {
+        // default path: warp-persistent units (half tiles); per-tile P_it
+        // words (zeroed at the frame start by the caller)
         launch_raster_units(ctx->num_sms * ctx->occ_raster, ctx->stream, p, ranges, vals, P0, P1, P2, image,
                             &ctr->tile_ctr[3], ptr<unsigned long long>(ctx->tile_pit), &ctr->p_it, ctr->dbg);
         check_launch(ctx);
@@ -390,12 +393,19 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
 
     AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
     AGSX_CUDA(cudaMemsetAsync(ctr, 0, counters_bytes(), st));
+    // every frame-scoped zeroing happens before the first kernel, so the
+    // kernels form one PDL chain
     AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
+    if (n > 0) AGSX_CUDA(cudaMemsetAsync(ctx->chunks.p, 0, chunk_slots(n) * 4, st));
+    if (raster_uses_units(p, maxt)) {
+        ensure(ctx->tile_pit, std::max<uint64_t>(tiles, 1) * 8);
+        AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, tiles * 8, st));
+    }
     if (maxt) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, n * 4, st));
     const SplatPlanes pl = planes_of(ctx);
     if (n > 0) {
         const int grid = static_cast<int>((n + 255) / 256);
-        k_preprocess<<<grid, 256, 0, st>>>(p, sc->view(), pl, ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys),
+        launch_pdl(k_preprocess, dim3(grid), dim3(256), 0, st, p, sc->view(), pl, ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys),
                                             ctr, dump);
         check_launch(ctx);
     }
@@ -408,7 +418,6 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     uint32_t* chunk_sum = ptr<uint32_t>(ctx->chunks);
     uint32_t* chunk_off = chunk_sum + chunk_slots(n);
     if (n > 0) {
-        AGSX_CUDA(cudaMemsetAsync(chunk_sum, 0, chunk_slots(n) * 4, st));
         sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m);
         for (int ps = 1; ps < 4; ++ps) {
             SortCountOut co;
@@ -426,10 +435,10 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     uint32_t* tk[2] = {ptr<uint32_t>(ctx->tkeys), ptr<uint32_t>(ctx->tkeys2)};
     uint32_t* pv[2] = {ptr<uint32_t>(ctx->pvals), ptr<uint32_t>(ctx->pvals2)};
     if (n > 0) {
-        k_scan_chunks<<<1, 1024, 0, st>>>(chunk_sum, chunk_off, ctr, ctx->pair_capacity);
+        launch_pdl(k_scan_chunks, dim3(1), dim3(1024), 0, st, chunk_sum, chunk_off, ctr, ctx->pair_capacity);
         check_launch(ctx);
-        k_emit<<<ctx->num_sms * ctx->occ_emit, 256, 0, st>>>(p, dv[0], ptr<uint32_t>(ctx->dcounts), chunk_off, pl,
-                                                            tk[0], pv[0], ctx->pair_capacity, ctr);
+        launch_pdl(k_emit, dim3(ctx->num_sms * ctx->occ_emit), dim3(256), 0, st, p, dv[0], ptr<uint32_t>(ctx->dcounts),
+                   chunk_off, pl, tk[0], pv[0], ctx->pair_capacity, ctr);
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[3], st));
@@ -442,7 +451,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
                                 8 * ps, false, nullptr);
             cur ^= 1;
         }
-        k_ranges_u32<<<ctx->num_sms * 8, 256, 0, st>>>(tk[cur], &ctr->p_eff, ptr<uint2>(ctx->ranges));
+        launch_pdl(k_ranges_u32, dim3(ctx->num_sms * 8), dim3(256), 0, st, tk[cur], &ctr->p_eff, ptr<uint2>(ctx->ranges));
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
@@ -678,6 +687,40 @@ int agsx_render_async(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera*
                       const agsx_config* cfg, const agsx_lut* lut) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int { return start_frame(ctx, scene, cam, cfg, lut, false); });
+}
+
+// Experiment hook (not in agsx.h): the enqueued frame captured once as a CUDA
+// graph and replayed `iters` times; *ms = device time per replay.
+extern "C" int agsx_debug_graph_replay(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                                       const agsx_config* cfg, const agsx_lut* lut, int iters, float* ms) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        int rc = start_frame(ctx, scene, cam, cfg, lut, false);  // sizes the arenas
+        if (rc) return rc;
+        rc = finish_frame(ctx, nullptr);
+        if (rc) return rc;
+        cudaGraph_t g;
+        AGSX_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        enqueue_frame(ctx, scene, ctx->f_params, false, nullptr);
+        AGSX_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+        cudaGraphExec_t ge;
+        AGSX_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        cudaEvent_t a, b;
+        AGSX_CUDA(cudaEventCreate(&a));
+        AGSX_CUDA(cudaEventCreate(&b));
+        for (int i = 0; i < 3; ++i) AGSX_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        AGSX_CUDA(cudaEventRecord(a, ctx->stream));
+        for (int i = 0; i < iters; ++i) AGSX_CUDA(cudaGraphLaunch(ge, ctx->stream));
+        AGSX_CUDA(cudaEventRecord(b, ctx->stream));
+        AGSX_CUDA(cudaEventSynchronize(b));
+        AGSX_CUDA(cudaEventElapsedTime(ms, a, b));
+        *ms /= iters;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        return AGSX_OK;
+    });
 }
 
 int agsx_render_async_to(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
@@ -1057,6 +1100,10 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
         ensure(ctx->ctr, counters_bytes());
         AGSX_CUDA(cudaMemsetAsync(ctx->ctr.p, 0, counters_bytes(), st));
         Counters* ctr = ptr<Counters>(ctx->ctr);
+        if (raster_uses_units(p, max_t != nullptr)) {
+            ensure(ctx->tile_pit, std::max<uint64_t>(tiles, 1) * 8);
+            AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, tiles * 8, st));
+        }
         launch_raster(ctx, p, ptr<uint2>(ctx->tmp4), ptr<uint32_t>(ctx->tmp3), pl.p0, pl.p1, pl.p2,
                       ptr<float>(ctx->image), max_t ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
         AGSX_CUDA(cudaMemcpyAsync(image, ctx->image.p, static_cast<size_t>(width) * height * 12,

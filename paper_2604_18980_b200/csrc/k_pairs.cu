@@ -70,6 +70,7 @@ __device__ __forceinline__ void emit_hits(const FrameParams& p, const SplatPlane
 __global__ void __launch_bounds__(1024)
 k_scan_chunks(const uint32_t* __restrict__ chunk_sum, uint32_t* __restrict__ chunk_off, Counters* ctr,
               uint64_t capacity) {
+    griddep_wait();
     __shared__ unsigned long long s_warp[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n = (ctr->m + 255u) / 256u;
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(256)
 k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts_sorted,
        const uint32_t* __restrict__ chunk_off, SplatPlanes pl, uint32_t* __restrict__ tkeys,
        uint32_t* __restrict__ pvals, uint64_t capacity, const Counters* ctr) {
+    griddep_wait();
     constexpr int kStage = 3072;  // pairs staged per chunk
     __shared__ uint32_t s_tile[kStage], s_gid[kStage];
     __shared__ uint32_t s_warp[8];
@@ -213,6 +215,7 @@ __global__ void k_emit_list(FrameParams p, uint64_t n, SplatPlanes pl,
 // without pairs keep the {0,0} written by the frame memset.
 __global__ void __launch_bounds__(256)
 k_ranges_u32(const uint32_t* __restrict__ keys, const uint32_t* n_dev, uint2* __restrict__ ranges) {
+    griddep_wait();
     const uint32_t n = *n_dev;
     const uint32_t nq = (n + 3) / 4;  // 16-byte groups (the key buffer is 16-byte aligned)
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < nq; g += gridDim.x * blockDim.x) {

@@ -86,6 +86,7 @@ __device__ __forceinline__ void eval_color(const DevScene& sc, uint64_t i, float
 __global__ void __launch_bounds__(256, AGSX_PRE_MINB)
 k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ status,
              uint32_t* __restrict__ dkeys, Counters* ctr, agsx_splat_view* __restrict__ dump) {
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
 

@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(256 / PPT)
 k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
            const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
            float* __restrict__ image, uint32_t* __restrict__ maxt, unsigned long long* __restrict__ pit) {
+    griddep_wait();
     constexpr int NW = 8 / PPT;  // warps per tile
     constexpr int R = 2 * PPT;   // rows per warp
     __shared__ __align__(16) float4 sA[NW][32];
@@ -362,6 +363,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
                float* __restrict__ image, uint32_t* unit_ctr, unsigned long long* __restrict__ tile_pit,
                unsigned long long* __restrict__ pit, unsigned long long* dbg) {
+    griddep_wait();
     // STATS: dbg[0] += splat iterations per warp, dbg[1] += live pixel
     // evaluations, dbg[2] += fast blends, dbg[3] += exact re-evaluations
     unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0, st_lo32 = 0, st_lo64 = 0;
@@ -578,10 +580,10 @@ void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const 
         return ((e && *e == '1') ? 1 : 0) | ((t && *t == '1') ? 2 : 0);
     }();
     switch (mode) {
-        case 0: k_raster_units<false, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
-        case 1: k_raster_units<true, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
-        case 2: k_raster_units<false, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
-        default: k_raster_units<true, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        case 0: launch_pdl(k_raster_units<false, false>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        case 1: launch_pdl(k_raster_units<true, false>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        case 2: launch_pdl(k_raster_units<false, true>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        default: launch_pdl(k_raster_units<true, true>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
     }
 }
 
@@ -598,6 +600,7 @@ __global__ void __launch_bounds__(256)
 k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
          const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
          float* __restrict__ image, uint32_t* __restrict__ maxt, unsigned long long* __restrict__ pit) {
+    griddep_wait();
     constexpr int B = 256;
     __shared__ __align__(16) float4 sA[2][B];
     __shared__ __align__(16) float4 sB[2][B];
@@ -738,11 +741,11 @@ static void launch16(bool exact, bool maxt, int grid, cudaStream_t st, const Fra
                      const uint32_t* vals, const float4* P0, const float4* P1, const float4* P2, float* image,
                      uint32_t* mt, unsigned long long* pit) {
     if (exact) {
-        if (maxt) k_raster16<Q, true, true><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
-        else k_raster16<Q, true, false><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        if (maxt) launch_pdl(k_raster16<Q, true, true>, dim3(grid), dim3(256 / Q), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else launch_pdl(k_raster16<Q, true, false>, dim3(grid), dim3(256 / Q), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
     } else {
-        if (maxt) k_raster16<Q, false, true><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
-        else k_raster16<Q, false, false><<<grid, 256 / Q, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        if (maxt) launch_pdl(k_raster16<Q, false, true>, dim3(grid), dim3(256 / Q), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else launch_pdl(k_raster16<Q, false, false>, dim3(grid), dim3(256 / Q), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
     }
 }
 
@@ -751,11 +754,11 @@ static void launch_ppt(bool exact, bool maxt, int grid, cudaStream_t st, const F
                        const uint2* ranges, const uint32_t* vals, const float4* P0, const float4* P1,
                        const float4* P2, float* image, uint32_t* mt, unsigned long long* pit) {
     if (exact) {
-        if (maxt) k_raster<PPT, true, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
-        else k_raster<PPT, true, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        if (maxt) launch_pdl(k_raster<PPT, true, true>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else launch_pdl(k_raster<PPT, true, false>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
     } else {
-        if (maxt) k_raster<PPT, false, true><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
-        else k_raster<PPT, false, false><<<grid, 256, 0, st>>>(p, ranges, vals, P0, P1, P2, image, mt, pit);
+        if (maxt) launch_pdl(k_raster<PPT, false, true>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
+        else launch_pdl(k_raster<PPT, false, false>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, mt, pit);
     }
 }
 

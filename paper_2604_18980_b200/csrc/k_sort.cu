@@ -54,6 +54,7 @@ template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
           K sentinel, uint32_t* __restrict__ counts) {
+    griddep_wait();
     constexpr int W = kSortThreads / 32;
     __shared__ uint32_t sh[W][256];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -96,6 +97,7 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
 // threads): counts[c][d] <- sum_{c' < c} counts[c'][d]; totals[d] = column sum.
 __global__ void __launch_bounds__(1024)
 k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ totals) {
+    griddep_wait();
     __shared__ uint32_t s_warp[32];
     const int d = blockIdx.x, c = threadIdx.x, lane = c & 31, warp = c >> 5;
     const uint32_t v = c < G ? counts[static_cast<uint64_t>(c) * 256 + d] : 0u;
@@ -131,6 +133,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             uint32_t* __restrict__ vout, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
             K sentinel, const uint32_t* __restrict__ counts_excl, const uint32_t* __restrict__ totals,
             uint32_t* n_out, SortCountOut co) {
+    griddep_wait();
     constexpr int W = kSortThreads / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s_keys = reinterpret_cast<K*>(smem_raw);
@@ -260,9 +263,9 @@ template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
                       uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift, bool use_sentinel,
                       K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out, SortCountOut co) {
-    k_upsweep<K><<<grid, kSortThreads, 0, st>>>(kin, n_dev, n_host, shift, use_sentinel ? 1 : 0, sentinel, counts);
-    k_scan_counts<<<256, (grid + 31) / 32 * 32, 0, st>>>(counts, grid, totals);
-    k_downsweep<K><<<grid, kSortThreads, smem, st>>>(kin, vin, kout, vout, n_dev, n_host, shift,
+    launch_pdl(k_upsweep<K>, dim3(grid), dim3(kSortThreads), 0, st, kin, n_dev, n_host, shift, use_sentinel ? 1 : 0, sentinel, counts);
+    launch_pdl(k_scan_counts, dim3(256), dim3((grid + 31) / 32 * 32), 0, st, counts, grid, totals);
+    launch_pdl(k_downsweep<K>, dim3(grid), dim3(kSortThreads), smem, st, kin, vin, kout, vout, n_dev, n_host, shift,
                                                      use_sentinel ? 1 : 0, sentinel, counts, totals, n_out, co);
 }
 

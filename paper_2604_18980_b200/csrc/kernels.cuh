@@ -4,6 +4,30 @@
 
 namespace agsx {
 
+// Programmatic dependent launch (PDL): a frame's kernels are launched with
+// programmatic stream serialization allowed, so each one's launch and CTA
+// setup overlap the tail of its predecessor; every such kernel calls
+// griddep_wait() before touching anything its predecessor writes (it then
+// sees all of the predecessor's memory operations).  Without PDL the wait is
+// a no-op.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t c{};
+    c.gridDim = grid;
+    c.blockDim = block;
+    c.dynamicSmemBytes = smem;
+    c.stream = st;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = 1;
+    c.attrs = a;
+    c.numAttrs = 1;
+    return cudaLaunchKernelEx(&c, kernel, static_cast<KArgs>(args)...);
+}
+
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;  // keys per onesweep tile
