@@ -366,7 +366,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
     griddep_wait();
     // STATS: dbg[0] += splat iterations per warp, dbg[1] += live pixel
     // evaluations, dbg[2] += fast blends, dbg[3] += exact re-evaluations
-    unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0, st_lo32 = 0, st_lo64 = 0;
+    unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0, st_lo32 = 0, st_lo64 = 0, st_empty = 0;
     constexpr int PPT = 4;
     constexpr int NWB = 8;  // warps per block
     __shared__ __align__(16) float4 sA[NWB][32];
@@ -471,6 +471,15 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                         st_need += need[k];
                     }
                 }
+                if (STATS) {  // iterations in which no pixel of the unit is within q <= qcut
+                    bool any_in = false;
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) {
+                        const float dy = py[k] - sa.y;
+                        any_in = any_in || !(__fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1) > qcut);
+                    }
+                    st_empty += !__any_sync(0xffffffffu, any_in);
+                }
                 if (sb.y >= aclamp) {  // alpha_at's clamp can bind only for opacity >= clamp
 #pragma unroll
                     for (int k = 0; k < PPT; ++k) e[k] = fminf(e[k], aclamp);
@@ -567,6 +576,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             atomicAdd(&dbg[3], st_need);
             atomicAdd(&dbg[4], st_lo32);
             atomicAdd(&dbg[5], st_lo64);
+            atomicAdd(&dbg[6], st_empty);
         }
     }
 }
