@@ -79,6 +79,30 @@ def gpu_render_into(renderer) -> RenderInto:
     return fn
 
 
+def gpu_render_pipelined(renderers):
+    """A batch renderer over several contexts of one device: consecutive views
+    alternate between the contexts (two streams), so one view's sort overlaps
+    the previous view's raster. Returns ``fn(scene, views, frames, kw) ->
+    [stats per view]``."""
+
+    def fn(scene, views, frames, kw):
+        out = [None] * len(views)
+        pending = {}  # renderer index -> view slot in flight
+        for i, v in enumerate(views):
+            ri = i % len(renderers)
+            r = renderers[ri]
+            if ri in pending:
+                out[pending.pop(ri)] = r.wait()
+            r.render_async_to(scene, v, frames[i].data_ptr(), mode=kw.get("mode", "ellipse"), k=kw.get("k", 0.0),
+                              lut_bins=kw.get("lut_bins", []), exact=kw.get("exact", False), camera=kw.get("camera"))
+            pending[ri] = i
+        for ri, i in pending.items():
+            out[i] = renderers[ri].wait()
+        return out
+
+    return fn
+
+
 class MultiViewRenderer:
     """Renders the views of a camera path owned by this rank and gathers them.
 
@@ -87,8 +111,13 @@ class MultiViewRenderer:
     here, so the gloo test exercises the partition and gather logic without a GPU.
     """
 
-    def __init__(self, render_into: RenderInto, device="cuda"):
+    def __init__(self, render_into: RenderInto = None, device="cuda", batch=None):
+        """Either ``render_into`` (one view at a time) or ``batch`` (a
+        `gpu_render_pipelined` function over several contexts)."""
+        if (render_into is None) == (batch is None):
+            raise ValueError("give exactly one of render_into / batch")
         self.render_into = render_into
+        self.batch = batch
         self.device = device
 
     def render_local(self, scene, views: Sequence[int], height: int, width: int, **kw):
@@ -96,8 +125,9 @@ class MultiViewRenderer:
 
         frames = torch.empty((max(len(views), 1), height, width, 3), dtype=torch.float32, device=self.device)
         stats = PathStats()
-        for i, v in enumerate(views):
-            st = self.render_into(scene, v, frames[i], kw)
+        per_view = (self.batch(scene, list(views), frames, kw) if self.batch is not None else
+                    [self.render_into(scene, v, frames[i], kw) for i, v in enumerate(views)])
+        for v, st in zip(views, per_view):
             stats.frames += 1
             stats.pair_count += int(st["pair_count"])
             stats.splat_count += int(st["splat_count"])

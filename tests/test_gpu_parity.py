@@ -558,3 +558,21 @@ def test_pair_report_matches_reference(ref):
     csv = P.pair_report_csv(got)
     assert csv.splitlines()[0].startswith("mode,k,pair_count,reduction_vs_ellipse_pct")
     assert P.format_double(100.0) == "100" and P.format_double(0.5) == "0.5"
+
+
+def test_multiview_pipelined_two_contexts(port):
+    """Camera path on two contexts of one GPU (frames alternate streams):
+    same frames and stats as the oracle, in path order."""
+    import paper_2604_18980_b200 as P
+    from paper_2604_18980_b200.multiview import MultiViewRenderer, gpu_render_pipelined
+
+    spec = dict(seed=5, count=3000, layout="veil", cameras=5, width=160, height=96, focal=120.0)
+    s = P.synth_scene(**spec)
+    o = port.synth_scene(**spec)
+    mv = MultiViewRenderer(batch=gpu_render_pipelined([P.Renderer(0), P.Renderer(0)]), device="cuda")
+    frames, stats = mv.render_path(s, 5, 96, 160, mode="ellipse", exact=True)
+    frames = frames.cpu().numpy()
+    for v in range(5):
+        want = port.render(o, o.cameras[v], port.config("ellipse"))
+        assert np.array_equal(frames[v].view(np.uint32), want["image"].view(np.uint32))
+        assert stats.per_view_pairs[v] == want["pair_count"]
