@@ -37,7 +37,7 @@ PY_INC   := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_paths()['
 PYBIND   := $(shell $(PYTHON) -c "import pybind11;print(pybind11.get_include())")
 CORE     := $(PKG)/_core$(PY_EXT)
 
-all: $(LIBDIR)/libagsx.so $(LIBDIR)/libags.so $(CORE) oracle
+all: $(LIBDIR)/libagsx.so $(LIBDIR)/libags.so $(CORE) $(LIBDIR)/render_cli oracle
 .PHONY: all oracle clean
 
 build/%.o: $(CSRC)/%.cu $(CU_HDRS)
@@ -59,6 +59,10 @@ $(LIBDIR)/libags.so: $(HOST_OBJS) $(LIBDIR)/libagsx.so
 $(CORE): $(CSRC)/python/bindings.cpp $(LIBDIR)/libags.so $(HOST_HDRS)
 	$(CXX) $(HOSTFLAGS) -shared -I$(PY_INC) -I$(PYBIND) $< -o $@ -L$(LIBDIR) -lags -lagsx \
 	    -Wl,-rpath,'$$ORIGIN/lib'
+
+# a reference-style C++ caller of the drop-in API (tests/cxx)
+$(LIBDIR)/render_cli: tests/cxx/render_cli.cpp $(LIBDIR)/libags.so $(HOST_HDRS)
+	$(CXX) $(HOSTFLAGS) $< -o $@ -L$(LIBDIR) -lags -lagsx -Wl,-rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle liboracle

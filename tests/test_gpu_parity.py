@@ -576,3 +576,28 @@ def test_multiview_pipelined_two_contexts(port):
         want = port.render(o, o.cameras[v], port.config("ellipse"))
         assert np.array_equal(frames[v].view(np.uint32), want["image"].view(np.uint32))
         assert stats.per_view_pairs[v] == want["pair_count"]
+
+
+@pytest.mark.parametrize("layout,mode,k,lutbin", [("veil", "adagscale", 0.3, 0.6), ("slab", "ellipse", 0.0, None),
+                                                  ("aniso", "obb", 0.0, None)])
+def test_cxx_drop_in_caller(tmp_path, port, layout, mode, k, lutbin):
+    """A C++ program written against include/ags/ags.hpp (tests/cxx/render_cli.cpp)
+    calls ags::render(std::span<const Gaussian3D>, ...) like the reference's
+    callers: pair/splat counts equal the oracle's, the image is within
+    tolerance, the DeviceScene overload agrees, and the reference's exception
+    types come back (invalid_argument x2, PairBudgetError)."""
+    import json
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_2604_18980_b200", "lib", "render_cli")
+    out = tmp_path / "img.f32"
+    args = [exe, "11", "3000", layout, "320", "240", "250", "1", mode, str(k), str(out)]
+    if lutbin is not None:
+        args.append(str(lutbin))
+    res = json.loads(subprocess.run(args, check=True, capture_output=True, text=True).stdout.strip().splitlines()[-1])
+    o = port.synth_scene(11, 3000, layout, cameras=2, width=320, height=240, focal=250.0)
+    want = port.render(o, o.cameras[1], port.config(mode, k=k), port.lut([lutbin] * 20) if lutbin else None)
+    assert res["pair_count"] == want["pair_count"] and res["splat_count"] == want["splat_count"]
+    img = np.fromfile(out, np.float32).reshape(240, 320, 3)
+    assert np.max(np.abs(img - want["image"])) <= IMG_MAX_ABS
+    assert res["device_scene_same"] and res["errors_ok"] == 3 and res["stage_keys"] == 4

@@ -38,9 +38,9 @@ def test_libags_cxx_api_loads():
 
 
 def test_module_surface_mirrors_reference():
-    # adagscale/__init__.py:4-26 minus the out-of-scope calibrate/load_ply (SURVEY §2 rows 12,14)
-    for name in ("Scene", "pack_pair_key", "peripheral_score_closed", "psnr", "render", "synth_scene",
-                 "write_image"):
+    # adagscale/__init__.py:4-26, every name (calibrate / load_ply are the next rows f1 / f2)
+    for name in ("Scene", "calibrate", "load_ply", "pack_pair_key", "peripheral_score_closed", "psnr", "render",
+                 "synth_scene", "write_image"):
         assert hasattr(P, name)
 
 
