@@ -200,9 +200,14 @@ FrameParams make_params(const agsx_camera& cam, const agsx_config& cfg, const ag
     FrameParams p;
     std::memset(&p, 0, sizeof(p));
     for (int i = 0; i < 3; ++i) p.cam_pos[i] = cam.position[i];
-    for (int i = 0; i < 9; ++i) p.R[i] = cam.rotation[i];
+    for (int i = 0; i < 9; ++i) {
+        p.R[i] = cam.rotation[i];
+        p.Rd[i] = static_cast<double>(cam.rotation[i]);
+    }
     p.fx = cam.fx;
     p.fy = cam.fy;
+    p.fxd = static_cast<double>(cam.fx);
+    p.fyd = static_cast<double>(cam.fy);
     p.W = cam.width;
     p.H = cam.height;
     p.ppx = 0.5f * static_cast<float>(cam.width);

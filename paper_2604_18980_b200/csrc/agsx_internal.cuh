@@ -25,6 +25,7 @@ struct FrameParams {
     int W, H;
     float ppx, ppy;       // principal_point(): 0.5f * (float)W, 0.5f * (float)H
     double lim_x, lim_y;  // guard_band * 0.5 * W / fx (preprocess.cpp:45-46), host-evaluated
+    double Rd[9], fxd, fyd;  // exact double copies of R, fx, fy (no per-thread conversions)
     // config (scene.hpp:65-78)
     int tile_size, tiles_x, tiles_y;
     int mode;
@@ -248,15 +249,16 @@ __device__ __forceinline__ void for_each_tile_hit(const TileTest& t, const Frame
     const float ts = static_cast<float>(p.tile_size);
     const float W = static_cast<float>(p.W), H = static_cast<float>(p.H);
     const float cx = t.cx, cy = t.cy;
-    for (int ty = s.ty0; ty <= s.ty1; ++ty) {
-        const float y0 = ty * ts;
+    float y0 = static_cast<float>(s.ty0) * ts;  // tile coordinates advance by exact float adds
+    const float x0_first = static_cast<float>(s.tx0) * ts;
+    for (int ty = s.ty0; ty <= s.ty1; ++ty, y0 += ts) {
         const float y1 = smin(y0 + ts, H);
         const float dy0 = y0 - cy, dy1 = y1 - cy;
         const float xh0 = cx - t.ixy * dy0 / t.ixx;
         const float xh1 = cx - t.ixy * dy1 / t.ixx;
         const bool row_in = cy >= y0 && cy <= y1;
-        for (int tx = s.tx0; tx <= s.tx1; ++tx) {
-            const float x0 = tx * ts;
+        float x0 = x0_first;
+        for (int tx = s.tx0; tx <= s.tx1; ++tx, x0 += ts) {
             const float x1 = smin(x0 + ts, W);
             if (!box_overlap(x0, y0, x1, y1, cx, cy, t.rx, t.ry)) continue;
             bool hit = row_in && cx >= x0 && cx <= x1;  // centre inside: min = 0 <= r2

@@ -119,12 +119,12 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
             const double iz = 1.0 / static_cast<double>(tz);
             const double txc = sclampd(tx * iz, -p.lim_x, p.lim_x) * tz;
             const double tyc = sclampd(ty * iz, -p.lim_y, p.lim_y) * tz;
-            const double j00 = p.fx * iz, j01 = 0.0, j02 = -p.fx * txc * iz * iz;
-            const double j10 = 0.0, j11 = p.fy * iz, j12 = -p.fy * tyc * iz * iz;
+            const double j00 = p.fxd * iz, j01 = 0.0, j02 = -p.fxd * txc * iz * iz;
+            const double j10 = 0.0, j11 = p.fyd * iz, j12 = -p.fyd * tyc * iz * iz;
             // jw = J * W  (rows 0, 1; Mat3 product math.hpp:50-59, s = 0 then +=)
             double jw[2][3];
             for (int c = 0; c < 3; ++c) {
-                const double w0 = p.R[c], w1 = p.R[3 + c], w2 = p.R[6 + c];
+                const double w0 = p.Rd[c], w1 = p.Rd[3 + c], w2 = p.Rd[6 + c];
                 double s = 0.0;
                 s += j00 * w0;
                 s += j01 * w1;
