@@ -156,7 +156,9 @@ def cpu_reference(cfg: str, mode: str, frames: int, warmup: int, want_image=Fals
     f = 500.0 * w / 640.0
     scene = o.synth_scene(1, n, "veil", cameras=cams, width=w, height=h, focal=f)
     threads = os.cpu_count() or 1
-    c = o.config(mode, k=scaled_k(w) if mode == "adagscale" else 0.0, thread_count=threads)
+    extra = {"fixed_radius_aabb": 1} if mode == "aabb_fixed3" else {}
+    c = o.config("aabb" if mode == "aabb_fixed3" else mode, k=scaled_k(w) if mode == "adagscale" else 0.0,
+                 thread_count=threads, **extra)
     lut = o.lut(LUT_BINS) if mode == "adagscale" else None
     times, out = [], None
     for i in range(warmup + frames):
@@ -540,7 +542,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
-    ap.add_argument("--mode", default="adagscale", choices=["adagscale", "ellipse", "aabb", "obb"])
+    ap.add_argument("--mode", default="adagscale", choices=["adagscale", "ellipse", "aabb", "obb", "aabb_fixed3"])
     ap.add_argument("--exact", action="store_true", help="glibc-exact alpha (bit-identical images)")
     ap.add_argument("--cpu-frames", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")

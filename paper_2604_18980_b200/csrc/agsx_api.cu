@@ -73,7 +73,8 @@ struct agsx_ctx {
     uint64_t launches = 0;
     uint32_t epoch = 1;
     int num_sms = 148;
-    int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1, occ_raster = 1;
+    int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1, occ_emit_big = 1, occ_raster = 1;
+    double pairs_per_splat = 0.0;  // previous frame's P / M (picks the emit stage)
     Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
     // device arenas (grow-only)
@@ -442,8 +443,10 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     if (n > 0) {
         launch_pdl(k_scan_chunks, dim3(1), dim3(1024), 0, st, chunk_sum, chunk_off, ctr, ctx->pair_capacity);
         check_launch(ctx);
-        launch_pdl(k_emit, dim3(ctx->num_sms * ctx->occ_emit), dim3(256), 0, st, p, dv[0], ptr<uint32_t>(ctx->dcounts),
-                   chunk_off, pl, tk[0], pv[0], ctx->pair_capacity, ctr);
+        // the big stage when the previous frame averaged > 10 pairs per splat
+        const bool big = ctx->pairs_per_splat > 10.0;
+        AGSX_CUDA(launch_emit(big, ctx->num_sms * (big ? ctx->occ_emit_big : ctx->occ_emit), st, p, dv[0],
+                              ptr<uint32_t>(ctx->dcounts), chunk_off, pl, tk[0], pv[0], ctx->pair_capacity, ctr));
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[3], st));
@@ -535,6 +538,7 @@ int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
             enqueue_frame(ctx, ctx->f_scene, ctx->f_params, ctx->f_maxt, nullptr);
             continue;
         }
+        ctx->pairs_per_splat = c.m ? static_cast<double>(c.p) / c.m : 0.0;
         if (out) {
             out->pair_count = c.p;
             out->splat_count = c.s;
@@ -579,7 +583,9 @@ int agsx_create(int device, agsx_ctx** out) {
         AGSX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
         AGSX_CUDA(sort_configure<uint32_t>(sort_smem(false), &ctx->occ_sort32));
         AGSX_CUDA(sort_configure<uint64_t>(sort_smem(true), &ctx->occ_sort64));
-        AGSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ_emit, k_emit, 256, 0));
+        AGSX_CUDA(emit_configure(false, &ctx->occ_emit));
+        AGSX_CUDA(emit_configure(true, &ctx->occ_emit_big));
+        ctx->occ_emit_big = std::max(ctx->occ_emit_big, 1);
         AGSX_CUDA(raster_units_occupancy(&ctx->occ_raster));
         ctx->occ_raster = std::max(ctx->occ_raster, 1);
         ctx->occ_sort32 = std::max(ctx->occ_sort32, 1);

@@ -113,13 +113,16 @@ k_scan_chunks(const uint32_t* __restrict__ chunk_sum, uint32_t* __restrict__ chu
 // chunk; block scan of the (sorted) tile counts + the chunk offset give each
 // splat's first pair; pairs (tile id, Gaussian id) are staged in shared memory
 // and written as one contiguous run of the chunk when they fit.
+template <int STAGE>
 __global__ void __launch_bounds__(256)
 k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts_sorted,
        const uint32_t* __restrict__ chunk_off, SplatPlanes pl, uint32_t* __restrict__ tkeys,
        uint32_t* __restrict__ pvals, uint64_t capacity, const Counters* ctr) {
     griddep_wait();
-    constexpr int kStage = 3072;  // pairs staged per chunk
-    __shared__ uint32_t s_tile[kStage], s_gid[kStage];
+    extern __shared__ __align__(16) uint32_t emit_stage[];  // STAGE tile ids, then STAGE Gaussian ids
+    uint32_t* s_tile = emit_stage;
+    uint32_t* s_gid = emit_stage + STAGE;
+    constexpr int kStage = STAGE;
     __shared__ uint32_t s_warp[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t m = ctr->m;
@@ -171,6 +174,24 @@ k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __rest
             }
         __syncthreads();
     }
+}
+
+cudaError_t launch_emit(bool big, int grid, cudaStream_t st, const FrameParams& p, const uint32_t* order,
+                        const uint32_t* counts_sorted, const uint32_t* chunk_off, const SplatPlanes& pl,
+                        uint32_t* tkeys, uint32_t* pvals, uint64_t capacity, const Counters* ctr) {
+    if (big)
+        return launch_pdl(k_emit<kEmitStageBig>, dim3(grid), dim3(256), emit_smem(true), st, p, order, counts_sorted,
+                          chunk_off, pl, tkeys, pvals, capacity, ctr);
+    return launch_pdl(k_emit<kEmitStageSmall>, dim3(grid), dim3(256), emit_smem(false), st, p, order, counts_sorted,
+                      chunk_off, pl, tkeys, pvals, capacity, ctr);
+}
+
+cudaError_t emit_configure(bool big, int* occupancy) {
+    const void* f = big ? reinterpret_cast<const void*>(k_emit<kEmitStageBig>)
+                        : reinterpret_cast<const void*>(k_emit<kEmitStageSmall>);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(emit_smem(big)));
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occupancy, f, 256, emit_smem(big));
 }
 
 // Standalone generate_pairs over a splat list (agsx_generate_pairs):

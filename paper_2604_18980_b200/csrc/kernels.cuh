@@ -41,10 +41,15 @@ __global__ void k_pack_scene(uint64_t n, int D, const float* mean, const float* 
 // K3 scan: exclusive scan of the per-chunk tile-count sums -> chunk offsets,
 // total P, capacity check (single block).
 __global__ void k_scan_chunks(const uint32_t* chunk_sum, uint32_t* chunk_off, Counters* ctr, uint64_t capacity);
-// K3 emit: one CTA per 256-splat chunk of the depth order.
-__global__ void k_emit(FrameParams p, const uint32_t* order, const uint32_t* counts_sorted,
-                       const uint32_t* chunk_off, SplatPlanes pl, uint32_t* tkeys, uint32_t* pvals,
-                       uint64_t capacity, const Counters* ctr);
+// K3 emit: one CTA per 256-splat chunk of the depth order; up to STAGE pairs
+// of a chunk are staged in (dynamic) shared memory and written as one
+// contiguous run (the big stage for frames with many pairs per splat).
+constexpr int kEmitStageSmall = 3072, kEmitStageBig = 8192;
+constexpr size_t emit_smem(bool big) { return 2 * (big ? kEmitStageBig : kEmitStageSmall) * sizeof(uint32_t); }
+cudaError_t launch_emit(bool big, int grid, cudaStream_t st, const FrameParams& p, const uint32_t* order,
+                        const uint32_t* counts_sorted, const uint32_t* chunk_off, const SplatPlanes& pl,
+                        uint32_t* tkeys, uint32_t* pvals, uint64_t capacity, const Counters* ctr);
+cudaError_t emit_configure(bool big, int* occupancy);
 __global__ void k_splats_to_planes(FrameParams p, const agsx_splat_view* splats, uint64_t n,
                                    SplatPlanes pl, uint32_t* counts, uint32_t* depth_bits);
 __global__ void k_emit_list(FrameParams p, uint64_t n, SplatPlanes pl, const uint32_t* counts,

@@ -62,7 +62,10 @@ agsx_config make_config(const std::string& mode, double k, int threads, int tile
                         std::size_t pair_budget) {
     ags::RenderConfig def;
     ags::Mode m;
-    if (!ags::parse_mode(mode, m)) throw py::value_error("unknown mode '" + mode + "'");
+    // "aabb_fixed3": the original 3D-GS tile test (AABB at a fixed 3 sigma,
+    // RenderConfig::fixed_radius_aabb, pair_gen.cpp:11-16) -- the config 2 baseline
+    const bool fixed3 = mode == "aabb_fixed3";
+    if (!ags::parse_mode(fixed3 ? std::string("aabb") : mode, m)) throw py::value_error("unknown mode '" + mode + "'");
     agsx_config c{};
     c.tile_size = tile_size;
     c.alpha_threshold = def.alpha_threshold;
@@ -73,7 +76,7 @@ agsx_config make_config(const std::string& mode, double k, int threads, int tile
     c.mode = static_cast<int>(m);
     c.k = static_cast<float>(k);
     c.thread_count = threads;
-    c.fixed_radius_aabb = 0;
+    c.fixed_radius_aabb = fixed3 ? 1 : 0;
     c.pair_budget = pair_budget;
     c.flags = exact ? AGSX_FLAG_EXACT_ALPHA : 0u;
     return c;
