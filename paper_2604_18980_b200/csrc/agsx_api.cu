@@ -102,6 +102,11 @@ struct agsx_ctx {
     bool f_maxt = false;
     float* f_image = nullptr;     // raster target of the frame (device image or mapped host buffer)
     bool f_image_on_host = false;  // the frame streamed its image into a mapped host buffer
+    float* f_band_host = nullptr;  // page-locked host image filled by banded copies behind the raster
+    cudaStream_t copy_stream = nullptr;
+    static constexpr int kBands = 8;
+    cudaEvent_t band_ev[kBands] = {};
+    cudaEvent_t copy_done = nullptr;
     uint32_t* f_tkeys = nullptr;
     uint32_t* f_pvals = nullptr;
     int f_tile_count = 0;
@@ -263,7 +268,7 @@ bool raster_uses_units(const FrameParams& p, bool maxt) {
 
 void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
                    const float4* P0, const float4* P1, const float4* P2, float* image,
-                   uint32_t* maxt, Counters* ctr) {
+                   uint32_t* maxt, Counters* ctr, uint32_t* unit_ctr = nullptr) {
     const int grid = p.tiles_x * p.tiles_y;
     if (grid == 0) return;
     const bool exact = (p.flags & AGSX_FLAG_EXACT_ALPHA) != 0;
@@ -271,7 +276,8 @@ void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, con
         // default path: warp-persistent units (half tiles); per-tile P_it
         // words (zeroed at the frame start by the caller)
         launch_raster_units(ctx->num_sms * ctx->occ_raster, ctx->stream, p, ranges, vals, P0, P1, P2, image,
-                            &ctr->tile_ctr[3], ptr<unsigned long long>(ctx->tile_pit), &ctr->p_it, ctr->dbg);
+                            unit_ctr ? unit_ctr : &ctr->tile_ctr[3], ptr<unsigned long long>(ctx->tile_pit),
+                            &ctr->p_it, ctr->dbg);
         check_launch(ctx);
         return;
     }
@@ -464,9 +470,37 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
     // K6
-    launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ctx->f_image,
-                  maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
-    AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
+    if (ctx->f_band_host && raster_uses_units(p, maxt) && p.tiles_y > 0) {
+        // banded egress: the raster runs in bands of whole tile rows; band b's
+        // rows are copied to the page-locked host image on the copy stream while
+        // band b+1 renders (the copy engine is the faster PCIe writer)
+        const int B = std::min(agsx_ctx::kBands, p.tiles_y);
+        const int rows_per = (p.tiles_y + B - 1) / B;
+        for (int b = 0; b < B; ++b) {
+            const int r0 = b * rows_per, r1 = std::min(p.tiles_y, r0 + rows_per);
+            if (r0 >= r1) break;
+            FrameParams pb = p;
+            pb.unit_lo = 2u * static_cast<uint32_t>(r0 * p.tiles_x);
+            pb.unit_hi = 2u * static_cast<uint32_t>(r1 * p.tiles_x);
+            launch_raster(ctx, pb, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ctx->f_image, nullptr, ctr,
+                          &ctr->tile_ctr[8 + b]);
+            AGSX_CUDA(cudaEventRecord(ctx->band_ev[b], st));
+            AGSX_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_ev[b], 0));
+            const size_t y0 = static_cast<size_t>(r0) * p.tile_size;
+            const size_t y1 = std::min(static_cast<size_t>(r1) * p.tile_size, static_cast<size_t>(p.H));
+            const size_t row_bytes = static_cast<size_t>(p.W) * 12;
+            AGSX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->f_band_host) + y0 * row_bytes,
+                                      reinterpret_cast<char*>(ctx->f_image) + y0 * row_bytes, (y1 - y0) * row_bytes,
+                                      cudaMemcpyDeviceToHost, ctx->copy_stream));
+        }
+        AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
+        AGSX_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+        AGSX_CUDA(cudaStreamWaitEvent(st, ctx->copy_done, 0));
+    } else {
+        launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ctx->f_image,
+                      maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
+        AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
+    }
     AGSX_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
     ctx->f_tkeys = tk[cur];
     ctx->f_pvals = pv[cur];
@@ -503,12 +537,23 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     // anything else gets the device image and a copy.
     ctx->f_image = device_target ? device_target : ptr<float>(ctx->image);
     ctx->f_image_on_host = device_target != nullptr;  // the ctx image is not this frame's
+    ctx->f_band_host = nullptr;
     if (host_image && !device_target) {
+        // A page-locked host destination: the default rasterizer fills it by
+        // banded copy-engine transfers behind the raster (57 GB/s); other
+        // rasterizers (exact / max_t / tile sizes) write it directly through
+        // the mapping (SM stores, 52 GB/s).  Pageable memory: one copy after.
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, host_image) == cudaSuccess && at.type == cudaMemoryTypeHost &&
-            at.devicePointer != nullptr && std::getenv("AGSX_NO_ZERO_COPY") == nullptr) {
-            ctx->f_image = static_cast<float*>(at.devicePointer);
-            ctx->f_image_on_host = true;
+            at.devicePointer != nullptr) {
+            const char* eg = std::getenv("AGSX_EGRESS");
+            if (raster_uses_units(p, maxt) && !(eg && std::strcmp(eg, "zerocopy") == 0)) {
+                ctx->f_band_host = host_image;
+                ctx->f_image_on_host = true;  // the frame's image ends up in the host buffer
+            } else if (!(eg && std::strcmp(eg, "copy") == 0)) {
+                ctx->f_image = static_cast<float*>(at.devicePointer);
+                ctx->f_image_on_host = true;
+            }
         }
         cudaGetLastError();  // clear a pageable-pointer query error
     }
@@ -580,6 +625,9 @@ int agsx_create(int device, agsx_ctx** out) {
     ctx->device = device;
     const int rc = guarded(ctx, [&]() -> int {
         AGSX_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        AGSX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        for (auto& e : ctx->band_ev) AGSX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        AGSX_CUDA(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
         AGSX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
         AGSX_CUDA(sort_configure<uint32_t>(sort_smem(false), &ctx->occ_sort32));
         AGSX_CUDA(sort_configure<uint64_t>(sort_smem(true), &ctx->occ_sort64));
@@ -620,6 +668,10 @@ void agsx_destroy(agsx_ctx* ctx) {
         for (auto& e : set)
             if (e) cudaEventDestroy(e);
     if (ctx->h_ctr) cudaFreeHost(ctx->h_ctr);
+    for (auto& e : ctx->band_ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -34,6 +34,7 @@ struct FrameParams {
     float bg[3];
     uint32_t flags;
     int raster_ppt;  // pixels per thread of the 16x16 rasterizer (2 or 4)
+    uint32_t unit_lo, unit_hi;  // raster work-unit range of this launch (unit_hi = 0: all units)
     // T_upper LUT (lut.hpp:11-26)
     int adaptive;
     float lut_dmin, lut_dmax;

@@ -379,14 +379,14 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
     if (tid < 32) sTab[tid] = kExp2fTab[tid];
     __syncthreads();
 
-    const uint32_t units = 2u * static_cast<uint32_t>(p.tiles_x * p.tiles_y);
+    const uint32_t units = p.unit_hi ? p.unit_hi : 2u * static_cast<uint32_t>(p.tiles_x * p.tiles_y);
     const float tau = p.tau, tfloor = p.tfloor, aclamp = p.aclamp;
     const float c_ex2 = -0.5f * 1.4426950408889634f;
     const int lx = lane & 15, g = lane >> 4;
 
     while (true) {
         uint32_t unit = 0;
-        if (lane == 0) unit = atomicAdd(unit_ctr, 1u);
+        if (lane == 0) unit = p.unit_lo + atomicAdd(unit_ctr, 1u);
         unit = __shfl_sync(0xffffffffu, unit, 0);
         if (unit >= units) break;
         const int tile = static_cast<int>(unit >> 1), half = static_cast<int>(unit & 1u);
