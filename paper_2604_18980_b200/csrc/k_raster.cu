@@ -369,9 +369,8 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
     unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0, st_lo32 = 0, st_lo64 = 0, st_empty = 0;
     constexpr int PPT = 4;
     constexpr int NWB = 8;  // warps per block
-    __shared__ __align__(16) float4 sA[NWB][32];
-    __shared__ __align__(16) float4 sB[NWB][32];
-    __shared__ __align__(16) float4 sC[NWB][32];
+    // staged splat j of warp w: sS[w][j][0..2] = P0, P1, {rgb, log2 opacity}
+    __shared__ __align__(16) float4 sS[NWB][32][3];
     __shared__ uint64_t sTab[32];
     __shared__ __align__(16) float sOut[NWB][8 * 16 * 3];
 
@@ -426,20 +425,20 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             if (RECT && rel) rel = !rect_outside(cA, cB.x, cB.z, cx0, cx1, cy0, cy1);
             uint32_t m = __ballot_sync(0xffffffffu, rel);
             if (!m) continue;
-            sA[warp][lane] = cA;
-            sB[warp][lane] = cB;
-            sC[warp][lane] = cC;
+            sS[warp][lane][0] = cA;
+            sS[warp][lane][1] = cB;
+            sS[warp][lane][2] = make_float4(cC.x, cC.y, cC.z, fast_log2(cB.y));  // extent no longer needed
             __syncwarp();
             while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
-                const float4 sa = sA[warp][j];  // mx, my, inv.xx, 2*inv.xy
-                const float4 sb = sB[warp][j];  // inv.yy, opacity, qcut, qsafe
-                const float4 sc = sC[warp][j];  // r, g, b, extent
+                const float4 sa = sS[warp][j][0];  // mx, my, inv.xx, 2*inv.xy
+                const float4 sb = sS[warp][j][1];  // inv.yy, opacity, qcut, qsafe
+                const float4 sc = sS[warp][j][2];  // r, g, b, log2 opacity
                 const float dx = px - sa.x;
                 const float t1 = sa.z * dx * dx;
                 const float t2 = sa.w * dx;
-                const float l2op = fast_log2(sb.y);
+                const float l2op = sc.w;
                 const float qcut = sb.z, qsafe = sb.w;
                 if (STATS) {
                     ++st_it;
