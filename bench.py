@@ -394,6 +394,28 @@ def run_ours(args, rank, world, local_rank):
                             "api": "render(..., image_u8=True) -> host uint8 PPM pixels (write_image quantisation "
                                    "on the GPU)"}
 
+        # a camera path through batch.render_views: one frame in flight per
+        # context (two contexts), so each frame's PCIe egress overlaps the
+        # next frame's kernels; per frame the same H2D / D2H as above
+        from paper_2604_18980_b200.batch import render_views
+
+        prs = [P.Renderer(local_rank), P.Renderer(local_rank)]
+        kw = dict(mode=mode, k=k, lut_bins=bins, exact=args.exact)
+        render_views(prs, scene, [view] * 4, on_frame=lambda i, o: None, **kw)
+        barrier()
+        n_path = max(6, 2 * steps_e2e)
+        t0 = time.perf_counter()
+        render_views(prs, scene, [view] * n_path, on_frame=lambda i, o: None, **kw)
+        barrier()
+        tp = torch.tensor([(time.perf_counter() - t0) / n_path], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
+        e2e["camera_path"] = {"value": world / float(tp.item()), "unit": "frames/s", "frames": n_path,
+                              "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(out["image"].nbytes) + 128,
+                              "api": "batch.render_views(renderers, scene, views) -> host float32 image per view "
+                                     "(two contexts, one frame in flight each)"}
+        del prs
+
     # ---- AdaGScale off, same scene (pairs + FPS) --------------------------
     off = None
     if mode == "adagscale" and not args.no_off:

@@ -167,6 +167,16 @@ int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out);
  * `target` must stay valid until agsx_render_wait returns. */
 int agsx_render_async_to(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
                          const agsx_config* cfg, const agsx_lut* lut, float* target);
+/* As agsx_render_async, with the image delivered to host memory `image`
+ * (H*W*3 f32, HWC) by the time agsx_render_wait returns: the egress of
+ * agsx_render (page-locked memory is filled by banded copies behind the
+ * raster; pageable memory gets one copy in agsx_render_wait).  Frames of two
+ * contexts on one device overlap one frame's PCIe egress with the next
+ * frame's kernels (paper_2604_18980_b200.batch.render_views).  Replaces a
+ * loop of ags::render() calls over a camera path (adagscale_main.cpp:224-226).
+ * `image` must stay valid until agsx_render_wait returns. */
+int agsx_render_async_host(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                           const agsx_config* cfg, const agsx_lut* lut, float* image);
 
 /* Device-timed stage durations (ms: preprocess, pair_gen, sort, raster) of
  * the last min(max_frames, 64) frames enqueued on this ctx, oldest first;

@@ -55,3 +55,46 @@ def pair_report(local_report: LocalReport, n_views: int, group=None) -> list:
     parts = [None] * world
     dist.all_gather_object(parts, mine, group=group)
     return merge_rows(parts)
+
+
+def render_views(renderers, scene, views: Sequence[int], on_frame=None, **kw) -> list:
+    """Render `views` of `scene` to host images, one frame in flight per renderer.
+
+    This is the camera-path loop of the reference CLI (``ags::render`` per view,
+    adagscale_main.cpp:224-226), pipelined. Each frame is rasterised into a
+    page-locked host image by banded copies behind the raster
+    (``Renderer.render_async_host``). Consecutive views alternate between the
+    renderers (contexts with their own stream and buffers on one device). So one
+    frame's PCIe egress overlaps the next frame's preprocess, sort and raster.
+
+    ``kw`` takes the keyword arguments of ``Renderer.render_async_host``
+    (mode, k, lut_bins, ...). Returns one dict per view in path order, as
+    ``render()`` returns them: image, pair_count, splat_count, stage_ms.
+    ``on_frame(i, out)``, if given, is called as each frame completes, in path
+    order; it replaces keeping the result, which bounds host memory on long paths.
+    """
+    if not renderers:
+        raise ValueError("need at least one renderer")
+    out = [None] * len(views)
+    pending = {}  # renderer index -> position of its frame in flight
+    nxt = 0  # next position to hand to on_frame
+
+    def done(ri):
+        nonlocal nxt
+        i = pending.pop(ri)
+        out[i] = renderers[ri].wait()
+        while nxt < len(out) and out[nxt] is not None:
+            if on_frame is not None:
+                on_frame(nxt, out[nxt])
+                out[nxt] = True  # delivered
+            nxt += 1
+
+    for i, v in enumerate(views):
+        ri = i % len(renderers)
+        if ri in pending:
+            done(ri)
+        renderers[ri].render_async_host(scene, v, **kw)
+        pending[ri] = i
+    for ri in sorted(pending, key=pending.get):
+        done(ri)
+    return out if on_frame is None else []

@@ -18,6 +18,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -85,6 +87,7 @@ struct agsx_ctx {
     uint64_t pair_capacity = 0;
 
     Counters* h_ctr = nullptr;  // pinned
+    uint32_t* h_ctr_dev = nullptr;  // its device-mapped alias
     static constexpr int kRing = 64;  // frames of stage events kept for timing
     cudaEvent_t ev_ring[kRing][6] = {};
     cudaEvent_t* ev = ev_ring[0];
@@ -102,6 +105,7 @@ struct agsx_ctx {
     bool f_maxt = false;
     float* f_image = nullptr;     // raster target of the frame (device image or mapped host buffer)
     bool f_image_on_host = false;  // the frame streamed its image into a mapped host buffer
+    float* f_host_dst = nullptr;   // agsx_render_async_host destination (copied in wait if pageable)
     float* f_band_host = nullptr;  // page-locked host image filled by banded copies behind the raster
     cudaStream_t copy_stream = nullptr;
     static constexpr int kBands = 8;
@@ -394,6 +398,10 @@ int prepare(agsx_ctx* ctx, const agsx_camera* cam, const agsx_config* cfg, const
 }
 
 // Enqueue the whole frame (no host synchronisation).
+__global__ void k_counters_out(const uint32_t* __restrict__ src, uint32_t* dst, int words) {
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+
 void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bool maxt,
                    agsx_splat_view* dump) {
     const uint64_t n = sc->n;
@@ -501,7 +509,13 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
                       maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
         AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
     }
-    AGSX_CUDA(cudaMemcpyAsync(ctx->h_ctr, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    // Counters to the host by SM stores into the mapped page-locked word block,
+    // not by a copy-engine transfer: with frames of several contexts in flight
+    // a small D2H copy would queue in the copy engine behind another frame's
+    // 191 MB of image bands, and this frame would finish only after that one.
+    k_counters_out<<<1, 64, 0, st>>>(reinterpret_cast<const uint32_t*>(ctr), ctx->h_ctr_dev,
+                                     static_cast<int>(sizeof(Counters) / 4));
+    check_launch(ctx);
     ctx->f_tkeys = tk[cur];
     ctx->f_pvals = pv[cur];
     ctx->f_tile_count = static_cast<int>(tiles);
@@ -538,6 +552,7 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     ctx->f_image = device_target ? device_target : ptr<float>(ctx->image);
     ctx->f_image_on_host = device_target != nullptr;  // the ctx image is not this frame's
     ctx->f_band_host = nullptr;
+    ctx->f_host_dst = nullptr;
     if (host_image && !device_target) {
         // A page-locked host destination: the default rasterizer fills it by
         // banded copy-engine transfers behind the raster (57 GB/s); other
@@ -617,6 +632,33 @@ void agsx_host_free(void* p) {
     if (p) cudaFreeHost(p);
 }
 
+}  // extern "C"
+
+namespace {
+// One frame-egress copy stream per device, shared by every context on it:
+// frames of several contexts then leave over PCIe in the order they were
+// enqueued (FIFO), so a pipelined camera path keeps the copy engine busy with
+// one whole frame after another instead of interleaving two frames' bands
+// (which finishes both late and leaves a gap before the next pair).
+cudaError_t shared_copy_stream(int device, cudaStream_t* out) {
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> streams;  // process lifetime
+    std::lock_guard<std::mutex> g(mu);
+    auto it = streams.find(device);
+    if (it != streams.end()) {
+        *out = it->second;
+        return cudaSuccess;
+    }
+    cudaStream_t st = nullptr;
+    const cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) streams[device] = st;
+    *out = st;
+    return e;
+}
+}  // namespace
+
+extern "C" {
+
 int agsx_create(int device, agsx_ctx** out) {
     if (!out) return AGSX_EINVAL;
     *out = nullptr;
@@ -625,7 +667,7 @@ int agsx_create(int device, agsx_ctx** out) {
     ctx->device = device;
     const int rc = guarded(ctx, [&]() -> int {
         AGSX_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-        AGSX_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+        AGSX_CUDA(shared_copy_stream(device, &ctx->copy_stream));
         for (auto& e : ctx->band_ev) AGSX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         AGSX_CUDA(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
         AGSX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -643,6 +685,7 @@ int agsx_create(int device, agsx_ctx** out) {
             for (auto& e : set) AGSX_CUDA(cudaEventCreate(&e));
         AGSX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ctr), sizeof(Counters)));
         std::memset(ctx->h_ctr, 0, sizeof(Counters));
+        AGSX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_ctr_dev), ctx->h_ctr, 0));
         return AGSX_OK;
     });
     if (rc != AGSX_OK) {
@@ -671,7 +714,7 @@ void agsx_destroy(agsx_ctx* ctx) {
     for (auto& e : ctx->band_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
-    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);  // shared per device: not destroyed
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -793,9 +836,29 @@ int agsx_render_async_to(agsx_ctx* ctx, const agsx_scene* scene, const agsx_came
     return guarded(ctx, [&]() -> int { return start_frame(ctx, scene, cam, cfg, lut, false, nullptr, target); });
 }
 
+int agsx_render_async_host(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                           const agsx_config* cfg, const agsx_lut* lut, float* image) {
+    if (!ctx) return AGSX_EINVAL;
+    if (!image) return fail(ctx, AGSX_EINVAL, "render_async_host: null image");
+    return guarded(ctx, [&]() -> int {
+        const int rc = start_frame(ctx, scene, cam, cfg, lut, false, image);
+        if (rc == AGSX_OK) ctx->f_host_dst = image;
+        return rc;
+    });
+}
+
 int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out) {
     if (!ctx) return AGSX_EINVAL;
-    return guarded(ctx, [&]() -> int { return finish_frame(ctx, out); });
+    return guarded(ctx, [&]() -> int {
+        float* dst = ctx->f_host_dst;
+        ctx->f_host_dst = nullptr;
+        const int rc = finish_frame(ctx, out);
+        if (rc || !dst || ctx->f_image_on_host) return rc;
+        AGSX_CUDA(cudaMemcpyAsync(dst, ctx->image.p, static_cast<size_t>(ctx->f_cam.width) * ctx->f_cam.height * 12,
+                                  cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return AGSX_OK;
+    });
 }
 
 int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,

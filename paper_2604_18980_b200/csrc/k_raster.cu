@@ -383,11 +383,33 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
     const float c_ex2 = -0.5f * 1.4426950408889634f;
     const int lx = lane & 15, g = lane >> 4;
 
-    while (true) {
-        uint32_t unit = 0;
-        if (lane == 0) unit = p.unit_lo + atomicAdd(unit_ctr, 1u);
-        unit = __shfl_sync(0xffffffffu, unit, 0);
-        if (unit >= units) break;
+    // Units are software-pipelined: while unit U renders, the ranges of U+1
+    // are in flight and the atomic for U+2 is issued; U+1's first batch of
+    // records is fetched before U's image stores.  So a unit starts on
+    // loaded data instead of a counter -> ranges -> vals -> planes chain.
+    uint32_t unit = 0, nunit = 0, my_nn = 0;
+    if (lane == 0) {
+        unit = p.unit_lo + atomicAdd(unit_ctr, 1u);
+        nunit = p.unit_lo + atomicAdd(unit_ctr, 1u);
+    }
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    nunit = __shfl_sync(0xffffffffu, nunit, 0);
+    uint2 rg = unit < units ? ranges[unit >> 1] : make_uint2(0u, 0u);
+    float4 nA = make_float4(0, 0, 0, 0), nB = nA, nC = nA;
+    auto fetch = [&](uint32_t base, uint32_t lim) {
+        const uint32_t i = base + lane;
+        if (i < lim) {
+            const uint32_t gid = __ldg(&vals[i]);
+            nA = __ldg(&P0[gid]);
+            nB = __ldg(&P1[gid]);
+            nC = __ldg(&P2[gid]);
+        }
+    };
+    bool pre = false;  // nA/nB/nC hold the first batch of `unit`
+
+    while (unit < units) {
+        if (lane == 0) my_nn = p.unit_lo + atomicAdd(unit_ctr, 1u);
+        const uint2 nrg = nunit < units ? ranges[nunit >> 1] : make_uint2(0u, 0u);
         const int tile = static_cast<int>(unit >> 1), half = static_cast<int>(unit & 1u);
         const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
         const int x0 = tx * 16, y0 = ty * 16 + half * 8;
@@ -403,43 +425,37 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
         const float cx0 = x0 + 0.5f, cx1 = x0 + w - 0.5f;
         const float cy0 = y0 + 0.5f, cy1 = y0 + h - 0.5f;
 
-        const uint2 rg = ranges[tile];
         const uint32_t start = rg.x, end = rg.y > rg.x ? rg.y : rg.x;
         uint32_t death = 0;
         bool all_done = h <= 0;
-        float4 nA = make_float4(0, 0, 0, 0), nB = nA, nC = nA;
-        auto fetch = [&](uint32_t base) {
-            const uint32_t i = base + lane;
-            if (i < end) {
-                const uint32_t gid = __ldg(&vals[i]);
-                nA = __ldg(&P0[gid]);
-                nB = __ldg(&P1[gid]);
-                nC = __ldg(&P2[gid]);
-            }
-        };
-        if (!all_done && start < end) fetch(start);
+        if (!pre && !all_done && start < end) fetch(start, end);
         for (uint32_t base = start; base < end && !all_done; base += 32) {
             const float4 cA = nA, cB = nB, cC = nC;
-            if (base + 32 < end) fetch(base + 32);
+            if (base + 32 < end) fetch(base + 32, end);
             bool rel = base + lane < end && meets_box(cA.x, cA.y, unpack_extent(cC.w), cx0, cx1, cy0, cy1);
             if (RECT && rel) rel = !rect_outside(cA, cB.x, cB.z, cx0, cx1, cy0, cy1);
             uint32_t m = __ballot_sync(0xffffffffu, rel);
             if (!m) continue;
             sS[warp][lane][0] = cA;
-            sS[warp][lane][1] = cB;
+            // {iyy, opacity, band width w = qcut - qsafe, qsafe}: a pixel is in
+            // the margin band only if 0 <= q - qsafe <= w (rounding is
+            // monotone, so fl(q - qsafe) <= fl(qcut - qsafe) whenever
+            // q <= qcut; +inf/-inf thresholds give w = +inf)
+            sS[warp][lane][1] = make_float4(cB.x, cB.y, cB.z - cB.w, cB.w);
             sS[warp][lane][2] = make_float4(cC.x, cC.y, cC.z, fast_log2(cB.y));  // extent no longer needed
             __syncwarp();
             while (m) {
                 const int j = __ffs(m) - 1;
                 m &= m - 1;
                 const float4 sa = sS[warp][j][0];  // mx, my, inv.xx, 2*inv.xy
-                const float4 sb = sS[warp][j][1];  // inv.yy, opacity, qcut, qsafe
+                const float4 sb = sS[warp][j][1];  // inv.yy, opacity, qcut - qsafe, qsafe
                 const float4 sc = sS[warp][j][2];  // r, g, b, log2 opacity
                 const float dx = px - sa.x;
                 const float t1 = sa.z * dx * dx;
                 const float t2 = sa.w * dx;
                 const float l2op = sc.w;
-                const float qcut = sb.z, qsafe = sb.w;
+                const float qsafe = sb.w;
+                const uint32_t wbits = __float_as_uint(sb.z);
                 if (STATS) {
                     ++st_it;
                     uint32_t mine = 0;
@@ -454,28 +470,32 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 // remaining blend weights sum to less than T <= floor = 1e-4,
                 // which bounds the image difference to the reference by
                 // 1e-4 per channel; the warp stops when all are saturated.
-                bool need_any = false;
-                bool need[PPT];
-                float e[PPT];
+                // band test as unsigned compares of float bits: q - qsafe < 0
+                // (a fast pixel) has the sign bit set and exceeds any w >= 0.
+                // It admits a superset of the band (pixels just above qcut);
+                // the exact path rejects those by its own alpha >= tau test.
+                uint32_t dmin = 0xffffffffu;
+                float e[PPT], qv[PPT];
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
                     const float dy = py[k] - sa.y;
                     const float q = __fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1);
+                    qv[k] = q;
                     const bool fast = q < qsafe;
                     e[k] = fast ? fast_exp2(__fmaf_rn(q, c_ex2, l2op)) : 0.0f;
-                    need[k] = !fast && !(q > qcut);
-                    need_any = need_any || need[k];
+                    dmin = umin(dmin, __float_as_uint(q - qsafe));
                     if (STATS) {
                         st_fast += fast && T[k] >= tfloor;
-                        st_need += need[k];
+                        st_need += __float_as_uint(q - qsafe) <= wbits;
                     }
                 }
+                const bool need_any = dmin <= wbits;
                 if (STATS) {  // iterations in which no pixel of the unit is within q <= qcut
                     bool any_in = false;
 #pragma unroll
                     for (int k = 0; k < PPT; ++k) {
                         const float dy = py[k] - sa.y;
-                        any_in = any_in || !(__fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1) > qcut);
+                        any_in = any_in || !(__fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1) > qsafe + sb.z);
                     }
                     st_empty += !__any_sync(0xffffffffu, any_in);
                 }
@@ -494,7 +514,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 if (__any_sync(0xffffffffu, need_any)) {  // margin band: the reference's alpha_at
 #pragma unroll
                     for (int k = 0; k < PPT; ++k) {
-                        if (!need[k]) continue;
+                        if (!(__float_as_uint(qv[k] - qsafe) <= wbits)) continue;
                         const float dy = py[k] - sa.y;
                         const float qr = (t1 + t2 * dy) + sb.x * dy * dy;  // reference order
                         const float a = exact_alpha(qr, sb.y, aclamp, sTab);
@@ -517,13 +537,17 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             __syncwarp();
         }
 
+        // the next unit's first batch, in flight during this unit's stores
+        pre = nunit < units && nrg.y > nrg.x;
+        if (pre) fetch(nrg.x, nrg.y);
+
         // P_it (rasterizer.cpp:55-56): per unit n if any pixel stays
         // unsaturated, else the 1-based index of the saturating pair; per
         // tile the max over both units.  Word = (units done << 32) | max.
         if (lane == 0 && pit) {
             const uint32_t mine = h <= 0 ? 0u : (all_done ? death : end - start);
             unsigned long long* wp = &tile_pit[tile];
-            unsigned long long old = *wp;
+            unsigned long long old = 0ull;  // guess "first unit of the tile": one CAS round trip when right
             while (true) {
                 const uint32_t mx = static_cast<uint32_t>(old) > mine ? static_cast<uint32_t>(old) : mine;
                 const unsigned long long r = atomicCAS(wp, old, (((old >> 32) + 1ull) << 32) | mx);
@@ -561,6 +585,9 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             }
             __syncwarp();
         }
+        unit = nunit;
+        rg = nrg;
+        nunit = __shfl_sync(0xffffffffu, my_nn, 0);
     }
     if (STATS) {
         for (int o = 16; o > 0; o >>= 1) {

@@ -299,6 +299,28 @@ public:
         if (rc != AGSX_OK) raise_status(rc, ctx_);
     }
 
+    // Frame delivered to a page-locked host image (banded copies behind the
+    // raster); wait() returns it as out["image"].  Two renderers on one
+    // device alternate frames so one frame's PCIe egress overlaps the next
+    // frame's kernels (batch.render_views).
+    void render_async_host(Scene& scene, int view, const std::string& mode, double k,
+                           const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size, bool exact,
+                           std::size_t pair_budget, py::object camera) {
+        const agsx_camera cam = camera.is_none() ? view_of(scene, view) : camera_from(camera.cast<py::dict>());
+        const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
+        const LutHolder lut(lut_bins, dmin, dmax);
+        agsx_scene* dev = device_scene(scene);
+        py::array_t<float> img = pinned_image<float>(cam.height, cam.width);
+        int rc;
+        {
+            py::gil_scoped_release nogil;
+            rc = agsx_render_async_host(ctx_, dev, &cam, &cfg, cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr,
+                                        img.mutable_data());
+        }
+        if (rc != AGSX_OK) raise_status(rc, ctx_);
+        pending_image_ = img;
+    }
+
     py::dict wait() {
         agsx_frame f{};
         int rc;
@@ -306,8 +328,11 @@ public:
             py::gil_scoped_release nogil;
             rc = agsx_render_wait(ctx_, &f);
         }
+        py::object img = pending_image_;
+        pending_image_ = py::none();
         if (rc != AGSX_OK) raise_status(rc, ctx_);
         py::dict out;
+        if (!img.is_none()) out["image"] = img;
         out["pair_count"] = f.pair_count;
         out["splat_count"] = f.splat_count;
         out["stage_ms"] = std::vector<float>(f.stage_ms, f.stage_ms + 4);
@@ -465,6 +490,7 @@ public:
 
 private:
     int device_;
+    py::object pending_image_ = py::none();  // host image of the frame in flight (render_async_host)
     agsx_ctx* ctx_ = nullptr;
     std::mutex mu_;
 };
@@ -749,6 +775,10 @@ PYBIND11_MODULE(_core, m) {
              py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("tile_size") = 16,
              py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27,
              py::arg("camera") = py::none())
+        .def("render_async_host", &Renderer::render_async_host, py::arg("scene"), py::arg("view") = 0,
+             py::arg("mode") = "ellipse", py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{},
+             py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("tile_size") = 16,
+             py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27, py::arg("camera") = py::none())
         .def("wait", &Renderer::wait)
         .def("pair_report", &Renderer::pair_report, py::arg("scene"), py::arg("specs"),
              py::arg("views") = std::vector<int>{}, py::arg("lut_bins") = std::vector<float>{},
