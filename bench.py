@@ -414,6 +414,17 @@ def run_ours(args, rank, world, local_rank):
                               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(out["image"].nbytes) + 128,
                               "api": "batch.render_views(renderers, scene, views) -> host float32 image per view "
                                      "(two contexts, one frame in flight each)"}
+        render_views(prs, scene, [view] * 4, on_frame=lambda i, o: None, image_u8=True, **kw)
+        barrier()
+        t0 = time.perf_counter()
+        render_views(prs, scene, [view] * n_path, on_frame=lambda i, o: None, image_u8=True, **kw)
+        barrier()
+        tp8 = torch.tensor([(time.perf_counter() - t0) / n_path], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tp8, op=dist.ReduceOp.MAX)
+        e2e["camera_path"]["u8_egress"] = {"value": world / float(tp8.item()), "unit": "frames/s",
+                                           "d2h_bytes_per_step": int(out8["image"].nbytes) + 128,
+                                           "api": "batch.render_views(..., image_u8=True)"}
         del prs
 
     # ---- AdaGScale off, same scene (pairs + FPS) --------------------------

@@ -177,6 +177,11 @@ int agsx_render_async_to(agsx_ctx* ctx, const agsx_scene* scene, const agsx_came
  * `image` must stay valid until agsx_render_wait returns. */
 int agsx_render_async_host(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
                            const agsx_config* cfg, const agsx_lut* lut, float* image);
+/* As agsx_render_async_host for the write_image bytes (agsx_render_u8): the
+ * frame is quantised band by band on the device and only the H*W*3 bytes
+ * cross PCIe, behind the raster when `image_u8` is page-locked. */
+int agsx_render_async_host_u8(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                              const agsx_config* cfg, const agsx_lut* lut, uint8_t* image_u8);
 
 /* Device-timed stage durations (ms: preprocess, pair_gen, sort, raster) of
  * the last min(max_frames, 64) frames enqueued on this ctx, oldest first;

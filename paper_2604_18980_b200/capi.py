@@ -23,7 +23,7 @@ FLAG_EXACT_ALPHA = 1
 EXPORTS = (
     "agsx_abi_version", "agsx_create", "agsx_destroy", "agsx_last_error", "agsx_stream",
     "agsx_scene_upload", "agsx_scene_free", "agsx_scene_count", "agsx_render",
-    "agsx_render_async", "agsx_render_async_to", "agsx_render_async_host", "agsx_render_wait", "agsx_device_image", "agsx_dump_tile_counts",
+    "agsx_render_async", "agsx_render_async_to", "agsx_render_async_host", "agsx_render_async_host_u8", "agsx_render_wait", "agsx_device_image", "agsx_dump_tile_counts",
     "agsx_dump_sorted_pairs", "agsx_dump_ranges", "agsx_preprocess_view",
     "agsx_generate_pairs", "agsx_sort_pairs", "agsx_raster", "agsx_device_logf",
     "agsx_device_expf", "agsx_kernel_launches", "agsx_stage_history",
@@ -184,6 +184,7 @@ class Lib:
         L.agsx_render_async.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut)]
         L.agsx_render_async_to.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp]
         L.agsx_render_async_host.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp]
+        L.agsx_render_async_host_u8.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp]
         L.agsx_render_u8.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp,
                                      C.POINTER(Frame)]
         L.agsx_render_wait.argtypes = [vp, C.POINTER(Frame)]

@@ -80,7 +80,7 @@ struct agsx_ctx {
     Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
     // device arenas (grow-only)
-    Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2, dcounts, chunks;
+    Buf status, p0, p1, p2, p3, p4, dkeys, dvals, dkeys2, dvals2, dcounts, chunks, img_u8;
     Buf tkeys, pvals, tkeys2, pvals2;
     Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext, tile_pit, calib;
     Buf tmp0, tmp1, tmp2, tmp3, tmp4;
@@ -106,6 +106,8 @@ struct agsx_ctx {
     float* f_image = nullptr;     // raster target of the frame (device image or mapped host buffer)
     bool f_image_on_host = false;  // the frame streamed its image into a mapped host buffer
     float* f_host_dst = nullptr;   // agsx_render_async_host destination (copied in wait if pageable)
+    uint8_t* f_band_host_u8 = nullptr;  // page-locked host PPM pixels filled by banded copies (f3 egress)
+    uint8_t* f_host_dst_u8 = nullptr;   // agsx_render_async_host_u8 destination (quantised in wait if pageable)
     float* f_band_host = nullptr;  // page-locked host image filled by banded copies behind the raster
     cudaStream_t copy_stream = nullptr;
     static constexpr int kBands = 8;
@@ -402,6 +404,20 @@ __global__ void k_counters_out(const uint32_t* __restrict__ src, uint32_t* dst, 
     for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
 }
 
+// write_image quantisation of n floats (src, dst 16-byte aligned) on stream st
+void launch_quantize(agsx_ctx* ctx, const float* src, uint8_t* dst, uint64_t n, cudaStream_t st) {
+    const uint64_t n16 = n / 16;
+    if (n16) {
+        const int grid = static_cast<int>(std::min<uint64_t>((n16 + 255) / 256, ctx->num_sms * 8));
+        k_quantize_u8<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<uint4*>(dst), n16);
+        check_launch(ctx);
+    }
+    if (n % 16) {
+        k_quantize_u8_tail<<<1, 16, 0, st>>>(src, dst, n16 * 16, n);
+        check_launch(ctx);
+    }
+}
+
 void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bool maxt,
                    agsx_splat_view* dump) {
     const uint64_t n = sc->n;
@@ -478,7 +494,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
     // K6
-    if (ctx->f_band_host && raster_uses_units(p, maxt) && p.tiles_y > 0) {
+    if ((ctx->f_band_host || ctx->f_band_host_u8) && raster_uses_units(p, maxt) && p.tiles_y > 0) {
         // banded egress: the raster runs in bands of whole tile rows; band b's
         // rows are copied to the page-locked host image on the copy stream while
         // band b+1 renders (the copy engine is the faster PCIe writer)
@@ -492,14 +508,26 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
             pb.unit_hi = 2u * static_cast<uint32_t>(r1 * p.tiles_x);
             launch_raster(ctx, pb, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ctx->f_image, nullptr, ctr,
                           &ctr->tile_ctr[8 + b]);
-            AGSX_CUDA(cudaEventRecord(ctx->band_ev[b], st));
-            AGSX_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_ev[b], 0));
             const size_t y0 = static_cast<size_t>(r0) * p.tile_size;
             const size_t y1 = std::min(static_cast<size_t>(r1) * p.tile_size, static_cast<size_t>(p.H));
-            const size_t row_bytes = static_cast<size_t>(p.W) * 12;
-            AGSX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->f_band_host) + y0 * row_bytes,
-                                      reinterpret_cast<char*>(ctx->f_image) + y0 * row_bytes, (y1 - y0) * row_bytes,
-                                      cudaMemcpyDeviceToHost, ctx->copy_stream));
+            if (ctx->f_band_host_u8) {
+                // row f3: quantise the band to PPM bytes (write_image) on the
+                // device; only the bytes cross PCIe
+                const uint64_t off = y0 * static_cast<uint64_t>(p.W) * 3, len = (y1 - y0) * static_cast<uint64_t>(p.W) * 3;
+                launch_quantize(ctx, ctx->f_image + off, ptr<uint8_t>(ctx->img_u8) + off, len, st);
+            }
+            AGSX_CUDA(cudaEventRecord(ctx->band_ev[b], st));
+            AGSX_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->band_ev[b], 0));
+            if (ctx->f_band_host_u8) {
+                const size_t row_bytes = static_cast<size_t>(p.W) * 3;
+                AGSX_CUDA(cudaMemcpyAsync(ctx->f_band_host_u8 + y0 * row_bytes, ptr<uint8_t>(ctx->img_u8) + y0 * row_bytes,
+                                          (y1 - y0) * row_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
+            } else {
+                const size_t row_bytes = static_cast<size_t>(p.W) * 12;
+                AGSX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->f_band_host) + y0 * row_bytes,
+                                          reinterpret_cast<char*>(ctx->f_image) + y0 * row_bytes, (y1 - y0) * row_bytes,
+                                          cudaMemcpyDeviceToHost, ctx->copy_stream));
+            }
         }
         AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
         AGSX_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
@@ -522,7 +550,8 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
 }
 
 int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, const agsx_config* cfg,
-                const agsx_lut* lut, bool maxt, float* host_image = nullptr, float* device_target = nullptr) {
+                const agsx_lut* lut, bool maxt, float* host_image = nullptr, float* device_target = nullptr,
+                uint8_t* host_u8 = nullptr) {
     if (!sc) return fail(ctx, AGSX_EINVAL, "render: null scene");
     if (sc->device != ctx->device) return fail(ctx, AGSX_EINVAL, "scene lives on another device");
     FrameParams p;
@@ -552,7 +581,19 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     ctx->f_image = device_target ? device_target : ptr<float>(ctx->image);
     ctx->f_image_on_host = device_target != nullptr;  // the ctx image is not this frame's
     ctx->f_band_host = nullptr;
+    ctx->f_band_host_u8 = nullptr;
     ctx->f_host_dst = nullptr;
+    ctx->f_host_dst_u8 = nullptr;
+    if (host_u8 && raster_uses_units(p, maxt)) {
+        cudaPointerAttributes at{};
+        const uint64_t n = static_cast<uint64_t>(cam->width) * cam->height * 3;
+        if (cudaPointerGetAttributes(&at, host_u8) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+            at.devicePointer != nullptr) {
+            ensure(ctx->img_u8, std::max<uint64_t>(n, 16));
+            ctx->f_band_host_u8 = host_u8;  // the float image stays in ctx->image as well
+        }
+        cudaGetLastError();
+    }
     if (host_image && !device_target) {
         // A page-locked host destination: the default rasterizer fills it by
         // banded copy-engine transfers behind the raster (57 GB/s); other
@@ -614,6 +655,30 @@ int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
     return fail(ctx, AGSX_ECUDA, "pair arena did not converge");
 }
 
+}  // namespace
+
+namespace {
+// The finished frame's write_image bytes into host memory `image_u8` when no
+// banded u8 egress ran: quantised on the device, then through the mapping
+// (page-locked) or one copy (pageable).
+int quantize_to_host(agsx_ctx* ctx, uint8_t* image_u8) {
+    const uint64_t n = static_cast<uint64_t>(ctx->f_cam.width) * ctx->f_cam.height * 3;
+    uint8_t* dst = nullptr;  // device-visible destination
+    cudaPointerAttributes at{};
+    const bool mapped = cudaPointerGetAttributes(&at, image_u8) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+                        at.devicePointer != nullptr && (reinterpret_cast<uintptr_t>(at.devicePointer) & 15u) == 0;
+    cudaGetLastError();
+    if (mapped) {
+        dst = static_cast<uint8_t*>(at.devicePointer);
+    } else {
+        ensure(ctx->tmp0, std::max<uint64_t>(n, 16));
+        dst = ptr<uint8_t>(ctx->tmp0);
+    }
+    launch_quantize(ctx, ptr<float>(ctx->image), dst, n, ctx->stream);
+    if (!mapped) AGSX_CUDA(cudaMemcpyAsync(image_u8, dst, n, cudaMemcpyDeviceToHost, ctx->stream));
+    AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+    return AGSX_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -702,7 +767,7 @@ void agsx_destroy(agsx_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (Buf* b : {&ctx->status, &ctx->p0, &ctx->p1, &ctx->p2, &ctx->p3, &ctx->p4, &ctx->dkeys,
-                   &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->dcounts, &ctx->chunks, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
+                   &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->dcounts, &ctx->chunks, &ctx->img_u8, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
                    &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
                    &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tile_pit, &ctx->calib, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
                    &ctx->tmp3, &ctx->tmp4})
@@ -851,9 +916,13 @@ int agsx_render_wait(agsx_ctx* ctx, agsx_frame* out) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
         float* dst = ctx->f_host_dst;
+        uint8_t* dst8 = ctx->f_host_dst_u8;
         ctx->f_host_dst = nullptr;
+        ctx->f_host_dst_u8 = nullptr;
         const int rc = finish_frame(ctx, out);
-        if (rc || !dst || ctx->f_image_on_host) return rc;
+        if (rc) return rc;
+        if (dst8) return ctx->f_band_host_u8 ? AGSX_OK : quantize_to_host(ctx, dst8);
+        if (!dst || ctx->f_image_on_host) return rc;
         AGSX_CUDA(cudaMemcpyAsync(dst, ctx->image.p, static_cast<size_t>(ctx->f_cam.width) * ctx->f_cam.height * 12,
                                   cudaMemcpyDeviceToHost, ctx->stream));
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -889,36 +958,23 @@ int agsx_render_u8(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* ca
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
         if (!image_u8) return fail(ctx, AGSX_EINVAL, "render_u8: null image");
-        int rc = start_frame(ctx, scene, cam, cfg, lut, false);
+        int rc = start_frame(ctx, scene, cam, cfg, lut, false, nullptr, nullptr, image_u8);
         if (rc) return rc;
         rc = finish_frame(ctx, out);
         if (rc) return rc;
-        const uint64_t n = static_cast<uint64_t>(cam->width) * cam->height * 3;
-        uint8_t* dst = nullptr;  // device-visible destination
-        cudaPointerAttributes at{};
-        const bool mapped = cudaPointerGetAttributes(&at, image_u8) == cudaSuccess &&
-                            at.type == cudaMemoryTypeHost && at.devicePointer != nullptr &&
-                            (reinterpret_cast<uintptr_t>(at.devicePointer) & 15u) == 0;
-        cudaGetLastError();
-        if (mapped) {
-            dst = static_cast<uint8_t*>(at.devicePointer);
-        } else {
-            ensure(ctx->tmp0, std::max<uint64_t>(n, 16));
-            dst = ptr<uint8_t>(ctx->tmp0);
-        }
-        const uint64_t n16 = n / 16;
-        if (n16) {
-            const int grid = static_cast<int>(std::min<uint64_t>((n16 + 255) / 256, ctx->num_sms * 8));
-            k_quantize_u8<<<grid, 256, 0, ctx->stream>>>(ptr<float4>(ctx->image), reinterpret_cast<uint4*>(dst), n16);
-            check_launch(ctx);
-        }
-        if (n % 16) {
-            k_quantize_u8_tail<<<1, 16, 0, ctx->stream>>>(ptr<float>(ctx->image), dst, n16 * 16, n);
-            check_launch(ctx);
-        }
-        if (!mapped) AGSX_CUDA(cudaMemcpyAsync(image_u8, dst, n, cudaMemcpyDeviceToHost, ctx->stream));
-        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
-        return AGSX_OK;
+        if (ctx->f_band_host_u8) return AGSX_OK;  // bands already copied behind the raster
+        return quantize_to_host(ctx, image_u8);
+    });
+}
+
+int agsx_render_async_host_u8(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                              const agsx_config* cfg, const agsx_lut* lut, uint8_t* image_u8) {
+    if (!ctx) return AGSX_EINVAL;
+    if (!image_u8) return fail(ctx, AGSX_EINVAL, "render_async_host_u8: null image");
+    return guarded(ctx, [&]() -> int {
+        const int rc = start_frame(ctx, scene, cam, cfg, lut, false, nullptr, nullptr, image_u8);
+        if (rc == AGSX_OK) ctx->f_host_dst_u8 = image_u8;
+        return rc;
     });
 }
 

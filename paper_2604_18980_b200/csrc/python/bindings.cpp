@@ -305,20 +305,30 @@ public:
     // frame's kernels (batch.render_views).
     void render_async_host(Scene& scene, int view, const std::string& mode, double k,
                            const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size, bool exact,
-                           std::size_t pair_budget, py::object camera) {
+                           std::size_t pair_budget, py::object camera, bool image_u8) {
         const agsx_camera cam = camera.is_none() ? view_of(scene, view) : camera_from(camera.cast<py::dict>());
         const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
         const LutHolder lut(lut_bins, dmin, dmax);
         agsx_scene* dev = device_scene(scene);
-        py::array_t<float> img = pinned_image<float>(cam.height, cam.width);
+        const agsx_lut* lp = cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr;
         int rc;
-        {
-            py::gil_scoped_release nogil;
-            rc = agsx_render_async_host(ctx_, dev, &cam, &cfg, cfg.mode == AGSX_MODE_ADAGSCALE ? &lut.lut : nullptr,
-                                        img.mutable_data());
+        if (image_u8) {
+            py::array_t<std::uint8_t> img = pinned_image<std::uint8_t>(cam.height, cam.width);
+            {
+                py::gil_scoped_release nogil;
+                rc = agsx_render_async_host_u8(ctx_, dev, &cam, &cfg, lp, img.mutable_data());
+            }
+            if (rc != AGSX_OK) raise_status(rc, ctx_);
+            pending_image_ = img;
+        } else {
+            py::array_t<float> img = pinned_image<float>(cam.height, cam.width);
+            {
+                py::gil_scoped_release nogil;
+                rc = agsx_render_async_host(ctx_, dev, &cam, &cfg, lp, img.mutable_data());
+            }
+            if (rc != AGSX_OK) raise_status(rc, ctx_);
+            pending_image_ = img;
         }
-        if (rc != AGSX_OK) raise_status(rc, ctx_);
-        pending_image_ = img;
     }
 
     py::dict wait() {
@@ -778,7 +788,8 @@ PYBIND11_MODULE(_core, m) {
         .def("render_async_host", &Renderer::render_async_host, py::arg("scene"), py::arg("view") = 0,
              py::arg("mode") = "ellipse", py::arg("k") = 0.0, py::arg("lut_bins") = std::vector<float>{},
              py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("tile_size") = 16,
-             py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27, py::arg("camera") = py::none())
+             py::arg("exact") = false, py::arg("pair_budget") = std::size_t{1} << 27, py::arg("camera") = py::none(),
+             py::arg("image_u8") = false)
         .def("wait", &Renderer::wait)
         .def("pair_report", &Renderer::pair_report, py::arg("scene"), py::arg("specs"),
              py::arg("views") = std::vector<int>{}, py::arg("lut_bins") = std::vector<float>{},

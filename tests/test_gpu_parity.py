@@ -522,6 +522,16 @@ def test_render_u8_egress_matches_host_quantisation(ctx, port):
     rc = ctx.L.agsx_render_u8(ctx.h, dev, C.byref(cam), C.byref(gpu_cfg("adagscale", 0.3, exact=True)),
                               C.byref(capi.make_lut([0.7] * 20)), buf.ctypes.data, C.byref(f))
     assert rc == 0 and np.array_equal(buf, want)
+    # default rasterizer: banded egress, each band quantised on the device and
+    # copied behind the raster (band lengths not multiples of 16 bytes)
+    f32 = r.render(s, 1, "adagscale", 0.3, [0.7] * 20)["image"]
+    want = np.floor(np.clip(f32, 0, 1).astype(np.float64) * 255.0 + 0.5).astype(np.uint8)
+    got = r.render(s, 1, "adagscale", 0.3, [0.7] * 20, image_u8=True)["image"]
+    assert np.array_equal(got, want)
+    buf[:] = 0
+    rc = ctx.L.agsx_render_u8(ctx.h, dev, C.byref(cam), C.byref(gpu_cfg("adagscale", 0.3)),
+                              C.byref(capi.make_lut([0.7] * 20)), buf.ctypes.data, C.byref(f))
+    assert rc == 0 and np.array_equal(buf, want)
 
 
 def test_psnr_device_matches_reference_formula():
@@ -598,6 +608,11 @@ def test_render_views_host_pipelined(port, n_ctx):
         assert out["image"].shape == (136, 200, 3)
         assert np.array_equal(out["image"].view(np.uint32), ref["image"].view(np.uint32)), v
         assert out["pair_count"] == ref["pair_count"] and out["splat_count"] == ref["splat_count"]
+    outs8 = render_views(rs, s, views, mode="ellipse", image_u8=True)  # banded PPM egress
+    for v, out in zip(views, outs8):
+        ref8 = P.render(s, view=v, mode="ellipse", image_u8=True)
+        assert out["image"].dtype == np.uint8 and np.array_equal(out["image"], ref8["image"]), v
+        assert out["pair_count"] == ref8["pair_count"]
     got = {}
     render_views(rs, s, views, on_frame=lambda i, out: got.__setitem__(i, out), mode="ellipse", exact=True)
     assert sorted(got) == list(range(len(views)))
