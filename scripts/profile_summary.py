@@ -22,7 +22,7 @@ col = {k: h.index(k) for k in ("Kernel Name", "gpu__time_duration.sum", "dram__b
 assert rows[1][col["gpu__time_duration.sum"]] == "us" and rows[1][col["dram__bytes_read.sum"]] == "Mbyte"
 agg = collections.OrderedDict()
 for r in rows[2:]:
-    base = r[col["Kernel Name"]].split("(")[0].replace("void ", "").split("<")[0].strip()
+    base = r[col["Kernel Name"]].split("(")[0].replace("void ", "").replace("<unnamed>::", "").split("<")[0].strip()
     st = STAGE.get(base, base)
     a = agg.setdefault(st, {"launches": 0, "ncu_us": 0.0, "dram_bytes": 0, "warp_inst": 0, "kernels": []})
     a["launches"] += 1
@@ -47,7 +47,7 @@ lh = lr[0]
 ki, vi = lh.index("Kernel Name"), lh.index("Metric Value")
 per = collections.OrderedDict()
 for r in lr[1:]:
-    per.setdefault(r[ki].split("(")[0].replace("void ", "").split("<")[0].strip(), []).append(float(r[vi]))
+    per.setdefault(r[ki].split("(")[0].replace("void ", "").replace("<unnamed>::", "").split("<")[0].strip(), []).append(float(r[vi]))
 tot = sum(sum(v) for k, v in per.items() if k != "k_pack_scene")
 with open(f"profiles/{tag}_launches_summary.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialised), bench.py --steps 2 "
