@@ -316,7 +316,7 @@ void sort_hist(agsx_ctx* ctx, const K* keys, const uint32_t* n_dev, uint64_t n_h
 // One stable LSD pass over at most n_host keys (three kernels).
 template <typename K>
 void sort_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32_t* vout, const uint32_t* n_dev,
-               uint64_t n_host, int shift, bool sentinel, uint32_t* n_out, SortCountOut co = {}) {
+               uint64_t n_host, int shift, bool sentinel, uint32_t* n_out, SortCountOut co = {}, SortBias sb = {}) {
     const bool k64 = sizeof(K) == 8;
     const uint64_t tiles = (n_host + kSortTile - 1) / kSortTile;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(
@@ -324,7 +324,7 @@ void sort_pass(agsx_ctx* ctx, const K* kin, const uint32_t* vin, K* kout, uint32
     ensure(ctx->sort_counts, static_cast<size_t>(grid) * 256 * 4 + 256 * 4);
     uint32_t* counts = ptr<uint32_t>(ctx->sort_counts);
     launch_sort_pass<K>(grid, sort_smem(k64), ctx->stream, kin, vin, kout, vout, n_dev, n_host, shift, sentinel,
-                        static_cast<K>(~K(0)), counts, counts + static_cast<size_t>(grid) * 256, n_out, co);
+                        static_cast<K>(~K(0)), counts, counts + static_cast<size_t>(grid) * 256, n_out, co, sb);
     check_launch(ctx);
     ctx->launches += 2;  // three kernels per pass
 }
@@ -400,6 +400,13 @@ int prepare(agsx_ctx* ctx, const agsx_camera* cam, const agsx_config* cfg, const
 }
 
 // Enqueue the whole frame (no host synchronisation).
+// Host twin of depth_keys_wide: whether the frame's depth order ended in the
+// [0] (4 passes) or [1] (3 passes) ping-pong buffers.
+bool depth_keys_wide_host(const Counters& c) {
+    const uint32_t kmin = ~c.kmin_c;
+    return c.kmax >= kmin && c.kmax - kmin >= (1u << 24);
+}
+
 __global__ void k_counters_out(const uint32_t* __restrict__ src, uint32_t* dst, int words) {
     for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
 }
@@ -453,17 +460,27 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     uint32_t* dv[2] = {ptr<uint32_t>(ctx->dvals), ptr<uint32_t>(ctx->dvals2)};
     uint32_t* chunk_sum = ptr<uint32_t>(ctx->chunks);
     uint32_t* chunk_off = chunk_sum + chunk_slots(n);
+    // Digits are those of key - kmin (K1's range counters): when the frame's
+    // keys span < 2^24 (depth max/min below ~2, the common case) the 4th pass
+    // exits at once on the device and the order is final after 3 passes, in
+    // dv[1] instead of dv[0] (K3 reads the one the device chose).
     if (n > 0) {
-        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m);
+        SortBias sb;
+        sb.kmin_c = &ctr->kmin_c;
+        sb.kmax = &ctr->kmax;
+        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m, {}, sb);
         for (int ps = 1; ps < 4; ++ps) {
             SortCountOut co;
-            if (ps == 3) {  // the depth order's tile counts + per-chunk sums for K3
+            SortBias sp = sb;
+            if (ps >= 2) {  // the depth order's tile counts + per-chunk sums for K3, from the last pass run
                 co.src = ptr<uint32_t>(ctx->status);
                 co.out = ptr<uint32_t>(ctx->dcounts);
                 co.chunk_sum = chunk_sum;
+                sp.co_if_narrow = ps == 2;
+                sp.only_wide = ps == 3;
             }
             sort_pass<uint32_t>(ctx, dk[ps & 1], dv[ps & 1], dk[(ps + 1) & 1], dv[(ps + 1) & 1], &ctr->m, n, 8 * ps,
-                                false, nullptr, co);
+                                false, nullptr, co, sp);
         }
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[2], st));
@@ -475,7 +492,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         check_launch(ctx);
         // the big stage when the previous frame averaged > 10 pairs per splat
         const bool big = ctx->pairs_per_splat > 10.0;
-        AGSX_CUDA(launch_emit(big, ctx->num_sms * (big ? ctx->occ_emit_big : ctx->occ_emit), st, p, dv[0],
+        AGSX_CUDA(launch_emit(big, ctx->num_sms * (big ? ctx->occ_emit_big : ctx->occ_emit), st, p, dv[0], dv[1],
                               ptr<uint32_t>(ctx->dcounts), chunk_off, pl, tk[0], pv[0], ctx->pair_capacity, ctr));
         check_launch(ctx);
     }
@@ -1051,8 +1068,9 @@ int agsx_dump_sorted_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* gids, uint64
         const uint64_t n = ctx->f_scene->n;
         std::vector<uint32_t> dk(c.m), dv(c.m), tk(P), pv(P);
         if (c.m) {
-            AGSX_CUDA(cudaMemcpy(dk.data(), ctx->dkeys.p, c.m * 4, cudaMemcpyDeviceToHost));
-            AGSX_CUDA(cudaMemcpy(dv.data(), ctx->dvals.p, c.m * 4, cudaMemcpyDeviceToHost));
+            const bool wide = depth_keys_wide_host(c);  // which ping-pong buffer holds the depth order
+            AGSX_CUDA(cudaMemcpy(dk.data(), wide ? ctx->dkeys.p : ctx->dkeys2.p, c.m * 4, cudaMemcpyDeviceToHost));
+            AGSX_CUDA(cudaMemcpy(dv.data(), wide ? ctx->dvals.p : ctx->dvals2.p, c.m * 4, cudaMemcpyDeviceToHost));
         }
         if (P) {
             AGSX_CUDA(cudaMemcpy(tk.data(), ctx->f_tkeys, P * 4, cudaMemcpyDeviceToHost));
@@ -1332,8 +1350,10 @@ int agsx_fold_max_t(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* c
         uint32_t* dfold = ptr<uint32_t>(ctx->calib);
         AGSX_CUDA(cudaMemsetAsync(dfold, 0, static_cast<size_t>(2 * nb) * 4, ctx->stream));
         if (scene->n) {
+            const bool wide = depth_keys_wide_host(*ctx->h_ctr);  // finish_frame synchronised
             k_fold_max_t<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
-                ptr<uint32_t>(ctx->dvals), ptr<uint32_t>(ctx->dkeys), &ptr<Counters>(ctx->ctr)->m,
+                ptr<uint32_t>(wide ? ctx->dvals : ctx->dvals2), ptr<uint32_t>(wide ? ctx->dkeys : ctx->dkeys2),
+                &ptr<Counters>(ctx->ctr)->m,
                 ptr<uint32_t>(ctx->maxt), lut_shape->depth_min, lut_shape->depth_max, nb, dfold, dfold + nb);
             check_launch(ctx);
         }

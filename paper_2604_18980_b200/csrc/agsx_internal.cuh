@@ -469,6 +469,15 @@ struct Counters {
     uint32_t pad0;
     unsigned long long p_it;  // pairs iterated before tile saturation (raster work)
     unsigned long long dbg[8];  // raster work counters (AGSX_RASTER_STATS=1)
+    uint32_t kmin_c;  // ~(min depth key of the splats with >= 1 tile), by atomicMax (0 = none)
+    uint32_t kmax;    // max depth key of those splats
 };
+
+// The depth keys of a frame span >= 2^24 (key - kmin needs a 4th 8-bit
+// pass); false when there are no keys.
+__device__ __forceinline__ bool depth_keys_wide(uint32_t kmin_c, uint32_t kmax) {
+    const uint32_t kmin = ~kmin_c;
+    return kmax >= kmin && kmax - kmin >= (1u << 24);
+}
 
 }  // namespace agsx

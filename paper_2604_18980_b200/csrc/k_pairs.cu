@@ -115,7 +115,8 @@ k_scan_chunks(const uint32_t* __restrict__ chunk_sum, uint32_t* __restrict__ chu
 // and written as one contiguous run of the chunk when they fit.
 template <int STAGE>
 __global__ void __launch_bounds__(256)
-k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __restrict__ counts_sorted,
+k_emit(FrameParams p, const uint32_t* __restrict__ order_wide, const uint32_t* __restrict__ order_narrow,
+       const uint32_t* __restrict__ counts_sorted,
        const uint32_t* __restrict__ chunk_off, SplatPlanes pl, uint32_t* __restrict__ tkeys,
        uint32_t* __restrict__ pvals, uint64_t capacity, const Counters* ctr) {
     griddep_wait();
@@ -126,7 +127,9 @@ k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __rest
     __shared__ uint32_t s_warp[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t m = ctr->m;
-    if (ctr->p_eff == 0u) return;  // nothing fits (overflow: the host grows the arena and re-runs)
+    if (ctr->p_eff == 0u) return;
+    // the depth order is in the buffer of the last sort pass that ran
+    const uint32_t* __restrict__ order = depth_keys_wide(ctr->kmin_c, ctr->kmax) ? order_wide : order_narrow;  // nothing fits (overflow: the host grows the arena and re-runs)
     const uint32_t nchunks = (m + 255u) / 256u;
     for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const uint32_t j = c * 256u + tid;
@@ -177,12 +180,14 @@ k_emit(FrameParams p, const uint32_t* __restrict__ order, const uint32_t* __rest
 }
 
 cudaError_t launch_emit(bool big, int grid, cudaStream_t st, const FrameParams& p, const uint32_t* order,
-                        const uint32_t* counts_sorted, const uint32_t* chunk_off, const SplatPlanes& pl,
+                        const uint32_t* order_narrow, const uint32_t* counts_sorted, const uint32_t* chunk_off, const SplatPlanes& pl,
                         uint32_t* tkeys, uint32_t* pvals, uint64_t capacity, const Counters* ctr) {
     if (big)
-        return launch_pdl(k_emit<kEmitStageBig>, dim3(grid), dim3(256), emit_smem(true), st, p, order, counts_sorted,
+        return launch_pdl(k_emit<kEmitStageBig>, dim3(grid), dim3(256), emit_smem(true), st, p, order, order_narrow,
+                          counts_sorted,
                           chunk_off, pl, tkeys, pvals, capacity, ctr);
-    return launch_pdl(k_emit<kEmitStageSmall>, dim3(grid), dim3(256), emit_smem(false), st, p, order, counts_sorted,
+    return launch_pdl(k_emit<kEmitStageSmall>, dim3(grid), dim3(256), emit_smem(false), st, p, order, order_narrow,
+                      counts_sorted,
                       chunk_off, pl, tkeys, pvals, capacity, ctr);
 }
 

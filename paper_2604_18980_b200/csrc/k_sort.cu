@@ -22,6 +22,18 @@ __device__ __forceinline__ uint32_t digit_of(K k, int shift) {
     return static_cast<uint32_t>(k >> shift) & 0xffu;
 }
 
+// Reads the pass's bias (kmin of the frame's depth keys, or 0) and whether the
+// pass runs at all (a 4th depth pass only when the keys span >= 2^24).
+__device__ __forceinline__ bool bias_of(const SortBias& sb, uint32_t& bias, bool& wide) {
+    bias = 0;
+    wide = true;
+    if (!sb.kmin_c) return true;
+    const uint32_t kmin_c = *sb.kmin_c, kmax = *sb.kmax;
+    wide = depth_keys_wide(kmin_c, kmax);
+    bias = ~kmin_c;
+    return !(sb.only_wide && !wide);
+}
+
 // Exclusive scan of one value per thread over a kSortThreads-thread block.
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t v, uint32_t* s_warp) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -53,8 +65,11 @@ __device__ __forceinline__ void chunk_of(uint64_t n, int G, int c, uint64_t& lo,
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
-          K sentinel, uint32_t* __restrict__ counts) {
+          K sentinel, uint32_t* __restrict__ counts, SortBias sb) {
     griddep_wait();
+    uint32_t bias;
+    bool wide;
+    if (!bias_of(sb, bias, wide)) return;
     constexpr int W = kSortThreads / 32;
     __shared__ uint32_t sh[W][256];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -77,7 +92,7 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
         for (int u = 0; u < U; ++u) {
             const uint32_t vmask = __ballot_sync(0xffffffffu, ok[u]);
             if (!vmask) continue;
-            const uint32_t d = digit_of(k[u], shift);
+            const uint32_t d = digit_of(static_cast<K>(k[u] - static_cast<K>(bias)), shift);
             const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(vmask) - 1);
             if (__all_sync(0xffffffffu, !ok[u] || d == d0)) {
                 if (lane == 0) sh[warp][d0] += __popc(vmask);
@@ -96,8 +111,11 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
 // Column scan of the G x 256 count matrix (one block per digit, G <= 1024
 // threads): counts[c][d] <- sum_{c' < c} counts[c'][d]; totals[d] = column sum.
 __global__ void __launch_bounds__(1024)
-k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ totals) {
+k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ totals, SortBias sb) {
     griddep_wait();
+    uint32_t bias;
+    bool wide;
+    if (!bias_of(sb, bias, wide)) return;
     __shared__ uint32_t s_warp[32];
     const int d = blockIdx.x, c = threadIdx.x, lane = c & 31, warp = c >> 5;
     const uint32_t v = c < G ? counts[static_cast<uint64_t>(c) * 256 + d] : 0u;
@@ -132,8 +150,12 @@ __global__ void __launch_bounds__(kSortThreads, 3)
 k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
             uint32_t* __restrict__ vout, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
             K sentinel, const uint32_t* __restrict__ counts_excl, const uint32_t* __restrict__ totals,
-            uint32_t* n_out, SortCountOut co) {
+            uint32_t* n_out, SortCountOut co, SortBias sb) {
     griddep_wait();
+    uint32_t bias;
+    bool wide;
+    if (!bias_of(sb, bias, wide)) return;
+    if (sb.co_if_narrow && wide) co.src = nullptr;  // a 4th pass follows and emits the counts
     constexpr int W = kSortThreads / 32;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s_keys = reinterpret_cast<K*>(smem_raw);
@@ -191,7 +213,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         uint32_t peers[kSortItems];
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
-            const uint32_t d = digit_of(k[it], shift);
+            const uint32_t d = digit_of(static_cast<K>(k[it] - static_cast<K>(bias)), shift);
             uint32_t pm = full ? 0xffffffffu : __ballot_sync(0xffffffffu, ok[it]);
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
@@ -202,7 +224,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         }
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
-            const uint32_t d = digit_of(k[it], shift);
+            const uint32_t d = digit_of(static_cast<K>(k[it] - static_cast<K>(bias)), shift);
             const uint32_t lt = peers[it] & lanemask_lt;
             const uint32_t before = s_whist[warp][d];
             rank[it] = before + __popc(lt);
@@ -225,7 +247,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
 #pragma unroll
         for (int it = 0; it < kSortItems; ++it) {
             if (full || ok[it]) {
-                const uint32_t d = digit_of(k[it], shift);
+                const uint32_t d = digit_of(static_cast<K>(k[it] - static_cast<K>(bias)), shift);
                 const uint32_t lsi = s_texcl[d] + s_whist[warp][d] + rank[it];
                 s_keys[lsi] = k[it];
                 s_vals[lsi] = v[it];
@@ -239,7 +261,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             uint32_t pos = 0, val = 0;
             if (act) {
                 const K key = s_keys[i];
-                pos = s_pos[digit_of(key, shift)] + i;
+                pos = s_pos[digit_of(static_cast<K>(key - static_cast<K>(bias)), shift)] + i;
                 kout[pos] = key;
                 val = s_vals[i];
                 vout[pos] = val;
@@ -262,11 +284,13 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
 template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
                       uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift, bool use_sentinel,
-                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out, SortCountOut co) {
-    launch_pdl(k_upsweep<K>, dim3(grid), dim3(kSortThreads), 0, st, kin, n_dev, n_host, shift, use_sentinel ? 1 : 0, sentinel, counts);
-    launch_pdl(k_scan_counts, dim3(256), dim3((grid + 31) / 32 * 32), 0, st, counts, grid, totals);
+                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out, SortCountOut co,
+                      SortBias sb) {
+    launch_pdl(k_upsweep<K>, dim3(grid), dim3(kSortThreads), 0, st, kin, n_dev, n_host, shift, use_sentinel ? 1 : 0,
+               sentinel, counts, sb);
+    launch_pdl(k_scan_counts, dim3(256), dim3((grid + 31) / 32 * 32), 0, st, counts, grid, totals, sb);
     launch_pdl(k_downsweep<K>, dim3(grid), dim3(kSortThreads), smem, st, kin, vin, kout, vout, n_dev, n_host, shift,
-                                                     use_sentinel ? 1 : 0, sentinel, counts, totals, n_out, co);
+               use_sentinel ? 1 : 0, sentinel, counts, totals, n_out, co, sb);
 }
 
 template <typename K>
@@ -279,10 +303,10 @@ cudaError_t sort_configure(size_t smem, int* occupancy) {
 
 template void launch_sort_pass<uint32_t>(int, size_t, cudaStream_t, const uint32_t*, const uint32_t*, uint32_t*,
                                          uint32_t*, const uint32_t*, uint64_t, int, bool, uint32_t, uint32_t*,
-                                         uint32_t*, uint32_t*, SortCountOut);
+                                         uint32_t*, uint32_t*, SortCountOut, SortBias);
 template void launch_sort_pass<uint64_t>(int, size_t, cudaStream_t, const uint64_t*, const uint32_t*, uint64_t*,
                                          uint32_t*, const uint32_t*, uint64_t, int, bool, uint64_t, uint32_t*,
-                                         uint32_t*, uint32_t*, SortCountOut);
+                                         uint32_t*, uint32_t*, SortCountOut, SortBias);
 template cudaError_t sort_configure<uint32_t>(size_t, int*);
 template cudaError_t sort_configure<uint64_t>(size_t, int*);
 

@@ -47,6 +47,7 @@ __global__ void k_scan_chunks(const uint32_t* chunk_sum, uint32_t* chunk_off, Co
 constexpr int kEmitStageSmall = 3072, kEmitStageBig = 8192;
 constexpr size_t emit_smem(bool big) { return 2 * (big ? kEmitStageBig : kEmitStageSmall) * sizeof(uint32_t); }
 cudaError_t launch_emit(bool big, int grid, cudaStream_t st, const FrameParams& p, const uint32_t* order,
+                        const uint32_t* order_narrow,
                         const uint32_t* counts_sorted, const uint32_t* chunk_off, const SplatPlanes& pl,
                         uint32_t* tkeys, uint32_t* pvals, uint64_t capacity, const Counters* ctr);
 cudaError_t emit_configure(bool big, int* occupancy);
@@ -73,10 +74,21 @@ struct SortCountOut {
     uint32_t* out = nullptr;
     uint32_t* chunk_sum = nullptr;
 };
+// Depth-key bias of a pass (32-bit keys): digits of (key - kmin), kmin from
+// K1's range counters; `only_wide` runs the pass only when the keys span
+// >= 2^24 (the 4th depth pass), `co_if_narrow` emits SortCountOut only when
+// they do not (the 3rd pass is then the last).
+struct SortBias {
+    const uint32_t* kmin_c = nullptr;  // nullptr: no bias, always run
+    const uint32_t* kmax = nullptr;
+    int only_wide = 0;
+    int co_if_narrow = 0;
+};
 template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
                       uint32_t* vout, const uint32_t* n_dev, uint64_t n_host, int shift, bool use_sentinel,
-                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out, SortCountOut co = {});
+                      K sentinel, uint32_t* counts, uint32_t* totals, uint32_t* n_out, SortCountOut co = {},
+                      SortBias sb = {});
 template <typename K>
 cudaError_t sort_configure(size_t smem, int* occupancy);
 // Histograms of the low `npasses` 8-bit digits into hist[npasses][256]
