@@ -22,15 +22,17 @@ for _ in range(10):
 torch.cuda.synchronize()
 dt = (time.perf_counter() - t0) / 10
 print(f"raw D2H 191MB: {dt*1e3:.3f} ms = {nbytes/dt/1e9:.1f} GB/s")
-for nctx in (1, 2, 3):
+for u8, nctx in ((False, 1), (False, 2), (False, 3), (True, 1), (True, 2), (True, 3)):
     rs = [P.Renderer(0) for _ in range(nctx)]
-    kw = dict(mode="adagscale", k=K, lut_bins=B)
+    kw = dict(mode="adagscale", k=K, lut_bins=B, image_u8=u8)
     render_views(rs, s, [0] * 6, on_frame=lambda i, o: None, **kw)
     ts = []
     t0 = time.perf_counter()
     render_views(rs, s, [0] * 24, on_frame=lambda i, o: ts.append(time.perf_counter() - t0), **kw)
     d = np.diff([0.0] + ts) * 1e3
-    print(f"{nctx} ctx: {24/ts[-1]:.1f} FPS; per-frame ms", " ".join(f"{x:.2f}" for x in d))
+    print(f"{'u8' if u8 else 'f32'} {nctx} ctx: {24/ts[-1]:.1f} FPS; per-frame ms", " ".join(f"{x:.2f}" for x in d[:8]))
+for _ in range(3):
+    P.render(s, 0, "adagscale", K, B)
 t0 = time.perf_counter()
 for _ in range(10):
     P.render(s, 0, "adagscale", K, B)
