@@ -12,6 +12,7 @@
 // read it there.  The host reads one 128-byte counter block when the caller
 // waits for the frame; a pair count above the buffer capacity (but within
 // pair_budget) grows the pair arena and re-runs the frame.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -113,6 +114,7 @@ struct agsx_ctx {
     static constexpr int kBands = 8;
     cudaEvent_t band_ev[kBands] = {};
     cudaEvent_t copy_done = nullptr;
+    cudaEvent_t ev_zeroed = nullptr;  // the frame's counters are zeroed (band flags valid from here)
     uint32_t* f_tkeys = nullptr;
     uint32_t* f_pvals = nullptr;
     int f_tile_count = 0;
@@ -400,6 +402,23 @@ int prepare(agsx_ctx* ctx, const agsx_camera* cam, const agsx_config* cfg, const
 }
 
 // Enqueue the whole frame (no host synchronisation).
+// cuStreamWaitValue32 through the runtime's driver entry point (no link
+// against libcuda): the copy stream waits on the raster's per-band unit
+// counts in device memory.  nullptr when the driver does not offer it.
+using WaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValue32Fn wait_value32() {
+    static const WaitValue32Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        cudaGetLastError();
+        return reinterpret_cast<WaitValue32Fn>(f);
+    }();
+    return fn;
+}
+
 // Host twin of depth_keys_wide: whether the frame's depth order ended in the
 // [0] (4 passes) or [1] (3 passes) ping-pong buffers.
 bool depth_keys_wide_host(const Counters& c) {
@@ -445,6 +464,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, tiles * 8, st));
     }
     if (maxt) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, n * 4, st));
+    AGSX_CUDA(cudaEventRecord(ctx->ev_zeroed, st));
     const SplatPlanes pl = planes_of(ctx);
     if (n > 0) {
         const int grid = static_cast<int>((n + 255) / 256);
@@ -511,10 +531,52 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
     // K6
-    if ((ctx->f_band_host || ctx->f_band_host_u8) && raster_uses_units(p, maxt) && p.tiles_y > 0) {
-        // banded egress: the raster runs in bands of whole tile rows; band b's
-        // rows are copied to the page-locked host image on the copy stream while
-        // band b+1 renders (the copy engine is the faster PCIe writer)
+    const bool banded = (ctx->f_band_host || ctx->f_band_host_u8) && raster_uses_units(p, maxt) && p.tiles_y > 0;
+    const char* eg = std::getenv("AGSX_EGRESS");
+    const bool flags = banded && wait_value32() && !(eg && std::strcmp(eg, "launches") == 0);
+    if (flags) {
+        // banded egress, one raster launch: every unit adds itself to its
+        // band's count once its pixels are stored; the copy stream waits for
+        // a band's count (cuStreamWaitValue32) and copies its rows to the
+        // page-locked host image while later bands render.  PPM egress: the
+        // raster also writes the quantised bytes and only those are copied.
+        const int B = std::min(agsx_ctx::kBands, p.tiles_y);
+        const int rows_per = (p.tiles_y + B - 1) / B;
+        uint8_t* u8 = ctx->f_band_host_u8 ? ptr<uint8_t>(ctx->img_u8) : nullptr;
+        launch_raster_units(ctx->num_sms * ctx->occ_raster, st, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1,
+                            pl.p2, ctx->f_image, &ctr->tile_ctr[3], ptr<unsigned long long>(ctx->tile_pit), &ctr->p_it,
+                            ctr->dbg, ctr->band_done, rows_per, u8);
+        check_launch(ctx);
+        AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
+        AGSX_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_zeroed, 0));  // not last frame's counts
+        for (int b = 0; b < B; ++b) {
+            const int r0 = b * rows_per, r1 = std::min(p.tiles_y, r0 + rows_per);
+            if (r0 >= r1) break;
+            const uint32_t units_b = 2u * static_cast<uint32_t>((r1 - r0) * p.tiles_x);
+            const CUresult cr = wait_value32()(reinterpret_cast<CUstream>(ctx->copy_stream),
+                                               reinterpret_cast<CUdeviceptr>(&ctr->band_done[b]), units_b,
+                                               CU_STREAM_WAIT_VALUE_GEQ);
+            if (cr != CUDA_SUCCESS)
+                throw StatusError{AGSX_ECUDA, "cuStreamWaitValue32 failed (" + std::to_string(static_cast<int>(cr)) + ")"};
+            const size_t y0 = static_cast<size_t>(r0) * p.tile_size;
+            const size_t y1 = std::min(static_cast<size_t>(r1) * p.tile_size, static_cast<size_t>(p.H));
+            if (u8) {
+                const size_t row_bytes = static_cast<size_t>(p.W) * 3;
+                AGSX_CUDA(cudaMemcpyAsync(ctx->f_band_host_u8 + y0 * row_bytes, u8 + y0 * row_bytes,
+                                          (y1 - y0) * row_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
+            } else {
+                const size_t row_bytes = static_cast<size_t>(p.W) * 12;
+                AGSX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->f_band_host) + y0 * row_bytes,
+                                          reinterpret_cast<char*>(ctx->f_image) + y0 * row_bytes, (y1 - y0) * row_bytes,
+                                          cudaMemcpyDeviceToHost, ctx->copy_stream));
+            }
+        }
+        AGSX_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
+        AGSX_CUDA(cudaStreamWaitEvent(st, ctx->copy_done, 0));
+    } else if (banded) {
+        // banded egress over one raster launch per band (drivers without
+        // stream wait-value): band b's rows are copied to the page-locked host
+        // image on the copy stream while band b+1 renders
         const int B = std::min(agsx_ctx::kBands, p.tiles_y);
         const int rows_per = (p.tiles_y + B - 1) / B;
         for (int b = 0; b < B; ++b) {
@@ -752,6 +814,7 @@ int agsx_create(int device, agsx_ctx** out) {
         AGSX_CUDA(shared_copy_stream(device, &ctx->copy_stream));
         for (auto& e : ctx->band_ev) AGSX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         AGSX_CUDA(cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming));
+        AGSX_CUDA(cudaEventCreateWithFlags(&ctx->ev_zeroed, cudaEventDisableTiming));
         AGSX_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
         AGSX_CUDA(sort_configure<uint32_t>(sort_smem(false), &ctx->occ_sort32));
         AGSX_CUDA(sort_configure<uint64_t>(sort_smem(true), &ctx->occ_sort64));
@@ -796,6 +859,7 @@ void agsx_destroy(agsx_ctx* ctx) {
     for (auto& e : ctx->band_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+    if (ctx->ev_zeroed) cudaEventDestroy(ctx->ev_zeroed);
     if (ctx->copy_stream) cudaStreamSynchronize(ctx->copy_stream);  // shared per device: not destroyed
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;

@@ -362,7 +362,8 @@ __global__ void __launch_bounds__(256, 3)
 k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
                float* __restrict__ image, uint32_t* unit_ctr, unsigned long long* __restrict__ tile_pit,
-               unsigned long long* __restrict__ pit, unsigned long long* dbg) {
+               unsigned long long* __restrict__ pit, unsigned long long* dbg, uint32_t* band_done, int band_rows,
+               uint8_t* __restrict__ img_u8) {
     griddep_wait();
     // STATS: dbg[0] += splat iterations per warp, dbg[1] += live pixel
     // evaluations, dbg[2] += fast blends, dbg[3] += exact re-evaluations
@@ -583,7 +584,32 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                     image[(static_cast<size_t>(y0 + row) * p.W + x0 + col) * 3 + c] = so[(row * 16 + col) * 3 + c];
                 }
             }
+            if (img_u8) {  // write_image bytes of the unit: lround(clamp(v) * 255) (gsio.cpp:265-281)
+                auto q8 = [](float v) {
+                    return static_cast<uint32_t>(floor(static_cast<double>(sclamp(v, 0.0f, 1.0f)) * 255.0 + 0.5));
+                };
+                if (w == 16 && (p.W & 3) == 0) {  // 12 words of 4 bytes per row
+                    for (int i = lane; i < 12 * h; i += 32) {
+                        const int row = i / 12, col = i % 12;
+                        const float* v = &so[row * 48 + 4 * col];
+                        const uint32_t word = q8(v[0]) | (q8(v[1]) << 8) | (q8(v[2]) << 16) | (q8(v[3]) << 24);
+                        *reinterpret_cast<uint32_t*>(img_u8 + (static_cast<size_t>(y0 + row) * p.W + x0) * 3 + 4 * col) =
+                            word;
+                    }
+                } else {
+                    for (int i = lane; i < w * h * 3; i += 32) {
+                        const int c = i % 3, pix = i / 3, row = pix / w, col = pix % w;
+                        img_u8[(static_cast<size_t>(y0 + row) * p.W + x0 + col) * 3 + c] =
+                            static_cast<uint8_t>(q8(so[(row * 16 + col) * 3 + c]));
+                    }
+                }
+            }
             __syncwarp();
+        }
+        if (band_done) {  // this unit's pixels are in memory: count it for its egress band
+            __threadfence();  // every lane's image stores, before the count the copy stream waits on
+            __syncwarp();
+            if (lane == 0) atomicAdd(&band_done[ty / band_rows], 1u);
         }
         unit = nunit;
         rg = nrg;
@@ -609,18 +635,21 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
 
 void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
                          const float4* P0, const float4* P1, const float4* P2, float* image, uint32_t* unit_ctr,
-                         unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg) {
+                         unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg,
+                         uint32_t* band_done, int band_rows, uint8_t* img_u8) {
     static const int mode = [] {
         const char* e = std::getenv("AGSX_RASTER_RECT");
         const char* t = std::getenv("AGSX_RASTER_STATS");
         return ((e && *e == '1') ? 1 : 0) | ((t && *t == '1') ? 2 : 0);
     }();
+#define AGSX_RU_ARGS st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg, band_done, band_rows, img_u8
     switch (mode) {
-        case 0: launch_pdl(k_raster_units<false, false>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
-        case 1: launch_pdl(k_raster_units<true, false>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
-        case 2: launch_pdl(k_raster_units<false, true>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
-        default: launch_pdl(k_raster_units<true, true>, dim3(grid), dim3(256), 0, st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg); break;
+        case 0: launch_pdl(k_raster_units<false, false>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
+        case 1: launch_pdl(k_raster_units<true, false>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
+        case 2: launch_pdl(k_raster_units<false, true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
+        default: launch_pdl(k_raster_units<true, true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
     }
+#undef AGSX_RU_ARGS
 }
 
 cudaError_t raster_units_occupancy(int* occ) {

@@ -106,7 +106,8 @@ void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t
 // per tile).
 void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
                          const float4* P0, const float4* P1, const float4* P2, float* image, uint32_t* unit_ctr,
-                         unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg);
+                         unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg,
+                         uint32_t* band_done = nullptr, int band_rows = 1, uint8_t* img_u8 = nullptr);
 cudaError_t raster_units_occupancy(int* occ);
 
 __global__ void k_fold_max_t(const uint32_t* order, const uint32_t* dkeys, const uint32_t* m_dev,
