@@ -534,6 +534,26 @@ def test_render_u8_egress_matches_host_quantisation(ctx, port):
     assert rc == 0 and np.array_equal(buf, want)
 
 
+@pytest.mark.parametrize("egress", ["launches", "zerocopy"])
+def test_egress_variants_identical(monkeypatch, egress):
+    """The host egress variants deliver the same frame: banded in one raster
+    launch with device band counts (default), one raster launch per band
+    (AGSX_EGRESS=launches, drivers without stream wait-value) and zero-copy
+    SM stores into the mapped buffer (AGSX_EGRESS=zerocopy); f32 and PPM."""
+    import paper_2604_18980_b200 as P
+
+    s = P.synth_scene(6, 20000, "veil", cameras=2, width=347, height=261, focal=270.0)
+    r = P.Renderer(0)
+    ref = r.render(s, 1, "adagscale", 0.3, [0.7] * 20)
+    ref8 = r.render(s, 1, "adagscale", 0.3, [0.7] * 20, image_u8=True)
+    monkeypatch.setenv("AGSX_EGRESS", egress)
+    out = r.render(s, 1, "adagscale", 0.3, [0.7] * 20)
+    out8 = r.render(s, 1, "adagscale", 0.3, [0.7] * 20, image_u8=True)
+    assert np.array_equal(out["image"].view(np.uint32), ref["image"].view(np.uint32))
+    assert np.array_equal(out8["image"], ref8["image"])
+    assert out["pair_count"] == ref["pair_count"]
+
+
 def test_psnr_device_matches_reference_formula():
     import torch
 
