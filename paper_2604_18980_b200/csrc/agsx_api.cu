@@ -111,7 +111,8 @@ struct agsx_ctx {
     uint8_t* f_host_dst_u8 = nullptr;   // agsx_render_async_host_u8 destination (quantised in wait if pageable)
     float* f_band_host = nullptr;  // page-locked host image filled by banded copies behind the raster
     cudaStream_t copy_stream = nullptr;
-    static constexpr int kBands = 8;
+    static constexpr int kBands = 8;       // egress bands with one raster launch per band (fallback)
+    static constexpr int kFlagBands = 16;  // egress bands of the one-launch path (Counters::band_done)
     cudaEvent_t band_ev[kBands] = {};
     cudaEvent_t copy_done = nullptr;
     cudaEvent_t ev_zeroed = nullptr;  // the frame's counters are zeroed (band flags valid from here)
@@ -535,13 +536,19 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     const char* eg = std::getenv("AGSX_EGRESS");
     const bool flags = banded && wait_value32() && !(eg && std::strcmp(eg, "launches") == 0);
     if (flags) {
-        // banded egress, one raster launch: every unit adds itself to its
-        // band's count once its pixels are stored; the copy stream waits for
-        // a band's count (cuStreamWaitValue32) and copies its rows to the
-        // page-locked host image while later bands render.  PPM egress: the
-        // raster also writes the quantised bytes and only those are copied.
-        const int B = std::min(agsx_ctx::kBands, p.tiles_y);
-        const int rows_per = (p.tiles_y + B - 1) / B;
+        // banded egress, one raster launch: the tile rows form 16 slots and
+        // every unit adds itself to its slot's count once its pixels are
+        // stored; the copy stream waits for the counts (cuStreamWaitValue32)
+        // and copies finished rows to the page-locked host image while later
+        // rows render.  f32 frames: slots are copied in groups 1, 2, 5, 8 --
+        // the raster runs ~4.6x faster than PCIe, so each group is done
+        // before the previous copy ends, the first copy starts after 1/16 of
+        // the raster and a frame costs 4 copies (each costs ~8 us of PCIe
+        // setup).  PPM bytes: PCIe is about as fast as the raster, so every
+        // slot is its own copy and the last copy is short.  The raster also
+        // writes the PPM bytes; only those are copied.
+        const int S = std::min(agsx_ctx::kFlagBands, p.tiles_y);
+        const int rows_per = (p.tiles_y + S - 1) / S;
         uint8_t* u8 = ctx->f_band_host_u8 ? ptr<uint8_t>(ctx->img_u8) : nullptr;
         launch_raster_units(ctx->num_sms * ctx->occ_raster, st, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1,
                             pl.p2, ctx->f_image, &ctr->tile_ctr[3], ptr<unsigned long long>(ctx->tile_pit), &ctr->p_it,
@@ -549,27 +556,36 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         check_launch(ctx);
         AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
         AGSX_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_zeroed, 0));  // not last frame's counts
-        for (int b = 0; b < B; ++b) {
-            const int r0 = b * rows_per, r1 = std::min(p.tiles_y, r0 + rows_per);
-            if (r0 >= r1) break;
-            const uint32_t units_b = 2u * static_cast<uint32_t>((r1 - r0) * p.tiles_x);
-            const CUresult cr = wait_value32()(reinterpret_cast<CUstream>(ctx->copy_stream),
-                                               reinterpret_cast<CUdeviceptr>(&ctr->band_done[b]), units_b,
-                                               CU_STREAM_WAIT_VALUE_GEQ);
-            if (cr != CUDA_SUCCESS)
-                throw StatusError{AGSX_ECUDA, "cuStreamWaitValue32 failed (" + std::to_string(static_cast<int>(cr)) + ")"};
-            const size_t y0 = static_cast<size_t>(r0) * p.tile_size;
-            const size_t y1 = std::min(static_cast<size_t>(r1) * p.tile_size, static_cast<size_t>(p.H));
-            if (u8) {
-                const size_t row_bytes = static_cast<size_t>(p.W) * 3;
-                AGSX_CUDA(cudaMemcpyAsync(ctx->f_band_host_u8 + y0 * row_bytes, u8 + y0 * row_bytes,
-                                          (y1 - y0) * row_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
-            } else {
-                const size_t row_bytes = static_cast<size_t>(p.W) * 12;
-                AGSX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->f_band_host) + y0 * row_bytes,
-                                          reinterpret_cast<char*>(ctx->f_image) + y0 * row_bytes, (y1 - y0) * row_bytes,
-                                          cudaMemcpyDeviceToHost, ctx->copy_stream));
+        static const int kF32Groups[] = {1, 3, 8, 16};  // slot group ends for f32 frames
+        int s0 = 0;
+        for (int gi = 0; s0 * rows_per < p.tiles_y; ++gi) {
+            const int s1 = u8 ? s0 + 1 : std::min(S, std::max(s0 + 1, kF32Groups[std::min(gi, 3)] * S / 16));
+            for (int sl = s0; sl < s1; ++sl) {
+                const int r0 = sl * rows_per, r1 = std::min(p.tiles_y, r0 + rows_per);
+                if (r0 >= r1) break;
+                const uint32_t units_s = 2u * static_cast<uint32_t>((r1 - r0) * p.tiles_x);
+                const CUresult cr = wait_value32()(reinterpret_cast<CUstream>(ctx->copy_stream),
+                                                   reinterpret_cast<CUdeviceptr>(&ctr->band_done[sl]), units_s,
+                                                   CU_STREAM_WAIT_VALUE_GEQ);
+                if (cr != CUDA_SUCCESS)
+                    throw StatusError{AGSX_ECUDA,
+                                      "cuStreamWaitValue32 failed (" + std::to_string(static_cast<int>(cr)) + ")"};
             }
+            const size_t y0 = static_cast<size_t>(s0) * rows_per * p.tile_size;
+            const size_t y1 = std::min(static_cast<size_t>(s1) * rows_per * p.tile_size, static_cast<size_t>(p.H));
+            if (y1 > y0) {
+                if (u8) {
+                    const size_t row_bytes = static_cast<size_t>(p.W) * 3;
+                    AGSX_CUDA(cudaMemcpyAsync(ctx->f_band_host_u8 + y0 * row_bytes, u8 + y0 * row_bytes,
+                                              (y1 - y0) * row_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
+                } else {
+                    const size_t row_bytes = static_cast<size_t>(p.W) * 12;
+                    AGSX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->f_band_host) + y0 * row_bytes,
+                                              reinterpret_cast<char*>(ctx->f_image) + y0 * row_bytes,
+                                              (y1 - y0) * row_bytes, cudaMemcpyDeviceToHost, ctx->copy_stream));
+                }
+            }
+            s0 = s1;
         }
         AGSX_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
         AGSX_CUDA(cudaStreamWaitEvent(st, ctx->copy_done, 0));
