@@ -255,7 +255,7 @@ struct BlendRecord {
 
 struct RecordOptions {
     bool max_t = false;
-    bool contributions = false;  // analysis-only stream; rejected on the device path
+    bool contributions = false;  // full blend-event stream (glibc-exact alpha on the device)
 };
 
 struct RenderReport {

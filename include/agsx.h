@@ -183,6 +183,25 @@ int agsx_render_async_host(agsx_ctx* ctx, const agsx_scene* scene, const agsx_ca
 int agsx_render_async_host_u8(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
                               const agsx_config* cfg, const agsx_lut* lut, uint8_t* image_u8);
 
+/* One alpha-blend event, BlendRecord (rasterizer.hpp:19-24). */
+typedef struct agsx_blend_record {
+    uint32_t pixel; /* y * width + x */
+    uint32_t splat; /* index into the view's splat sequence (survivors in Gaussian order) */
+    float alpha;
+    float weight; /* alpha * T */
+} agsx_blend_record;
+
+/* agsx_render with RecordOptions::contributions (rasterizer.cpp:21-100,
+ * 135-161): the frame is rendered with the glibc-exact alpha and its
+ * blend-event stream written to `records` in the reference's order (tile
+ * index, then pair order, then row-major pixel).  *count receives the stream
+ * length; AGSX_ECAPACITY when `capacity` is smaller (the frame and `out` are
+ * complete either way, so a caller sizes the buffer and calls again).  `out`
+ * as for agsx_render (image and max_t optional). */
+int agsx_render_contributions(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                              const agsx_config* cfg, const agsx_lut* lut, agsx_blend_record* records,
+                              uint64_t capacity, uint64_t* count, agsx_frame* out);
+
 /* Device-timed stage durations (ms: preprocess, pair_gen, sort, raster) of
  * the last min(max_frames, 64) frames enqueued on this ctx, oldest first;
  * synchronises the stream. */

@@ -851,9 +851,15 @@ static float alpha_at(const ago_splat* s, float px, float py, float clamp) {
     return a < clamp ? a : clamp;
 }
 
+/* Blend-event sink of raster_tile (RecordOptions::contributions). */
+typedef struct {
+    ago_blend* out;
+    uint64_t capacity, count;
+} blend_sink;
+
 static void raster_tile(const ago_splat* splats, const uint32_t* idx,
                         uint32_t begin, uint32_t end, const grid_t* g, int tile,
-                        const ago_config* cfg, float* image, float* max_t) {
+                        const ago_config* cfg, float* image, float* max_t, blend_sink* sink) {
     const int tx = tile % g->tiles_x, ty = tile / g->tiles_x;
     const int x0 = tx * g->tile_size, y0 = ty * g->tile_size;
     const int w = mini_(g->tile_size, g->width - x0);
@@ -879,6 +885,16 @@ static void raster_tile(const ago_splat* splats, const uint32_t* idx,
                 if (a < tau) continue;
                 if (max_t && t_cur > max_t[idx[p]]) max_t[idx[p]] = t_cur;
                 const float weight = a * t_cur;
+                if (sink) { /* rasterizer.cpp:73-77 */
+                    if (sink->count < sink->capacity) {
+                        ago_blend* r = &sink->out[sink->count];
+                        r->pixel = (uint32_t)((y0 + iy) * g->width + (x0 + ix));
+                        r->splat = idx[p];
+                        r->alpha = a;
+                        r->weight = weight;
+                    }
+                    ++sink->count;
+                }
                 C[pi * 3 + 0] += weight * s->rgb[0];
                 C[pi * 3 + 1] += weight * s->rgb[1];
                 C[pi * 3 + 2] += weight * s->rgb[2];
@@ -899,6 +915,17 @@ static void raster_tile(const ago_splat* splats, const uint32_t* idx,
     free(C);
 }
 
+static void raster_all(const ago_splat* splats, uint64_t n_splats, const uint32_t* splat_index,
+                       const uint32_t* ranges, int32_t width, int32_t height, const ago_config* cfg,
+                       float* image, float* max_t, blend_sink* sink) {
+    const grid_t g = make_grid(width, height, cfg->tile_size);
+    if (max_t) memset(max_t, 0, sizeof(float) * n_splats);
+    memset(image, 0, sizeof(float) * 3 * (size_t)width * height);
+    for (int t = 0; t < g.tiles_x * g.tiles_y; ++t) /* tile-index order (rasterizer.cpp:155-161) */
+        raster_tile(splats, splat_index, ranges[2 * t], ranges[2 * t + 1], &g, t,
+                    cfg, image, max_t, sink);
+}
+
 int ago_raster(const ago_splat* splats, uint64_t n_splats,
                const uint64_t* keys, const uint32_t* splat_index,
                uint64_t n_pairs, const uint32_t* ranges, int32_t width,
@@ -906,20 +933,15 @@ int ago_raster(const ago_splat* splats, uint64_t n_splats,
                float* max_t) {
     (void)keys;
     (void)n_pairs;
-    const grid_t g = make_grid(width, height, cfg->tile_size);
-    if (max_t) memset(max_t, 0, sizeof(float) * n_splats);
-    memset(image, 0, sizeof(float) * 3 * (size_t)width * height);
-    for (int t = 0; t < g.tiles_x * g.tiles_y; ++t)
-        raster_tile(splats, splat_index, ranges[2 * t], ranges[2 * t + 1], &g, t,
-                    cfg, image, max_t);
+    raster_all(splats, n_splats, splat_index, ranges, width, height, cfg, image, max_t, NULL);
     return AGO_OK;
 }
 
 /* ------------------------------------------------------------------ */
-int ago_render(const ago_scene* scene, const ago_camera* cam,
-               const ago_config* cfg, const ago_lut* lut, float* image,
-               uint64_t* pair_count, uint64_t* splat_count, float* max_t,
-               double* stage_s) {
+static int render_impl(const ago_scene* scene, const ago_camera* cam,
+                       const ago_config* cfg, const ago_lut* lut, float* image,
+                       uint64_t* pair_count, uint64_t* splat_count, float* max_t,
+                       double* stage_s, blend_sink* sink) {
     if (!cfg_valid(cfg) || !cam_valid(cam)) return AGO_EINVAL;
     static const float ones20[20] = {1, 1, 1, 1, 1, 1, 1, 1, 1, 1,
                                      1, 1, 1, 1, 1, 1, 1, 1, 1, 1};
@@ -941,8 +963,7 @@ int ago_render(const ago_scene* scene, const ago_camera* cam,
                             keys, idx, total, counts, &total);
     uint32_t* ranges = (uint32_t*)malloc(sizeof(uint32_t) * 2 * (size_t)g.tiles_x * g.tiles_y);
     ago_sort_pairs(keys, idx, total, g.tiles_x * g.tiles_y, ranges);
-    ago_raster(splats, ns, keys, idx, total, ranges, cam->width, cam->height, cfg,
-               image, max_t);
+    raster_all(splats, ns, idx, ranges, cam->width, cam->height, cfg, image, max_t, sink);
     *pair_count = total;
     *splat_count = ns;
     if (stage_s) stage_s[0] = stage_s[1] = stage_s[2] = stage_s[3] = 0.0;
@@ -952,6 +973,24 @@ int ago_render(const ago_scene* scene, const ago_camera* cam,
     free(idx);
     free(ranges);
     return AGO_OK;
+}
+
+int ago_render(const ago_scene* scene, const ago_camera* cam,
+               const ago_config* cfg, const ago_lut* lut, float* image,
+               uint64_t* pair_count, uint64_t* splat_count, float* max_t,
+               double* stage_s) {
+    return render_impl(scene, cam, cfg, lut, image, pair_count, splat_count, max_t, stage_s, NULL);
+}
+
+int ago_render_contributions(const ago_scene* scene, const ago_camera* cam, const ago_config* cfg,
+                             const ago_lut* lut, float* image, ago_blend* out, uint64_t capacity,
+                             uint64_t* count) {
+    blend_sink sink = {out, out ? capacity : 0, 0};
+    uint64_t pc = 0, sc = 0;
+    const int rc = render_impl(scene, cam, cfg, lut, image, &pc, &sc, NULL, NULL, &sink);
+    if (rc) return rc;
+    *count = sink.count;
+    return sink.count > sink.capacity ? AGO_ECAPACITY : AGO_OK;
 }
 
 double ago_psnr(const float* a, const float* b, uint64_t n) {

@@ -134,6 +134,23 @@ int ago_render(const ago_scene* scene, const ago_camera* cam,
                uint64_t* pair_count, uint64_t* splat_count, float* max_t,
                double* stage_s);
 
+/* BlendRecord (rasterizer.hpp:19-24): one alpha-blend event. */
+typedef struct {
+    uint32_t pixel; /* y * width + x */
+    uint32_t splat; /* index into the view's (compacted) splat sequence */
+    float alpha;
+    float weight; /* alpha * T */
+} ago_blend;
+
+/* render with RecordOptions::contributions (rasterizer.cpp:21-100,
+ * 135-161): the blend-event stream in tile-index order, within a tile pair
+ * order then row-major pixel order.  out: capacity records; *count receives
+ * the stream length; AGO_ECAPACITY when capacity is too small (the image is
+ * rendered either way). */
+int ago_render_contributions(const ago_scene* scene, const ago_camera* cam, const ago_config* cfg,
+                             const ago_lut* lut, float* image, ago_blend* out, uint64_t capacity,
+                             uint64_t* count);
+
 /* psnr (analysis.cpp:14-25). */
 double ago_psnr(const float* a, const float* b, uint64_t n);
 

@@ -93,6 +93,10 @@ def _fp(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_float))
 
 
+# BlendRecord (rasterizer.hpp:19-24) / ago_blend / agsx_blend_record
+BLEND_DTYPE = np.dtype([("pixel", "<u4"), ("splat", "<u4"), ("alpha", "<f4"), ("weight", "<f4")])
+
+
 def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -313,6 +317,25 @@ class Oracle:
         if max_t:
             out["max_t"] = mt[: sc.value].copy()
         return out
+
+    def render_contributions(self, scene: SoAScene, cam, cfg, lut=None):
+        """render with RecordOptions::contributions: (image, records) with records a
+        structured array {pixel u32, splat u32, alpha f32, weight f32} in the
+        reference's order (tile index, then pair, then row-major pixel)."""
+        img = np.zeros((cam.height, cam.width, 3), np.float32)
+        d = scene.desc()
+        if cfg.mode == MODES["adagscale"] and lut is None:
+            lut = Lut(0.0, 100.0, 0, None)
+        count = C.c_uint64()
+        args = (C.byref(d), C.byref(cam), C.byref(cfg), C.byref(lut) if lut is not None else None, _p(img))
+        rc = self.lib.ago_render_contributions(*args, None, 0, C.byref(count))
+        if rc not in (AGO_OK, AGO_ECAPACITY):
+            raise OracleError(rc, "render_contributions")
+        rec = np.zeros(max(count.value, 1), BLEND_DTYPE)
+        rc = self.lib.ago_render_contributions(*args, rec.ctypes.data_as(C.c_void_p), len(rec), C.byref(count))
+        if rc:
+            raise OracleError(rc, "render_contributions")
+        return img, rec[: count.value]
 
     def calibrate(self, scene: SoAScene, target_drop: float, calib_views: int = 16, thread_count: int = 0):
         """Reference calibrate_scene (build_lut + search_k); reference build only."""

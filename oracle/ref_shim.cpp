@@ -326,6 +326,29 @@ int ago_render(const ago_scene* scene, const ago_camera* cam,
     });
 }
 
+// render with RecordOptions::contributions (rasterizer.cpp:135-161).
+int ago_render_contributions(const ago_scene* scene, const ago_camera* cam, const ago_config* cfg,
+                             const ago_lut* lut, float* image, ago_blend* out, uint64_t capacity,
+                             uint64_t* count) {
+    return guarded([&] {
+        const auto g = to_scene(scene);
+        const ags::TUpperLUT l = to_lut(lut);
+        const ags::RenderConfig c = to_cfg(cfg);
+        ags::RecordOptions rec;
+        rec.contributions = true;
+        const ags::RenderReport rep =
+            ags::render(g, to_cam(cam), c, c.mode == ags::Mode::AdaGScale ? &l : nullptr, rec);
+        std::memcpy(image, rep.image.data.data(), rep.image.data.size() * sizeof(float));
+        *count = rep.contributions.size();
+        if (!out || capacity < rep.contributions.size()) return AGO_ECAPACITY;
+        for (std::size_t i = 0; i < rep.contributions.size(); ++i) {
+            const ags::BlendRecord& r = rep.contributions[i];
+            out[i] = ago_blend{r.pixel, r.splat, r.alpha, r.weight};
+        }
+        return AGO_OK;
+    });
+}
+
 // calibrate_scene of the reference binding (bindings.cpp:104-127):
 // build_lut + search_k (calibrate.cpp:14-155) with a default RenderConfig.
 int ago_calibrate(const ago_scene* scene, const ago_camera* views, int32_t n_views, double target_drop,

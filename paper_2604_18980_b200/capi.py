@@ -23,7 +23,7 @@ FLAG_EXACT_ALPHA = 1
 EXPORTS = (
     "agsx_abi_version", "agsx_create", "agsx_destroy", "agsx_last_error", "agsx_stream",
     "agsx_scene_upload", "agsx_scene_free", "agsx_scene_count", "agsx_render",
-    "agsx_render_async", "agsx_render_async_to", "agsx_render_async_host", "agsx_render_async_host_u8", "agsx_render_wait", "agsx_device_image", "agsx_dump_tile_counts",
+    "agsx_render_async", "agsx_render_async_to", "agsx_render_async_host", "agsx_render_async_host_u8", "agsx_render_contributions", "agsx_render_wait", "agsx_device_image", "agsx_dump_tile_counts",
     "agsx_dump_sorted_pairs", "agsx_dump_ranges", "agsx_preprocess_view",
     "agsx_generate_pairs", "agsx_sort_pairs", "agsx_raster", "agsx_device_logf",
     "agsx_device_expf", "agsx_kernel_launches", "agsx_stage_history",
@@ -103,6 +103,10 @@ class SceneDesc(C.Structure):
         ("opacity", C.c_void_p),
         ("sh", C.c_void_p),
     ]
+
+
+# agsx_blend_record / BlendRecord (rasterizer.hpp:19-24)
+BLEND_DTYPE = np.dtype([("pixel", "<u4"), ("splat", "<u4"), ("alpha", "<f4"), ("weight", "<f4")])
 
 
 class Frame(C.Structure):
@@ -185,6 +189,8 @@ class Lib:
         L.agsx_render_async_to.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp]
         L.agsx_render_async_host.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp]
         L.agsx_render_async_host_u8.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp]
+        L.agsx_render_contributions.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp,
+                                                C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(Frame)]
         L.agsx_render_u8.argtypes = [vp, vp, C.POINTER(Camera), C.POINTER(Config), C.POINTER(Lut), vp,
                                      C.POINTER(Frame)]
         L.agsx_render_wait.argtypes = [vp, C.POINTER(Frame)]
@@ -275,6 +281,22 @@ class Context:
         if max_t:
             out["max_t_by_gid"] = mt
         return out
+
+    def render_contributions(self, scene, cam: Camera, cfg: Config, lut=None):
+        """(image, records): agsx_render_contributions, sized by a first call."""
+        img = np.zeros((cam.height, cam.width, 3), np.float32)
+        f = Frame(_p(img), None, 0, 0)
+        count = C.c_uint64()
+        lp = C.byref(lut) if lut is not None else None
+        rc = self.L.agsx_render_contributions(self.h, scene, C.byref(cam), C.byref(cfg), lp, None, 0,
+                                              C.byref(count), C.byref(f))
+        if rc not in (0, 5):
+            self._check(rc)
+        rec = np.zeros(max(count.value, 1), BLEND_DTYPE)
+        self._check(self.L.agsx_render_contributions(self.h, scene, C.byref(cam), C.byref(cfg), lp,
+                                                     rec.ctypes.data_as(C.c_void_p), len(rec), C.byref(count),
+                                                     C.byref(f)))
+        return img, rec[: count.value]
 
     def render_async(self, scene, cam, cfg, lut=None):
         self._check(self.L.agsx_render_async(self.h, scene, C.byref(cam), C.byref(cfg),

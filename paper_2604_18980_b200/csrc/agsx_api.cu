@@ -1075,6 +1075,71 @@ int agsx_render_async_host_u8(agsx_ctx* ctx, const agsx_scene* scene, const agsx
     });
 }
 
+int agsx_render_contributions(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
+                              const agsx_config* cfg, const agsx_lut* lut, agsx_blend_record* records,
+                              uint64_t capacity, uint64_t* count, agsx_frame* out) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!cfg || !count) return fail(ctx, AGSX_EINVAL, "render_contributions: null config or count");
+        agsx_config c = *cfg;
+        c.flags |= AGSX_FLAG_EXACT_ALPHA;  // the stream records the reference's alpha values
+        const bool maxt = out && out->max_t;
+        int rc = start_frame(ctx, scene, cam, &c, lut, maxt, out ? out->image : nullptr);
+        if (rc) return rc;
+        rc = finish_frame(ctx, out);
+        if (rc) return rc;
+        const FrameParams& p = ctx->f_params;
+        const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
+        const uint64_t n = scene->n;
+        if (out && out->image && !ctx->f_image_on_host)
+            AGSX_CUDA(cudaMemcpyAsync(out->image, ctx->image.p, static_cast<size_t>(cam->width) * cam->height * 12,
+                                      cudaMemcpyDeviceToHost, ctx->stream));
+        if (maxt && n)
+            AGSX_CUDA(cudaMemcpyAsync(out->max_t, ctx->maxt.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        // pass 1: events per tile; host scan -> per-tile offsets in tile order
+        ensure(ctx->tmp1, std::max<uint64_t>(tiles, 1) * 4);
+        ensure(ctx->tmp2, std::max<uint64_t>(tiles, 1) * 8);
+        const SplatPlanes pl = planes_of(ctx);
+        AGSX_CUDA(launch_raster_records(ctx->stream, p, ptr<uint2>(ctx->ranges), ctx->f_pvals, pl.p0, pl.p1, pl.p2,
+                                        ptr<float>(ctx->image), ptr<uint32_t>(ctx->tmp1), nullptr, nullptr));
+        ++ctx->launches;
+        std::vector<uint32_t> per_tile(tiles);
+        std::vector<uint64_t> off(tiles);
+        if (tiles)
+            AGSX_CUDA(cudaMemcpyAsync(per_tile.data(), ctx->tmp1.p, tiles * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        uint64_t total = 0;
+        for (uint64_t t = 0; t < tiles; ++t) {
+            off[t] = total;
+            total += per_tile[t];
+        }
+        *count = total;
+        if (!records || capacity < total)
+            return fail(ctx, AGSX_ECAPACITY, "render_contributions: " + std::to_string(total) + " records");
+        if (total == 0) return AGSX_OK;
+        // pass 2: the records, then Gaussian id -> index in the view's splat sequence
+        ensure(ctx->tmp3, total * sizeof(agsx_blend_record));
+        AGSX_CUDA(cudaMemcpyAsync(ctx->tmp2.p, off.data(), tiles * 8, cudaMemcpyHostToDevice, ctx->stream));
+        AGSX_CUDA(launch_raster_records(ctx->stream, p, ptr<uint2>(ctx->ranges), ctx->f_pvals, pl.p0, pl.p1, pl.p2,
+                                        ptr<float>(ctx->image), nullptr, ptr<uint64_t>(ctx->tmp2),
+                                        ptr<agsx_blend_record>(ctx->tmp3)));
+        ++ctx->launches;
+        AGSX_CUDA(cudaMemcpyAsync(records, ctx->tmp3.p, total * sizeof(agsx_blend_record), cudaMemcpyDeviceToHost,
+                                  ctx->stream));
+        std::vector<uint32_t> st(n);
+        if (n) AGSX_CUDA(cudaMemcpyAsync(st.data(), ctx->status.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::vector<uint32_t> view_index(n);
+        uint32_t k = 0;
+        for (uint64_t i = 0; i < n; ++i) {  // survivors in Gaussian order (preprocess.cpp:158-162)
+            view_index[i] = k;
+            k += (st[i] & kAliveBit) ? 1u : 0u;
+        }
+        for (uint64_t i = 0; i < total; ++i) records[i].splat = view_index[records[i].splat];
+        return AGSX_OK;
+    });
+}
+
 int agsx_stage_history(agsx_ctx* ctx, float* stage_ms, int32_t max_frames, int32_t* out_frames) {
     if (!ctx || !stage_ms || !out_frames) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {

@@ -547,9 +547,6 @@ RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderCon
                     const TUpperLUT* lut, const RecordOptions& rec) {
     if (const std::string bad = validate(cfg); !bad.empty()) throw std::invalid_argument("render: " + bad);
     if (const std::string bad = validate(cam); !bad.empty()) throw std::invalid_argument("render: " + bad);
-    if (rec.contributions)
-        throw std::invalid_argument("render: the contributions stream is an analysis-only "
-                                    "recording and is not produced by the device path");
     agsx_ctx* ctx = thread_ctx();
     const agsx_camera c = to_c(cam);
     const agsx_config k = to_c(cfg);
@@ -565,7 +562,21 @@ RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderCon
         f.max_t = maxt_by_gid.data();
     }
     auto* sc = static_cast<const agsx_scene*>(scene.handle());
-    check(agsx_render(ctx, sc, &c, &k, lut ? &l : nullptr, &f), ctx);
+    if (rec.contributions) {
+        // blend-event stream (rasterizer.cpp:135-161): size it, then fill it
+        std::uint64_t count = 0;
+        const int rc0 = agsx_render_contributions(ctx, sc, &c, &k, lut ? &l : nullptr, nullptr, 0, &count, &f);
+        if (rc0 != AGSX_OK && rc0 != AGSX_ECAPACITY) check(rc0, ctx);
+        rep.contributions.resize(count);
+        static_assert(sizeof(BlendRecord) == sizeof(agsx_blend_record), "BlendRecord layout");
+        if (count)
+            check(agsx_render_contributions(ctx, sc, &c, &k, lut ? &l : nullptr,
+                                            reinterpret_cast<agsx_blend_record*>(rep.contributions.data()), count,
+                                            &count, &f),
+                  ctx);
+    } else {
+        check(agsx_render(ctx, sc, &c, &k, lut ? &l : nullptr, &f), ctx);
+    }
     rep.pair_count = f.pair_count;
     rep.splat_count = f.splat_count;
     rep.stage_times["preprocess"] = f.stage_ms[0] * 1e-3;

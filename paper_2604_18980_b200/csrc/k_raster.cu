@@ -845,3 +845,125 @@ void launch_raster_kernel(int ppt, bool exact, bool maxt, int grid, cudaStream_t
 }
 
 }  // namespace agsx
+
+namespace agsx {
+
+// raster_tile with the blend-event stream (RecordOptions::contributions,
+// rasterizer.cpp:21-100): one warp per tile, the reference's exact
+// per-pixel semantics (masked once T < floor, glibc-exact alpha, stop when
+// every pixel is saturated).  Per pair the tile's pixels are visited in
+// chunks of 256, lane l owning the 8 consecutive row-major pixels
+// 8l..8l+7 of a chunk, so a warp scan of the per-lane event counts places
+// the events in the reference's order (pair, then row-major pixel).  With
+// `out == nullptr` the pass only counts the tile's events into counts[tile];
+// otherwise they are written from offsets[tile].  The image is written too.
+// T and C of the tile live in shared memory (16 bytes per pixel).
+__global__ void __launch_bounds__(32)
+k_raster_records(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
+                 const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
+                 float* __restrict__ image, uint32_t* __restrict__ counts, const uint64_t* __restrict__ offsets,
+                 agsx_blend_record* __restrict__ out) {
+    extern __shared__ __align__(16) float rec_smem[];
+    __shared__ uint64_t sTab[32];
+    const int lane = threadIdx.x;
+    sTab[lane] = kExp2fTab[lane];
+    const int tile = blockIdx.x;
+    const int ts = p.tile_size;
+    const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+    const int x0 = tx * ts, y0 = ty * ts;
+    const int w = imin(ts, p.W - x0), h = imin(ts, p.H - y0);
+    const int npx = w * h;
+    float* T = rec_smem;
+    float* C = rec_smem + npx;
+    for (int i = lane; i < npx; i += 32) {
+        T[i] = 1.0f;
+        C[3 * i] = C[3 * i + 1] = C[3 * i + 2] = 0.0f;
+    }
+    __syncwarp();
+    const uint2 rg = ranges[tile];
+    const float tau = p.tau, fl = p.tfloor, aclamp = p.aclamp;
+    uint64_t at = out ? offsets[tile] : 0;
+    uint32_t n = 0;
+    int active = npx;
+    for (uint32_t k = rg.x; k < rg.y && active > 0; ++k) {
+        const uint32_t gid = vals[k];
+        const float4 a4 = P0[gid], b4 = P1[gid], c4 = P2[gid];  // {mean, ixx, 2 ixy}, {iyy, opacity, ..}, {rgb, ..}
+        for (int base = 0; base < npx; base += 256) {
+            float al[8];
+            uint32_t flags = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                al[j] = 0.0f;
+                const int pi = base + 8 * lane + j;
+                if (pi >= npx || T[pi] < fl) continue;
+                const int iy = pi / w, ix = pi - iy * w;
+                // alpha_at (rasterizer.hpp:44-50): SymMat2::quad in the reference's order
+                const float dx = (static_cast<float>(x0 + ix) + 0.5f) - a4.x;
+                const float dy = (static_cast<float>(y0 + iy) + 0.5f) - a4.y;
+                const float q = (a4.z * dx * dx + a4.w * dx * dy) + b4.x * dy * dy;
+                const float a = exact_alpha(q, b4.y, aclamp, sTab);
+                if (a < tau) continue;
+                al[j] = a;
+                flags |= 1u << j;
+            }
+            const uint32_t cnt = __popc(flags);
+            uint32_t incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            uint64_t idx = at + n + (incl - cnt);
+            int dead = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (!((flags >> j) & 1u)) continue;
+                const int pi = base + 8 * lane + j;
+                const float a = al[j], t_cur = T[pi];
+                const float weight = a * t_cur;
+                if (out) {
+                    const int iy = pi / w, ix = pi - iy * w;
+                    agsx_blend_record r;
+                    r.pixel = static_cast<uint32_t>((y0 + iy) * p.W + (x0 + ix));
+                    r.splat = gid;
+                    r.alpha = a;
+                    r.weight = weight;
+                    out[idx++] = r;
+                }
+                C[3 * pi] += weight * c4.x;
+                C[3 * pi + 1] += weight * c4.y;
+                C[3 * pi + 2] += weight * c4.z;
+                const float t_next = t_cur * (1.0f - a);
+                T[pi] = t_next;
+                dead += t_next < fl;
+            }
+            n += total;
+            active -= __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(dead));
+        }
+    }
+    if (!out && lane == 0) counts[tile] = n;
+    __syncwarp();
+    for (int i = lane; i < npx; i += 32) {
+        const int iy = i / w, ix = i - iy * w;
+        float* o = &image[(static_cast<size_t>(y0 + iy) * p.W + (x0 + ix)) * 3];
+        o[0] = sclamp(C[3 * i] + T[i] * p.bg[0], 0.0f, 1.0f);
+        o[1] = sclamp(C[3 * i + 1] + T[i] * p.bg[1], 0.0f, 1.0f);
+        o[2] = sclamp(C[3 * i + 2] + T[i] * p.bg[2], 0.0f, 1.0f);
+    }
+}
+
+cudaError_t launch_raster_records(cudaStream_t st, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
+                                  const float4* P0, const float4* P1, const float4* P2, float* image,
+                                  uint32_t* counts, const uint64_t* offsets, agsx_blend_record* out) {
+    const int grid = p.tiles_x * p.tiles_y;
+    if (grid == 0) return cudaSuccess;
+    const size_t smem = static_cast<size_t>(p.tile_size) * p.tile_size * 16;
+    static const cudaError_t attr = cudaFuncSetAttribute(k_raster_records, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         64 * 64 * 16);
+    if (attr != cudaSuccess) return attr;
+    k_raster_records<<<grid, 32, smem, st>>>(p, ranges, vals, P0, P1, P2, image, counts, offsets, out);
+    return cudaGetLastError();
+}
+
+}  // namespace agsx

@@ -109,6 +109,11 @@ void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const 
                          unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg,
                          uint32_t* band_done = nullptr, int band_rows = 1, uint8_t* img_u8 = nullptr);
 cudaError_t raster_units_occupancy(int* occ);
+// raster_tile with the blend-event stream (RecordOptions::contributions): a
+// counting pass (out == nullptr, counts per tile) or the writing pass.
+cudaError_t launch_raster_records(cudaStream_t st, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
+                                  const float4* P0, const float4* P1, const float4* P2, float* image,
+                                  uint32_t* counts, const uint64_t* offsets, agsx_blend_record* out);
 
 __global__ void k_fold_max_t(const uint32_t* order, const uint32_t* dkeys, const uint32_t* m_dev,
                              const uint32_t* maxt, float dmin, float dmax, int nbins, uint32_t* folded,

@@ -44,6 +44,18 @@ int main(int argc, char** argv) {
         .write(reinterpret_cast<const char*>(rep.image.data.data()),
                static_cast<std::streamsize>(rep.image.data.size() * sizeof(float)));
 
+    // analysis.cpp:171-173: max_t and the blend-event stream in one render
+    ags::RecordOptions rec;
+    rec.max_t = true;
+    rec.contributions = true;
+    const ags::RenderReport rep3 = ags::render(dev, cam, cfg, lp, rec);
+    std::ofstream(std::string(argv[10]) + ".contrib", std::ios::binary)
+        .write(reinterpret_cast<const char*>(rep3.contributions.data()),
+               static_cast<std::streamsize>(rep3.contributions.size() * sizeof(ags::BlendRecord)));
+    std::ofstream(std::string(argv[10]) + ".maxt", std::ios::binary)
+        .write(reinterpret_cast<const char*>(rep3.max_t.data()),
+               static_cast<std::streamsize>(rep3.max_t.size() * sizeof(float)));
+
     // exception contract (rasterizer.cpp:105-108, preprocess.cpp:123-125, pair_gen.cpp:181-184)
     int errors_ok = 0;
     try {
@@ -68,7 +80,8 @@ int main(int argc, char** argv) {
         ++errors_ok;
     }
     std::printf("{\"pair_count\": %zu, \"splat_count\": %zu, \"device_scene_same\": %s, \"errors_ok\": %d, "
-                "\"stage_keys\": %zu}\n",
-                rep.pair_count, rep.splat_count, same ? "true" : "false", errors_ok, rep.stage_times.size());
+                "\"stage_keys\": %zu, \"contributions\": %zu}\n",
+                rep.pair_count, rep.splat_count, same ? "true" : "false", errors_ok, rep.stage_times.size(),
+                rep3.contributions.size());
     return 0;
 }

@@ -554,6 +554,31 @@ def test_egress_variants_identical(monkeypatch, egress):
     assert out["pair_count"] == ref["pair_count"]
 
 
+@pytest.mark.parametrize("layout,mode,ts", [("veil", "adagscale", 16), ("slab", "ellipse", 16), ("aniso", "obb", 8),
+                                           ("ramp", "aabb", 32), ("two_slab", "ellipse", 64)])
+def test_contributions_match_oracle(ctx, port, layout, mode, ts):
+    """agsx_render_contributions (RecordOptions::contributions, rasterizer.cpp:21-100,
+    135-161): every blend event {pixel, view splat index, alpha, weight} bit-exact
+    and in the reference's order, the image bit-exact; the capacity protocol."""
+    import ctypes as C
+
+    oscene, dev = scene_pair(port, ctx, 12, 2500, layout, 2, 200, 136, 160.0)
+    ocfg = port.config(mode, k=0.4, tile_size=ts)
+    gcfg = gpu_cfg(mode, 0.4, tile_size=ts)
+    olut = port.lut([0.6] * 20)
+    glut = capi.make_lut([0.6] * 20)
+    want_img, want = port.render_contributions(oscene, oscene.cameras[1], ocfg, olut)
+    img, got = ctx.render_contributions(dev, to_gpu_cam(oscene.cameras[1]), gcfg, glut)
+    assert len(want) > 1000 and len(got) == len(want)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    assert np.array_equal(img.view(np.uint32), want_img.view(np.uint32))
+    count = C.c_uint64()
+    small = np.zeros(10, capi.BLEND_DTYPE)
+    rc = ctx.L.agsx_render_contributions(ctx.h, dev, C.byref(to_gpu_cam(oscene.cameras[1])), C.byref(gcfg),
+                                         C.byref(glut), small.ctypes.data_as(C.c_void_p), 10, C.byref(count), None)
+    assert rc == 5 and count.value == len(want)
+
+
 def test_psnr_device_matches_reference_formula():
     import torch
 
@@ -664,3 +689,12 @@ def test_cxx_drop_in_caller(tmp_path, port, layout, mode, k, lutbin):
     img = np.fromfile(out, np.float32).reshape(240, 320, 3)
     assert np.max(np.abs(img - want["image"])) <= IMG_MAX_ABS
     assert res["device_scene_same"] and res["errors_ok"] == 3 and res["stage_keys"] == 4
+    # RecordOptions{max_t, contributions} (analysis.cpp:171-173): the oracle's stream, record for record
+    cfg = port.config(mode, k=k)
+    lut = port.lut([lutbin] * 20) if lutbin else None
+    _, want_rec = port.render_contributions(o, o.cameras[1], cfg, lut)
+    got_rec = np.fromfile(str(out) + ".contrib", capi.BLEND_DTYPE)
+    assert res["contributions"] == len(want_rec) == len(got_rec) > 0
+    assert np.array_equal(got_rec.view(np.uint32), want_rec.view(np.uint32))
+    want_mt = port.render(o, o.cameras[1], cfg, lut, max_t=True)["max_t"]
+    assert np.array_equal(np.fromfile(str(out) + ".maxt", np.float32).view(np.uint32), want_mt.view(np.uint32))

@@ -80,6 +80,24 @@ def test_port_matches_reference_build(port, ref, layout):
             assert np.array_equal(ra["max_t"].view(np.uint32), rb["max_t"].view(np.uint32))
 
 
+@pytest.mark.parametrize("layout,mode,ts", [("veil", "adagscale", 16), ("slab", "ellipse", 16), ("aniso", "obb", 8)])
+def test_port_contributions_match_reference_build(port, ref, layout, mode, ts):
+    """RecordOptions::contributions (rasterizer.cpp:21-100,135-161): the port's
+    blend-event stream equals the reference's record for record, in order."""
+    a = port.synth_scene(4, 1500, layout, cameras=2, width=160, height=120, focal=125.0)
+    b = ref.synth_scene(4, 1500, layout, cameras=2, width=160, height=120, focal=125.0)
+    lut = port.lut([0.6] * 20)
+    ia, ra = port.render_contributions(a, a.cameras[1], port.config(mode, k=0.4, tile_size=ts), lut)
+    ib, rb = ref.render_contributions(b, b.cameras[1], ref.config(mode, k=0.4, tile_size=ts), lut)
+    assert len(ra) > 1000 and len(ra) == len(rb)
+    assert np.array_equal(ra.view(np.uint32), rb.view(np.uint32))
+    assert np.array_equal(ia.view(np.uint32), ib.view(np.uint32))
+    # test_rasterizer.cpp:167-180: per pixel the blend weights never exceed unit energy
+    per_pixel = np.zeros(160 * 120)
+    np.add.at(per_pixel, ra["pixel"], ra["weight"].astype(np.float64))
+    assert per_pixel.max() <= 1.0 + 1e-5
+
+
 def test_port_libm_is_host_glibc(port, ref):
     x = np.linspace(1.0, 255.0, 100_001, dtype=np.float32)
     assert np.array_equal(port.logf(x), ref.logf(x))
