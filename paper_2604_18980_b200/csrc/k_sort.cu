@@ -4,7 +4,7 @@
 //              8 passes over the 64-bit key, single-threaded)
 //
 // A pass is three kernels over G contiguous chunks (one CTA per chunk):
-//   upsweep    : per-chunk digit counts -> counts[c][d];
+//   upsweep    : per-chunk digit counts -> counts[d][c] (digit-major);
 //   scan       : column prefix of the count matrix + digit totals;
 //   downsweep  : per 2048-key tile: warp-multisplit ranking stable in input
 //                order, shared-memory staging, contiguous per-digit runs.
@@ -60,7 +60,7 @@ __device__ __forceinline__ void chunk_of(uint64_t n, int G, int c, uint64_t& lo,
     hi = min(n, lo + per * kSortTile);
 }
 
-// Upsweep: per-chunk 256-bin digit counts -> counts[c][d] (warp-private
+// Upsweep: per-chunk 256-bin digit counts -> counts[d][c] (warp-private
 // shared histograms; a warp whose 32 digits agree adds once).
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
@@ -105,11 +105,11 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
     uint32_t c = 0;
 #pragma unroll
     for (int w = 0; w < W; ++w) c += sh[w][tid];
-    counts[static_cast<uint64_t>(blockIdx.x) * 256 + tid] = c;
+    counts[static_cast<uint64_t>(tid) * gridDim.x + blockIdx.x] = c;  // digit-major: columns contiguous
 }
 
 // Column scan of the G x 256 count matrix (one block per digit, G <= 1024
-// threads): counts[c][d] <- sum_{c' < c} counts[c'][d]; totals[d] = column sum.
+// threads): counts[d][c] <- sum_{c' < c} counts[d][c']; totals[d] = column sum.
 __global__ void __launch_bounds__(1024)
 k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ totals, SortBias sb) {
     griddep_wait();
@@ -118,7 +118,7 @@ k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ total
     if (!bias_of(sb, bias, wide)) return;
     __shared__ uint32_t s_warp[32];
     const int d = blockIdx.x, c = threadIdx.x, lane = c & 31, warp = c >> 5;
-    const uint32_t v = c < G ? counts[static_cast<uint64_t>(c) * 256 + d] : 0u;
+    const uint32_t v = c < G ? counts[static_cast<uint64_t>(d) * G + c] : 0u;
     uint32_t incl = v;
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -138,7 +138,7 @@ k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ total
         if (lane == nw - 1) totals[d] = xi;
     }
     __syncthreads();
-    if (c < G) counts[static_cast<uint64_t>(c) * 256 + d] = s_warp[warp] + incl - v;
+    if (c < G) counts[static_cast<uint64_t>(d) * G + c] = s_warp[warp] + incl - v;
 }
 
 // Downsweep: CTA c walks its chunk in kSortTile-key tiles: warp multisplit
@@ -170,7 +170,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
 
     const uint32_t total = totals[tid];
     const uint32_t dexcl = block_excl_scan(total, s_scan);
-    s_base[tid] = dexcl + counts_excl[static_cast<uint64_t>(c) * 256 + tid];
+    s_base[tid] = dexcl + counts_excl[static_cast<uint64_t>(tid) * gridDim.x + c];
     if (c == 0 && tid == 255 && n_out) *n_out = dexcl + total;  // keys kept
     __syncthreads();
 
