@@ -24,7 +24,7 @@ NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -prec-div=true -prec-
 HOSTFLAGS := -std=gnu++20 -O3 -fPIC -ffp-contract=off -fno-fast-math -Iinclude -I$(CSRC)/host
 
 CU_SRCS  := $(CSRC)/k_preprocess.cu $(CSRC)/k_pairs.cu $(CSRC)/k_sort.cu $(CSRC)/k_raster.cu \
-            $(CSRC)/k_calib.cu $(CSRC)/agsx_api.cu
+            $(CSRC)/k_calib.cu $(CSRC)/agsx_frame.cu $(CSRC)/agsx_api.cu $(CSRC)/agsx_stage_api.cu
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 CU_HDRS  := $(wildcard $(CSRC)/*.cuh) include/agsx.h
 
