@@ -235,8 +235,8 @@ __device__ __forceinline__ bool tile_hit(const TileTest& t, int tx, int ty, cons
 // order (pair_gen.cpp:152-158).  For the ellipse / AdaGScale test the
 // horizontal-edge minimisers (one exact division each) depend only on the
 // tile row and are hoisted out of the column loop, and min(h0, h1, v0, v1)
-// <= r2 is decided edge by edge (the same values, so the same decision as
-// min_quad_to_rect, pair_gen.cpp:65-83).
+// <= r2 is decided edge by edge, nearest edges first (the same values, so
+// the same decision as min_quad_to_rect, pair_gen.cpp:65-83).
 template <class F>
 __device__ __forceinline__ void for_each_tile_hit(const TileTest& t, const FrameParams& p, F&& f) {
     const Span s = tile_span(t, p);
@@ -258,20 +258,27 @@ __device__ __forceinline__ void for_each_tile_hit(const TileTest& t, const Frame
         const float xh0 = cx - t.ixy * dy0 / t.ixx;
         const float xh1 = cx - t.ixy * dy1 / t.ixx;
         const bool row_in = cy >= y0 && cy <= y1;
+        // the edges nearer the centre first: a hit usually shows there (the
+        // decision is "some edge minimum <= r2" whatever the order)
+        const bool h0_first = fabsf(dy0) <= fabsf(dy1);
+        const float xha = h0_first ? xh0 : xh1, dya = h0_first ? dy0 : dy1;
+        const float xhb = h0_first ? xh1 : xh0, dyb = h0_first ? dy1 : dy0;
         float x0 = x0_first;
         for (int tx = s.tx0; tx <= s.tx1; ++tx, x0 += ts) {
             const float x1 = smin(x0 + ts, W);
             if (!box_overlap(x0, y0, x1, y1, cx, cy, t.rx, t.ry)) continue;
             bool hit = row_in && cx >= x0 && cx <= x1;  // centre inside: min = 0 <= r2
-            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh0, x0, x1) - cx, dy0) <= t.r2;
-            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh1, x0, x1) - cx, dy1) <= t.r2;
+            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xha, x0, x1) - cx, dya) <= t.r2;
+            const float dxl = x0 - cx, dxr = x1 - cx;
+            const bool v0_first = fabsf(dxl) <= fabsf(dxr);
             if (!hit) {
-                const float dx = x0 - cx;
+                const float dx = v0_first ? dxl : dxr;
                 const float y = sclamp(cy - t.ixy * dx / t.iyy, y0, y1);
                 hit = quad_form(t.ixx, t.ixy, t.iyy, dx, y - cy) <= t.r2;
             }
+            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xhb, x0, x1) - cx, dyb) <= t.r2;
             if (!hit) {
-                const float dx = x1 - cx;
+                const float dx = v0_first ? dxr : dxl;
                 const float y = sclamp(cy - t.ixy * dx / t.iyy, y0, y1);
                 hit = quad_form(t.ixx, t.ixy, t.iyy, dx, y - cy) <= t.r2;
             }
