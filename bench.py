@@ -482,12 +482,16 @@ def run_ours(args, rank, world, local_rank):
     props = torch.cuda.get_device_properties(local_rank)
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     issue_peak = props.multi_processor_count * 4 * sm_mhz * 1e6  # warp-instructions / s
-    if "raster" in prof and stage_ms[3] > 0:
-        stages["raster"]["issue_roofline"] = {
-            "bound": "issue", "achieved": prof["raster"]["warp_inst"] / (stage_ms[3] * 1e-3),
-            "peak": issue_peak, "unit": "warp-inst/s", "frac": prof["raster"]["warp_inst"] / (stage_ms[3] * 1e-3) / issue_peak,
-            "warp_inst_per_frame": prof["raster"]["warp_inst"],
-            "peak_def": f"{props.multi_processor_count} SMs x 4 SMSPs x 1 warp-inst/clk x {sm_mhz:.0f} MHz"}
+    # instruction-issue roofline of every stage (warp-instructions per frame from
+    # the ncu capture over the live stage time): the raster and K1 are issue-bound,
+    # the sort passes latency-bound (low on both rooflines)
+    for si, nm in enumerate(names):
+        if nm in prof and stage_ms[si] > 0 and prof[nm].get("warp_inst"):
+            ach = prof[nm]["warp_inst"] / (stage_ms[si] * 1e-3)
+            stages[nm]["issue_roofline"] = {
+                "bound": "issue", "achieved": ach, "peak": issue_peak, "unit": "warp-inst/s", "frac": ach / issue_peak,
+                "warp_inst_per_frame": prof[nm]["warp_inst"],
+                "peak_def": f"{props.multi_processor_count} SMs x 4 SMSPs x 1 warp-inst/clk x {sm_mhz:.0f} MHz"}
     roofline = {
         "bound": "hbm",
         "kernel": names[dom],
