@@ -253,26 +253,16 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
 
     if (i < sc.n) dkeys[i] = keep ? __float_as_uint(depth) : 0xffffffffu;
     // range of the depth keys (positive floats: bit order = value order), so
-    // the depth sort can skip its top digit when the keys span < 2^24
-    // (one atomic pair per CTA: per-warp atomics on two words contend)
+    // the depth sort can skip its top digit when the keys span < 2^24.  Per
+    // warp, and an atomic only when it improves on the value last seen (the
+    // counters only grow), so neither a block barrier nor contended atomics.
     {
-        __shared__ uint32_t s_kmax[8], s_kminc[8];
         const uint32_t kb = __float_as_uint(depth);
         const uint32_t wmax = __reduce_max_sync(0xffffffffu, keep ? kb : 0u);
         const uint32_t wminc = __reduce_max_sync(0xffffffffu, keep ? ~kb : 0u);
-        const int warp = threadIdx.x >> 5;
-        if (lane == 0) {
-            s_kmax[warp] = wmax;
-            s_kminc[warp] = wminc;
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const uint32_t a = lane < 8 ? s_kmax[lane] : 0u, b = lane < 8 ? s_kminc[lane] : 0u;
-            const uint32_t bmax = __reduce_max_sync(0xffffffffu, a), bminc = __reduce_max_sync(0xffffffffu, b);
-            if (lane == 0 && bminc) {  // bminc = 0: no splat of this CTA has a tile
-                atomicMax(&ctr->kmax, bmax);
-                atomicMax(&ctr->kmin_c, bminc);
-            }
+        if (lane == 0 && wminc) {  // wminc = 0: no splat of this warp has a tile
+            if (wmax > *reinterpret_cast<volatile uint32_t*>(&ctr->kmax)) atomicMax(&ctr->kmax, wmax);
+            if (wminc > *reinterpret_cast<volatile uint32_t*>(&ctr->kmin_c)) atomicMax(&ctr->kmin_c, wminc);
         }
     }
     const uint32_t alive_cnt = __popc(__ballot_sync(0xffffffffu, alive));
