@@ -545,7 +545,8 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
         // P_it (rasterizer.cpp:55-56): per unit n if any pixel stays
         // unsaturated, else the 1-based index of the saturating pair; per
         // tile the max over both units.  Word = (units done << 32) | max.
-        if (lane == 0 && pit) {
+        // (an empty tile contributes 0 from both units: no word to combine)
+        if (lane == 0 && pit && end > start) {
             const uint32_t mine = h <= 0 ? 0u : (all_done ? death : end - start);
             unsigned long long* wp = &tile_pit[tile];
             unsigned long long old = 0ull;  // guess "first unit of the tile": one CAS round trip when right

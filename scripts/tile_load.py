@@ -15,3 +15,6 @@ for mode, k, b in (("adagscale", K, B), ("ellipse", 0.0, [])):
     top = np.sort(n)[::-1][:10]
     print(mode, "tiles", len(n), "empty", int((n == 0).sum()), "pctl50/90/99/99.9/max", q.tolist(), "top10", top.tolist(),
           "sum", int(n.sum()), "top1pct_share", round(float(np.sort(n)[::-1][: len(n) // 100].sum() / n.sum()), 3))
+    rows = n.reshape(216, 288).sum(axis=1)
+    print(mode, "pairs per tile row (first, middle, last 10 rows):", rows[:10].tolist(), rows[100:110].tolist(),
+          rows[-10:].tolist())
