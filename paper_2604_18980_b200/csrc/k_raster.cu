@@ -433,7 +433,30 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
         for (uint32_t base = start; base < end && !all_done; base += 32) {
             const float4 cA = nA, cB = nB, cC = nC;
             if (base + 32 < end) fetch(base + 32, end);
-            bool rel = base + lane < end && meets_box(cA.x, cA.y, unpack_extent(cC.w), cx0, cx1, cy0, cy1);
+            // Box of the unit's live pixel centres (T >= floor; it only shrinks
+            // during the batch): a splat whose extent misses it can blend no
+            // live pixel -- the reference masks saturated pixels, so skipping
+            // it only drops weight below the floor and no P_it event.
+            float lx0 = cx0, lx1 = cx1, ly0 = cy0, ly1 = cy1;
+            if (base != start) {
+                int r_lo = 8, r_hi = -1;
+#pragma unroll
+                for (int k = PPT - 1; k >= 0; --k)
+                    if (T[k] >= tfloor) r_lo = 4 * g + k;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k)
+                    if (T[k] >= tfloor) r_hi = 4 * g + k;
+                const bool lv = r_hi >= 0;
+                const int xlo = __reduce_min_sync(0xffffffffu, lv ? lx : 16);
+                const int xhi = __reduce_max_sync(0xffffffffu, lv ? lx : -1);
+                const int ylo = __reduce_min_sync(0xffffffffu, lv ? r_lo : 8);
+                const int yhi = __reduce_max_sync(0xffffffffu, lv ? r_hi : -1);
+                lx0 = static_cast<float>(x0 + xlo) + 0.5f;
+                lx1 = static_cast<float>(x0 + xhi) + 0.5f;
+                ly0 = static_cast<float>(y0 + ylo) + 0.5f;
+                ly1 = static_cast<float>(y0 + yhi) + 0.5f;
+            }
+            bool rel = base + lane < end && meets_box(cA.x, cA.y, unpack_extent(cC.w), lx0, lx1, ly0, ly1);
             if (RECT && rel) rel = !rect_outside(cA, cB.x, cB.z, cx0, cx1, cy0, cy1);
             uint32_t m = __ballot_sync(0xffffffffu, rel);
             if (!m) continue;

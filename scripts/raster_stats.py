@@ -14,4 +14,4 @@ for mode, k, b in (("adagscale", K, B), ("ellipse", 0.0, [])):
     it, ev, fa, ex = st["raster_iters"], st["raster_evals"], st["raster_fast"], st["raster_exact"]
     print(mode, "pairs", st["pair_count"], "p_it", st["p_it"], "warp-iters", it, "per p_it %.2f" % (it / st["p_it"]),
           "live-evals", ev, "(%.1f of 128 per iter)" % (ev / it), "fast blends", fa, "(%.1f%% of live)" % (100 * fa / ev),
-          "exact", ex, "iters live<=32", st["raster_iters_live_le32"], "<=64", st["raster_iters_live_le64"], "empty", st["raster_iters_empty"], flush=True)
+          "exact", ex, "iters live<=32", st["raster_iters_live_le32"], "<=64", st["raster_iters_live_le64"], "empty", st["raster_iters_empty"], "no live pixel", st["raster_iters_no_live_pixel"], flush=True)
