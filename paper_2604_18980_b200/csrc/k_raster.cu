@@ -367,7 +367,8 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
     griddep_wait();
     // STATS: dbg[0] += splat iterations per warp, dbg[1] += live pixel
     // evaluations, dbg[2] += fast blends, dbg[3] += exact re-evaluations
-    unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0, st_lo32 = 0, st_lo64 = 0, st_empty = 0;
+    unsigned long long st_it = 0, st_on = 0, st_fast = 0, st_need = 0, st_lo32 = 0, st_lo64 = 0, st_empty = 0,
+                       st_dead = 0;
     constexpr int PPT = 4;
     constexpr int NWB = 8;  // warps per block
     // staged splat j of warp w: sS[w][j][0..2] = P0, P1, {rgb, log2 opacity}
@@ -522,6 +523,14 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                         any_in = any_in || !(__fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1) > qsafe + sb.z);
                     }
                     st_empty += !__any_sync(0xffffffffu, any_in);
+                    bool any_live = false;  // ... or within q <= qcut of no live (T >= floor) pixel
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) {
+                        const float dy = py[k] - sa.y;
+                        any_live = any_live || (T[k] >= tfloor &&
+                                                !(__fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1) > qsafe + sb.z));
+                    }
+                    st_dead += !__any_sync(0xffffffffu, any_live);
                 }
                 if (sb.y >= aclamp) {  // alpha_at's clamp can bind only for opacity >= clamp
 #pragma unroll
@@ -653,6 +662,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             atomicAdd(&dbg[4], st_lo32);
             atomicAdd(&dbg[5], st_lo64);
             atomicAdd(&dbg[6], st_empty);
+            atomicAdd(&dbg[7], st_dead);
         }
     }
 }
