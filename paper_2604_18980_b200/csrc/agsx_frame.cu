@@ -269,21 +269,27 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
 
     AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
     AGSX_CUDA(cudaMemsetAsync(ctr, 0, counters_bytes(), st));
-    // every frame-scoped zeroing happens before the first kernel, so the
-    // kernels form one PDL chain
-    AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
-    if (n > 0) AGSX_CUDA(cudaMemsetAsync(ctx->chunks.p, 0, chunk_slots(n) * 4, st));
-    if (raster_uses_units(p, maxt)) {
-        ensure(ctx->tile_pit, std::max<uint64_t>(tiles, 1) * 8);
-        AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, tiles * 8, st));
+    // the other frame-scoped buffers (ranges, chunk sums, per-tile P_it words)
+    // are zeroed by K1 itself, so the kernels form one PDL chain
+    const bool units = raster_uses_units(p, maxt);
+    if (units) ensure(ctx->tile_pit, std::max<uint64_t>(tiles, 1) * 8);
+    FrameZero fz;
+    fz.ranges = ptr<uint2>(ctx->ranges);
+    fz.tile_pit = units ? ptr<unsigned long long>(ctx->tile_pit) : nullptr;
+    fz.chunks = ptr<uint32_t>(ctx->chunks);
+    fz.n_tiles = static_cast<uint32_t>(tiles);
+    fz.n_chunks = n > 0 ? static_cast<uint32_t>(chunk_slots(n)) : 0u;
+    if (n == 0) {  // no K1: the raster still reads the (empty) ranges
+        AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
+        if (units) AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, tiles * 8, st));
     }
     if (maxt) AGSX_CUDA(cudaMemsetAsync(ctx->maxt.p, 0, n * 4, st));
     AGSX_CUDA(cudaEventRecord(ctx->ev_zeroed, st));
     const SplatPlanes pl = planes_of(ctx);
     if (n > 0) {
         const int grid = static_cast<int>((n + 255) / 256);
-        launch_pdl(k_preprocess, dim3(grid), dim3(256), 0, st, p, sc->view(), pl, ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys),
-                                            ctr, dump);
+        launch_pdl(k_preprocess, dim3(grid), dim3(256), 0, st, p, sc->view(), pl, ptr<uint32_t>(ctx->status),
+                   ptr<uint32_t>(ctx->dkeys), ctr, dump, fz);
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[1], st));

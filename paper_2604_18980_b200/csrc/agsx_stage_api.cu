@@ -38,7 +38,7 @@ int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_came
         if (n) {
             k_preprocess<<<static_cast<int>((n + 255) / 256), 256, 0, ctx->stream>>>(
                 p, scene->view(), planes_of(ctx), ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys), ctr,
-                ptr<agsx_splat_view>(ctx->dump));
+                ptr<agsx_splat_view>(ctx->dump), FrameZero{});
             check_launch(ctx);
         }
         std::vector<uint32_t> st(n);

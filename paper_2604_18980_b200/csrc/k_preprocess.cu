@@ -85,8 +85,17 @@ __device__ __forceinline__ void eval_color(const DevScene& sc, uint64_t i, float
 
 __global__ void __launch_bounds__(256, AGSX_PRE_MINB)
 k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ status,
-             uint32_t* __restrict__ dkeys, Counters* ctr, agsx_splat_view* __restrict__ dump) {
+             uint32_t* __restrict__ dkeys, Counters* ctr, agsx_splat_view* __restrict__ dump, FrameZero fz) {
     griddep_wait();
+    // frame-scoped zeroing (the previous frame's readers have completed)
+    for (uint64_t z = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; z < fz.n_tiles || z < fz.n_chunks;
+         z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (z < fz.n_tiles) {
+            fz.ranges[z] = make_uint2(0u, 0u);
+            if (fz.tile_pit) fz.tile_pit[z] = 0ull;
+        }
+        if (z < fz.n_chunks) fz.chunks[z] = 0u;
+    }
     const int lane = threadIdx.x & 31;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
 

@@ -32,8 +32,16 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = 8;
 constexpr int kSortTile = kSortThreads * kSortItems;  // keys per onesweep tile
 
+// Frame-scoped buffers K1 zeroes before any later kernel of the frame reads
+// them (instead of memsets ahead of the launch chain).
+struct FrameZero {
+    uint2* ranges = nullptr;                 // tiles
+    unsigned long long* tile_pit = nullptr;  // tiles (units rasterizer)
+    uint32_t* chunks = nullptr;              // chunk sums
+    uint32_t n_tiles = 0, n_chunks = 0;
+};
 __global__ void k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* status,
-                             uint32_t* dkeys, Counters* ctr, agsx_splat_view* dump);
+                             uint32_t* dkeys, Counters* ctr, agsx_splat_view* dump, FrameZero fz);
 __global__ void k_pack_scene(uint64_t n, int D, const float* mean, const float* scale,
                              const float* rot, const float* op, const float* sh, float4* pos_op,
                              float4* rotq, float4* scale_r, float2* sh_gb, float* sh_rest);
