@@ -993,9 +993,11 @@ cudaError_t launch_raster_records(cudaStream_t st, const FrameParams& p, const u
     const int grid = p.tiles_x * p.tiles_y;
     if (grid == 0) return cudaSuccess;
     const size_t smem = static_cast<size_t>(p.tile_size) * p.tile_size * 16;
-    static const cudaError_t attr = cudaFuncSetAttribute(k_raster_records, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         64 * 64 * 16);
-    if (attr != cudaSuccess) return attr;
+    if (smem > 48 * 1024) {  // per device (a process may drive several)
+        const cudaError_t attr = cudaFuncSetAttribute(k_raster_records, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      static_cast<int>(smem));
+        if (attr != cudaSuccess) return attr;
+    }
     k_raster_records<<<grid, 32, smem, st>>>(p, ranges, vals, P0, P1, P2, image, counts, offsets, out);
     return cudaGetLastError();
 }
