@@ -306,6 +306,8 @@ public:
     void render_async_host(Scene& scene, int view, const std::string& mode, double k,
                            const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size, bool exact,
                            std::size_t pair_budget, py::object camera, bool image_u8) {
+        if (!pending_image_.is_none())  // the in-flight frame still writes into its host image
+            throw std::runtime_error("render_async_host: a host frame is in flight; call wait() first");
         const agsx_camera cam = camera.is_none() ? view_of(scene, view) : camera_from(camera.cast<py::dict>());
         const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
         const LutHolder lut(lut_bins, dmin, dmax);
