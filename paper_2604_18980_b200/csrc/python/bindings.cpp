@@ -269,6 +269,8 @@ public:
     void render_async(Scene& scene, int view, const std::string& mode, double k,
                       const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size,
                       bool exact, std::size_t pair_budget, py::object camera) {
+        if (!pending_image_.is_none())
+            throw std::runtime_error("a host frame is in flight on this renderer; call wait() first");
         const agsx_camera cam = camera.is_none() ? view_of(scene, view) : camera_from(camera.cast<py::dict>());
         const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
         const LutHolder lut(lut_bins, dmin, dmax);
@@ -286,6 +288,8 @@ public:
     void render_async_to(Scene& scene, int view, std::uintptr_t target, const std::string& mode, double k,
                          const std::vector<float>& lut_bins, float dmin, float dmax, int tile_size, bool exact,
                          std::size_t pair_budget, py::object camera) {
+        if (!pending_image_.is_none())
+            throw std::runtime_error("a host frame is in flight on this renderer; call wait() first");
         const agsx_camera cam = camera.is_none() ? view_of(scene, view) : camera_from(camera.cast<py::dict>());
         const agsx_config cfg = make_config(mode, k, 0, tile_size, exact, pair_budget);
         const LutHolder lut(lut_bins, dmin, dmax);
