@@ -658,6 +658,12 @@ def test_render_views_host_pipelined(port, n_ctx):
         ref8 = P.render(s, view=v, mode="ellipse", image_u8=True)
         assert out["image"].dtype == np.uint8 and np.array_equal(out["image"], ref8["image"]), v
         assert out["pair_count"] == ref8["pair_count"]
+    rs[0].render_async_host(s, 0, mode="ellipse")
+    with pytest.raises(RuntimeError):  # its image is still being written
+        rs[0].render_async_host(s, 1, mode="ellipse")
+    with pytest.raises(RuntimeError):
+        rs[0].render_async(s, 1, mode="ellipse")
+    assert rs[0].wait()["image"].shape == (136, 200, 3)
     got = {}
     render_views(rs, s, views, on_frame=lambda i, out: got.__setitem__(i, out), mode="ellipse", exact=True)
     assert sorted(got) == list(range(len(views)))
