@@ -135,6 +135,17 @@ def test_render_config3_full_size_vs_reference(ctx, ref, mode, pairs):
     assert psnr(fast, oimg) >= IMG_MIN_PSNR
 
 
+@pytest.mark.parametrize("mode,fixed,pairs", [("aabb", 1, 27_942_602), ("ellipse", 0, 24_572_513)])
+def test_render_config2_full_size_vs_reference(ctx, ref, mode, fixed, pairs):
+    """Config 2 (veil 1M, 4608x3456): the original 3D-GS baseline (AABB with
+    fixed_radius_aabb, r = 3) and Ellipse against the reference build itself:
+    per-Gaussian tile counts, sorted keys and ranges bit-exact, the glibc-exact
+    image bit-identical; pair totals as SURVEY.md §8(d) measured them."""
+    oscene, dev = scene_pair(ref, ctx, 1, 1_000_000, "veil", 16, 4608, 3456, 3600.0)
+    out, _ = check_frame(ctx, ref, oscene, dev, 0, mode, exact=True, fixed_radius_aabb=fixed)
+    assert out["pair_count"] == pairs
+
+
 def test_fast_alpha_within_tolerance(ctx, port):
     oscene, dev = scene_pair(port, ctx, 9, 4000, "veil", 2, 480, 320, 375.0)
     check_frame(ctx, port, oscene, dev, 0, "ellipse", exact=False)
