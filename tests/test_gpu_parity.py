@@ -146,6 +146,17 @@ def test_render_config2_full_size_vs_reference(ctx, ref, mode, fixed, pairs):
     assert out["pair_count"] == pairs
 
 
+def test_render_config4_left_eye_vs_reference(ctx, ref):
+    """Config 4 (veil 3M, one 3660x3200 eye, AdaGScale with K scaled to
+    fx = 2859.375) against the reference build: tile counts, sorted keys,
+    ranges and the glibc-exact image bit-exact; 4,125,726 pairs."""
+    fx = 500.0 * 3660 / 640.0
+    k = float(np.float32(K1080 * (fx / 1500.0) ** 2))
+    oscene, dev = scene_pair(ref, ctx, 1, 3_000_000, "veil", 16, 3660, 3200, fx)
+    out, _ = check_frame(ctx, ref, oscene, dev, 0, "adagscale", k=k, lut_bins=LUT_BINS, exact=True)
+    assert out["pair_count"] == 4_125_726
+
+
 def test_fast_alpha_within_tolerance(ctx, port):
     oscene, dev = scene_pair(port, ctx, 9, 4000, "veil", 2, 480, 320, 375.0)
     check_frame(ctx, port, oscene, dev, 0, "ellipse", exact=False)
