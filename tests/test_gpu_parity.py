@@ -157,6 +157,15 @@ def test_render_config4_left_eye_vs_reference(ctx, ref):
     assert out["pair_count"] == 4_125_726
 
 
+@pytest.mark.parametrize("view", [0, 37])
+def test_render_config5_views_vs_reference(ctx, ref, view):
+    """Config 5 (veil 6M, 4608x3456, a 64-view path): views of the path against
+    the reference build, tile counts / keys / ranges / exact image bit-exact."""
+    k = float(np.float32(K1080 * (3600.0 / 1500.0) ** 2))
+    oscene, dev = scene_pair(ref, ctx, 1, 6_000_000, "veil", 64, 4608, 3456, 3600.0)
+    check_frame(ctx, ref, oscene, dev, view, "adagscale", k=k, lut_bins=LUT_BINS, exact=True)
+
+
 def test_fast_alpha_within_tolerance(ctx, port):
     oscene, dev = scene_pair(port, ctx, 9, 4000, "veil", 2, 480, 320, 375.0)
     check_frame(ctx, port, oscene, dev, 0, "ellipse", exact=False)
