@@ -111,7 +111,7 @@ struct agsx_ctx {
     float* f_band_host = nullptr;  // page-locked host image filled by banded copies behind the raster
     cudaStream_t copy_stream = nullptr;
     static constexpr int kBands = 8;       // egress bands with one raster launch per band (fallback)
-    static constexpr int kFlagBands = 16;  // egress bands of the one-launch path (Counters::band_done)
+    static constexpr int kFlagBands = 32;  // egress row slots of the one-launch path (Counters::band_done)
     cudaEvent_t band_ev[kBands] = {};
     cudaEvent_t copy_done = nullptr;
     cudaEvent_t ev_zeroed = nullptr;  // the frame's counters are zeroed (band flags valid from here)

@@ -355,17 +355,17 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     const char* eg = std::getenv("AGSX_EGRESS");
     const bool flags = banded && wait_value32() && !(eg && std::strcmp(eg, "launches") == 0);
     if (flags) {
-        // banded egress, one raster launch: the tile rows form 16 slots and
+        // banded egress, one raster launch: the tile rows form 32 slots and
         // every unit adds itself to its slot's count once its pixels are
         // stored; the copy stream waits for the counts (cuStreamWaitValue32)
         // and copies finished rows to the page-locked host image while later
-        // rows render.  f32 frames: slots are copied in groups 1, 2, 5, 8 --
+        // rows render.  f32 frames: slots are copied in groups 1, 4, 19, 8 --
         // the raster runs ~4.6x faster than PCIe, so each group is done
-        // before the previous copy ends, the first copy starts after 1/16 of
+        // before the previous copy ends, the first copy starts after 1/32 of
         // the raster and a frame costs 4 copies (each costs ~8 us of PCIe
-        // setup).  PPM bytes: PCIe is about as fast as the raster, so every
-        // slot is its own copy and the last copy is short.  The raster also
-        // writes the PPM bytes; only those are copied.
+        // setup).  PPM bytes: PCIe is about as fast as the raster, so slots
+        // go in pairs and the last copy is short.  The raster also writes the
+        // PPM bytes; only those are copied.
         const int S = std::min(agsx_ctx::kFlagBands, p.tiles_y);
         const int rows_per = (p.tiles_y + S - 1) / S;
         uint8_t* u8 = ctx->f_band_host_u8 ? ptr<uint8_t>(ctx->img_u8) : nullptr;
@@ -375,10 +375,10 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         check_launch(ctx);
         AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
         AGSX_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_zeroed, 0));  // not last frame's counts
-        static const int kF32Groups[] = {1, 3, 8, 16};  // slot group ends for f32 frames
+        static const int kF32Groups[] = {1, 5, 24, 32};  // slot group ends (of 32) for f32 frames
         int s0 = 0;
         for (int gi = 0; s0 * rows_per < p.tiles_y; ++gi) {
-            const int s1 = u8 ? s0 + 1 : std::min(S, std::max(s0 + 1, kF32Groups[std::min(gi, 3)] * S / 16));
+            const int s1 = u8 ? std::min(S, s0 + 2) : std::min(S, std::max(s0 + 1, kF32Groups[std::min(gi, 3)] * S / 32));
             for (int sl = s0; sl < s1; ++sl) {
                 const int r0 = sl * rows_per, r1 = std::min(p.tiles_y, r0 + rows_per);
                 if (r0 >= r1) break;

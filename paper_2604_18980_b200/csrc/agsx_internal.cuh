@@ -478,7 +478,7 @@ struct Counters {
     unsigned long long dbg[8];  // raster work counters (AGSX_RASTER_STATS=1)
     uint32_t kmin_c;  // ~(min depth key of the splats with >= 1 tile), by atomicMax (0 = none)
     uint32_t kmax;    // max depth key of those splats
-    uint32_t band_done[16];  // units finished per egress band (banded host egress)
+    uint32_t band_done[32];  // units finished per egress row slot (banded host egress)
 };
 
 // The depth keys of a frame span >= 2^24 (key - kmin needs a 4th 8-bit
