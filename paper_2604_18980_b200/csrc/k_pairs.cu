@@ -46,8 +46,7 @@ __device__ __forceinline__ TileTest planes_tile_test(const FrameParams& p, const
 // from its P3 hit record (mask) or, for spans over 64 tiles, by re-running
 // the tile test.
 template <class F>
-__device__ __forceinline__ void emit_hits(const FrameParams& p, const SplatPlanes& pl, uint32_t g, F&& f) {
-    const uint4 r = reinterpret_cast<const uint4*>(pl.p3)[g];
+__device__ __forceinline__ void emit_hits_rec(const FrameParams& p, const SplatPlanes& pl, uint32_t g, uint4 r, F&& f) {
     if (r.w != kHitsRecompute) {
         unsigned long long mask = static_cast<unsigned long long>(r.x) | (static_cast<unsigned long long>(r.y) << 32);
         const int tx0 = static_cast<int>(r.z & 0xffffu), ty0 = static_cast<int>(r.z >> 16);
@@ -61,6 +60,11 @@ __device__ __forceinline__ void emit_hits(const FrameParams& p, const SplatPlane
     }
     const TileTest t = planes_tile_test(p, pl, g);
     for_each_tile_hit(t, p, f);
+}
+
+template <class F>
+__device__ __forceinline__ void emit_hits(const FrameParams& p, const SplatPlanes& pl, uint32_t g, F&& f) {
+    emit_hits_rec(p, pl, g, reinterpret_cast<const uint4*>(pl.p3)[g], f);
 }
 
 // Exclusive scan of the per-chunk sums of tile counts (chunk = 256 splats
@@ -127,17 +131,34 @@ k_emit(FrameParams p, const uint32_t* __restrict__ order_wide, const uint32_t* _
     __shared__ uint32_t s_warp[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t m = ctr->m;
-    if (ctr->p_eff == 0u) return;
+    if (ctr->p_eff == 0u) return;  // nothing fits (overflow: the host grows the arena and re-runs)
     // the depth order is in the buffer of the last sort pass that ran
-    const uint32_t* __restrict__ order = depth_keys_wide(ctr->kmin_c, ctr->kmax) ? order_wide : order_narrow;  // nothing fits (overflow: the host grows the arena and re-runs)
+    const uint32_t* __restrict__ order = depth_keys_wide(ctr->kmin_c, ctr->kmax) ? order_wide : order_narrow;
     const uint32_t nchunks = (m + 255u) / 256u;
-    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        const uint32_t j = c * 256u + tid;
-        uint32_t g = 0, cnt = 0;
-        if (j < m) {
-            g = order[j];
-            cnt = counts_sorted[j];
+    // chunks are software-pipelined: the depth order and counts of the chunk
+    // after next and the P3 records of the next chunk are in flight while a
+    // chunk emits (its gathers are otherwise exposed per chunk)
+    const uint4* __restrict__ p3 = reinterpret_cast<const uint4*>(pl.p3);
+    auto load = [&](uint32_t cc, uint32_t& gg, uint32_t& nn) {
+        const uint32_t jj = cc * 256u + tid;
+        gg = 0;
+        nn = 0;
+        if (cc < nchunks && jj < m) {
+            gg = order[jj];
+            nn = counts_sorted[jj];
         }
+    };
+    uint32_t g_n, cnt_n, g_nn, cnt_nn;
+    load(blockIdx.x, g_n, cnt_n);
+    uint4 rec_n = cnt_n ? p3[g_n] : make_uint4(0u, 0u, 0u, 0u);
+    load(blockIdx.x + gridDim.x, g_nn, cnt_nn);
+    for (uint32_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const uint32_t g = g_n, cnt = cnt_n;
+        const uint4 rec = rec_n;
+        g_n = g_nn;
+        cnt_n = cnt_nn;
+        rec_n = cnt_n ? p3[g_n] : make_uint4(0u, 0u, 0u, 0u);
+        load(c + 2 * gridDim.x, g_nn, cnt_nn);
         uint32_t incl = cnt;
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
@@ -157,7 +178,7 @@ k_emit(FrameParams p, const uint32_t* __restrict__ order_wide, const uint32_t* _
         const bool staged = total <= static_cast<uint32_t>(kStage);
         if (cnt) {
             uint32_t at = local;
-            emit_hits(p, pl, g, [&](int tx, int ty) {
+            emit_hits_rec(p, pl, g, rec, [&](int tx, int ty) {
                 const uint32_t tile = static_cast<uint32_t>(ty * p.tiles_x + tx);
                 if (staged) {
                     s_tile[at] = tile;
