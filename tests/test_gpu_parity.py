@@ -610,6 +610,37 @@ def test_contributions_match_oracle(ctx, port, layout, mode, ts):
     assert rc == 5 and count.value == len(want)
 
 
+@pytest.mark.parametrize("env", ["AGSX_RASTER_STATS=1", "AGSX_RASTER_RECT=1"])
+def test_raster_diagnostic_variants(tmp_path, env):
+    """The diagnostic rasterizer variants (work counters; fp64 rectangle cull)
+    render the same frame as the default one (counters: iterations and live
+    evaluations reported, every fast blend counted once)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, '.'); import paper_2604_18980_b200 as P\n"
+        "s = P.synth_scene(3, 20000, 'veil', cameras=2, width=320, height=240, focal=250.0)\n"
+        "r = P.Renderer(0); r.render_async(s, 1, 'adagscale', 0.3, [0.7] * 20); r.wait()\n"
+        "img = P.render(s, 1, 'adagscale', 0.3, [0.7] * 20)['image']\n"
+        "np.save(sys.argv[1], img); st = r.frame_stats()\n"
+        "print(st['raster_iters'], st['raster_evals'], st['raster_fast'])\n")
+    root = os.path.dirname(os.path.dirname(__file__))
+    base = subprocess.run([sys.executable, "-c", code, str(tmp_path / "a.npy")], cwd=root, check=True,
+                          capture_output=True, text=True)
+    k, v = env.split("=")
+    var = subprocess.run([sys.executable, "-c", code, str(tmp_path / "b.npy")], cwd=root, check=True,
+                         capture_output=True, text=True, env={**os.environ, k: v})
+    a, b = np.load(tmp_path / "a.npy"), np.load(tmp_path / "b.npy")
+    if k == "AGSX_RASTER_STATS":
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+        it, ev, fast = (int(x) for x in var.stdout.split())
+        assert it > 0 and ev > 0 and 0 < fast <= ev
+        assert base.stdout.split() == ["0", "0", "0"]  # counters off by default
+    else:  # the rect cull only drops splats that reach no pixel centre: same alpha >= tau decisions
+        assert np.max(np.abs(a - b)) <= 1e-4
+
+
 def test_psnr_device_matches_reference_formula():
     import torch
 
