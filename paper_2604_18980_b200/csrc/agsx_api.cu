@@ -374,7 +374,14 @@ int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n) {
     return guarded(ctx, [&]() -> int {
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         const Counters c = *ctx->h_ctr;
-        const uint64_t v[14] = {c.s, c.m, c.p, c.p_it, c.overflow, static_cast<uint64_t>(ctx->f_tile_count),
+        uint64_t p_it = c.p_it;
+        if (ctx->f_pit_tiles && ctx->f_tile_count > 0) {  // the units rasterizer keeps P_it per tile
+            std::vector<unsigned long long> w(static_cast<size_t>(ctx->f_tile_count));
+            AGSX_CUDA(cudaMemcpy(w.data(), ctx->tile_pit.p, w.size() * 8, cudaMemcpyDeviceToHost));
+            p_it = 0;
+            for (const unsigned long long x : w) p_it += static_cast<uint32_t>(x);
+        }
+        const uint64_t v[14] = {c.s, c.m, c.p, p_it, c.overflow, static_cast<uint64_t>(ctx->f_tile_count),
                                 c.dbg[0], c.dbg[1], c.dbg[2], c.dbg[3], c.dbg[4], c.dbg[5], c.dbg[6], c.dbg[7]};
         for (int i = 0; i < n && i < 14; ++i) stats[i] = v[i];
         return AGSX_OK;

@@ -118,6 +118,7 @@ struct agsx_ctx {
     uint32_t* f_tkeys = nullptr;
     uint32_t* f_pvals = nullptr;
     int f_tile_count = 0;
+    bool f_pit_tiles = false;  // P_it lives in the per-tile words (units rasterizer), not Counters::p_it
 };
 
 namespace agsx::host {

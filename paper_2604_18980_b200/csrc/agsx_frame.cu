@@ -461,6 +461,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     ctx->f_tkeys = tk[cur];
     ctx->f_pvals = pv[cur];
     ctx->f_tile_count = static_cast<int>(tiles);
+    ctx->f_pit_tiles = raster_uses_units(p, maxt);
 }
 
 int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, const agsx_config* cfg,

@@ -576,22 +576,11 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
 
         // P_it (rasterizer.cpp:55-56): per unit n if any pixel stays
         // unsaturated, else the 1-based index of the saturating pair; per
-        // tile the max over both units.  Word = (units done << 32) | max.
-        // (an empty tile contributes 0 from both units: no word to combine)
+        // tile the max over both units, by a fire-and-forget atomicMax on
+        // the tile's word (summed over the tiles when the stats are read).
         if (lane == 0 && pit && end > start) {
             const uint32_t mine = h <= 0 ? 0u : (all_done ? death : end - start);
-            unsigned long long* wp = &tile_pit[tile];
-            unsigned long long old = 0ull;  // guess "first unit of the tile": one CAS round trip when right
-            while (true) {
-                const uint32_t mx = static_cast<uint32_t>(old) > mine ? static_cast<uint32_t>(old) : mine;
-                const unsigned long long r = atomicCAS(wp, old, (((old >> 32) + 1ull) << 32) | mx);
-                if (r == old) break;
-                old = r;
-            }
-            if ((old >> 32) == 1ull) {  // second unit of the tile: publish the tile's max
-                const uint32_t mx = static_cast<uint32_t>(old) > mine ? static_cast<uint32_t>(old) : mine;
-                if (mx) atomicAdd(pit, static_cast<unsigned long long>(mx));
-            }
+            if (mine) atomicMax(reinterpret_cast<unsigned int*>(&tile_pit[tile]), mine);
         }
 
         // store: stage the unit in shared memory, then whole rows (float4)
