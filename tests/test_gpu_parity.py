@@ -100,12 +100,29 @@ def check_frame(ctx, port, oscene, dev, view, mode, k=0.0, lut_bins=None, exact=
     return out, oimg
 
 
+def check_default_image(ctx, dev, ocam, mode, k, bins, oimg, pairs, **kw):
+    """The default (fast, k_raster_units) image of the same frame against the
+    oracle's image: max abs <= 1e-3 per channel, PSNR >= 50 dB."""
+    out = ctx.render(dev, to_gpu_cam(ocam), gpu_cfg(mode, k, **kw), capi.make_lut(bins) if bins else
+                     (capi.make_lut() if mode == "adagscale" else None))
+    assert out["pair_count"] == pairs
+    fast = out["image"]
+    assert np.max(np.abs(fast - oimg)) <= IMG_MAX_ABS
+    assert psnr(fast, oimg) >= IMG_MIN_PSNR
+    return out
+
+
 # --------------------------------------------------------------------------- full pipeline
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "default"])
 @pytest.mark.parametrize("layout", ["slab", "two_slab", "veil", "ramp", "aniso"])
 @pytest.mark.parametrize("mode", ["aabb", "obb", "ellipse", "adagscale"])
-def test_render_matches_oracle_small(ctx, port, layout, mode):
+def test_render_matches_oracle_small(ctx, port, layout, mode, exact):
+    """The mode x layout matrix on both rasterisers: the glibc-exact one
+    (bit-identical image) and the default fast one (k_raster_units, the path
+    users and the bench run: max abs <= 1e-3, PSNR >= 50 dB)."""
     oscene, dev = scene_pair(port, ctx, 5, 3000, layout, 3, 320, 240, 250.0)
-    check_frame(ctx, port, oscene, dev, 1, mode, k=0.3, lut_bins=[0.6] * 20 if mode == "adagscale" else None)
+    check_frame(ctx, port, oscene, dev, 1, mode, k=0.3, lut_bins=[0.6] * 20 if mode == "adagscale" else None,
+                exact=exact)
 
 
 @pytest.mark.parametrize("exact", [True, False])
@@ -129,10 +146,7 @@ def test_render_config3_full_size_vs_reference(ctx, ref, mode, pairs):
     out, oimg = check_frame(ctx, ref, oscene, dev, 0, mode, k=k if mode == "adagscale" else 0.0, lut_bins=bins,
                             exact=True)
     assert out["pair_count"] == pairs  # SURVEY.md §8(a) [measured] on the reference
-    fast = ctx.render(dev, to_gpu_cam(oscene.cameras[0]), gpu_cfg(mode, k if mode == "adagscale" else 0.0),
-                      capi.make_lut(bins) if bins else None)["image"]
-    assert np.max(np.abs(fast - oimg)) <= IMG_MAX_ABS
-    assert psnr(fast, oimg) >= IMG_MIN_PSNR
+    check_default_image(ctx, dev, oscene.cameras[0], mode, k if mode == "adagscale" else 0.0, bins, oimg, pairs)
 
 
 @pytest.mark.parametrize("mode,fixed,pairs", [("aabb", 1, 27_942_602), ("ellipse", 0, 24_572_513)])
@@ -142,8 +156,9 @@ def test_render_config2_full_size_vs_reference(ctx, ref, mode, fixed, pairs):
     per-Gaussian tile counts, sorted keys and ranges bit-exact, the glibc-exact
     image bit-identical; pair totals as SURVEY.md §8(d) measured them."""
     oscene, dev = scene_pair(ref, ctx, 1, 1_000_000, "veil", 16, 4608, 3456, 3600.0)
-    out, _ = check_frame(ctx, ref, oscene, dev, 0, mode, exact=True, fixed_radius_aabb=fixed)
+    out, oimg = check_frame(ctx, ref, oscene, dev, 0, mode, exact=True, fixed_radius_aabb=fixed)
     assert out["pair_count"] == pairs
+    check_default_image(ctx, dev, oscene.cameras[0], mode, 0.0, None, oimg, pairs, fixed_radius_aabb=fixed)
 
 
 def test_render_config4_left_eye_vs_reference(ctx, ref):
@@ -153,8 +168,9 @@ def test_render_config4_left_eye_vs_reference(ctx, ref):
     fx = 500.0 * 3660 / 640.0
     k = float(np.float32(K1080 * (fx / 1500.0) ** 2))
     oscene, dev = scene_pair(ref, ctx, 1, 3_000_000, "veil", 16, 3660, 3200, fx)
-    out, _ = check_frame(ctx, ref, oscene, dev, 0, "adagscale", k=k, lut_bins=LUT_BINS, exact=True)
+    out, oimg = check_frame(ctx, ref, oscene, dev, 0, "adagscale", k=k, lut_bins=LUT_BINS, exact=True)
     assert out["pair_count"] == 4_125_726
+    check_default_image(ctx, dev, oscene.cameras[0], "adagscale", k, LUT_BINS, oimg, 4_125_726)
 
 
 @pytest.mark.parametrize("view", [0, 37])
@@ -163,7 +179,8 @@ def test_render_config5_views_vs_reference(ctx, ref, view):
     the reference build, tile counts / keys / ranges / exact image bit-exact."""
     k = float(np.float32(K1080 * (3600.0 / 1500.0) ** 2))
     oscene, dev = scene_pair(ref, ctx, 1, 6_000_000, "veil", 64, 4608, 3456, 3600.0)
-    check_frame(ctx, ref, oscene, dev, view, "adagscale", k=k, lut_bins=LUT_BINS, exact=True)
+    out, oimg = check_frame(ctx, ref, oscene, dev, view, "adagscale", k=k, lut_bins=LUT_BINS, exact=True)
+    check_default_image(ctx, dev, oscene.cameras[view], "adagscale", k, LUT_BINS, oimg, out["pair_count"])
 
 
 def test_fast_alpha_within_tolerance(ctx, port):
