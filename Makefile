@@ -20,11 +20,11 @@ CUDA_LIB := /usr/local/cuda/lib64
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 # --fmad=false: the reference path has no FMA contraction.
 NVCCFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 --fmad=false -prec-div=true -prec-sqrt=true \
-             -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills -Iinclude
+             -Xcompiler -fPIC,-ffp-contract=off -Xptxas -warn-spills -Iinclude $(EXTRA_NVCC)
 HOSTFLAGS := -std=gnu++20 -O3 -fPIC -ffp-contract=off -fno-fast-math -Iinclude -I$(CSRC)/host
 
 CU_SRCS  := $(CSRC)/k_preprocess.cu $(CSRC)/k_pairs.cu $(CSRC)/k_sort.cu $(CSRC)/k_raster.cu \
-            $(CSRC)/k_calib.cu $(CSRC)/agsx_frame.cu $(CSRC)/agsx_api.cu $(CSRC)/agsx_stage_api.cu
+            $(CSRC)/k_calib.cu $(CSRC)/k_bucket.cu $(CSRC)/agsx_frame.cu $(CSRC)/agsx_api.cu $(CSRC)/agsx_stage_api.cu
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 CU_HDRS  := $(wildcard $(CSRC)/*.cuh) include/agsx.h
 

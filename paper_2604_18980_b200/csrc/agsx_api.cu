@@ -49,6 +49,8 @@ int agsx_create(int device, agsx_ctx** out) {
         ctx->occ_sort32 = std::max(ctx->occ_sort32, 1);
         ctx->occ_sort64 = std::max(ctx->occ_sort64, 1);
         ctx->occ_emit = std::max(ctx->occ_emit, 1);
+        AGSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->occ_tile_sort, k_tile_sort, 256, 0));
+        ctx->occ_tile_sort = std::max(ctx->occ_tile_sort, 1);
         for (auto& set : ctx->ev_ring)
             for (auto& e : set) AGSX_CUDA(cudaEventCreate(&e));
         AGSX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ctr), sizeof(Counters)));
@@ -73,7 +75,7 @@ void agsx_destroy(agsx_ctx* ctx) {
                    &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->dcounts, &ctx->chunks, &ctx->img_u8, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
                    &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
                    &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tile_pit, &ctx->calib, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
-                   &ctx->tmp3, &ctx->tmp4})
+                   &ctx->tmp3, &ctx->tmp4, &ctx->bk_hits, &ctx->bk_gd, &ctx->ekeys, &ctx->ekeys2, &ctx->big_list})
         release(*b);
     for (auto& set : ctx->ev_ring)
         for (auto& e : set)
@@ -425,6 +427,24 @@ int agsx_dump_sorted_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* gids, uint64
         if (out_count) *out_count = P;
         if (P > capacity) return fail(ctx, AGSX_ECAPACITY, "buffer too small");
         const uint64_t n = ctx->f_scene->n;
+        if (ctx->f_bucket) {
+            // tile ids from the ranges, depths from the {gid, depth} list
+            const uint64_t T = static_cast<uint64_t>(ctx->f_tile_count);
+            std::vector<uint2> rg(T);
+            std::vector<uint2> gd(c.m);
+            std::vector<uint32_t> pv(P);
+            if (T) AGSX_CUDA(cudaMemcpy(rg.data(), ctx->ranges.p, T * 8, cudaMemcpyDeviceToHost));
+            if (c.m) AGSX_CUDA(cudaMemcpy(gd.data(), ctx->bk_gd.p, c.m * 8, cudaMemcpyDeviceToHost));
+            if (P) AGSX_CUDA(cudaMemcpy(pv.data(), ctx->f_pvals, P * 4, cudaMemcpyDeviceToHost));
+            std::vector<uint32_t> depth_by_gid(n, 0);
+            for (const uint2& e : gd) depth_by_gid[e.x] = e.y;
+            for (uint64_t t = 0; t < T; ++t)
+                for (uint32_t i = rg[t].x; i < rg[t].y && i < P; ++i) {
+                    if (keys) keys[i] = (t << 32) | depth_by_gid[pv[i]];
+                    if (gids) gids[i] = pv[i];
+                }
+            return AGSX_OK;
+        }
         std::vector<uint32_t> dk(c.m), dv(c.m), tk(P), pv(P);
         if (c.m) {
             const bool wide = depth_keys_wide_host(c);  // which ping-pong buffer holds the depth order

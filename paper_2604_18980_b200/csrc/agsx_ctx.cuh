@@ -75,7 +75,7 @@ struct agsx_ctx {
     uint64_t launches = 0;
     uint32_t epoch = 1;
     int num_sms = 148;
-    int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1, occ_emit_big = 1, occ_raster = 1;
+    int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1, occ_emit_big = 1, occ_raster = 1, occ_tile_sort = 1;
     double pairs_per_splat = 0.0;  // previous frame's P / M (picks the emit stage)
     Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
@@ -84,6 +84,7 @@ struct agsx_ctx {
     Buf tkeys, pvals, tkeys2, pvals2;
     Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext, tile_pit, calib;
     Buf tmp0, tmp1, tmp2, tmp3, tmp4;
+    Buf bk_hits, bk_gd, ekeys, ekeys2, big_list;  // tile-bucketed sort path
     uint64_t pair_capacity = 0;
 
     Counters* h_ctr = nullptr;  // pinned
@@ -118,6 +119,7 @@ struct agsx_ctx {
     uint32_t* f_tkeys = nullptr;
     uint32_t* f_pvals = nullptr;
     int f_tile_count = 0;
+    bool f_bucket = false;     // the frame used the tile-bucketed sort (k_bucket.cu)
     bool f_pit_tiles = false;  // P_it lives in the per-tile words (units rasterizer), not Counters::p_it
 };
 

@@ -140,6 +140,23 @@ size_t sort_smem(bool k64) {
 }
 
 size_t counters_bytes() { return sizeof(Counters); }
+// The bucketed path's tile histogram lives right behind the counters, so one
+// memset per frame zeroes both.
+size_t tile_cnt_offset() { return (sizeof(Counters) + 255) / 256 * 256; }
+uint32_t* tile_cnt_of(agsx_ctx* ctx) {
+    return reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->ctr.p) + tile_cnt_offset());
+}
+
+// Sort path of a frame: the depth-then-tile radix path (default), or the
+// tile-bucketed path of k_bucket.cu with AGSX_SORT=bucket (bit-identical
+// output; measured slower at config 3).
+bool use_bucket() {
+    static const bool bucket = [] {
+        const char* e = std::getenv("AGSX_SORT");
+        return e && std::strcmp(e, "bucket") == 0;
+    }();
+    return bucket;
+}
 // 256-splat chunks of the depth order (K3 work units)
 uint64_t chunk_slots(uint64_t n) { return std::max<uint64_t>((n + 255) / 256, 1); }
 
@@ -168,17 +185,27 @@ void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pi
     ensure(ctx->chunks, 2 * chunk_slots(n) * 4);
     ensure(ctx->ranges, std::max<uint64_t>(tiles, 1) * 8);
     ensure(ctx->image, std::max<uint64_t>(pixels, 1) * 12);
-    ensure(ctx->ctr, counters_bytes());
+    ensure(ctx->ctr, tile_cnt_offset() + std::max<uint64_t>(tiles, 1) * 4 + 16);
+    if (use_bucket()) {
+        ensure(ctx->bk_hits, std::max<uint64_t>(n, 1) * 16);
+        ensure(ctx->bk_gd, std::max<uint64_t>(n, 1) * 8);
+        ensure(ctx->big_list, std::max<uint64_t>(tiles, 1) * 4);
+    }
     if (ctx->pair_capacity == 0) {
         // first guess: 12 pairs per Gaussian, at most the budget, at least 1M
         ctx->pair_capacity = std::min<uint64_t>(std::max<uint64_t>(12 * n, 1u << 20),
                                                 std::max<uint64_t>(pair_budget, 1));
     }
     const uint64_t cap = ctx->pair_capacity;
-    ensure(ctx->tkeys, cap * 4);
     ensure(ctx->pvals, cap * 4);
-    ensure(ctx->tkeys2, cap * 4);
-    ensure(ctx->pvals2, cap * 4);
+    if (use_bucket()) {
+        ensure(ctx->ekeys, cap * 8);
+        ensure(ctx->ekeys2, cap * 8);
+    } else {
+        ensure(ctx->tkeys, cap * 4);
+        ensure(ctx->tkeys2, cap * 4);
+        ensure(ctx->pvals2, cap * 4);
+    }
     ensure_lb(ctx, std::max(cap, n));
 }
 
@@ -258,6 +285,10 @@ void launch_quantize(agsx_ctx* ctx, const float* src, uint8_t* dst, uint64_t n, 
     }
 }
 
+void enqueue_bucket_sort(agsx_ctx* ctx, const FrameParams& p, const BucketOut& bk);
+void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FrameParams& p, const SplatPlanes& pl);
+void enqueue_raster(agsx_ctx* ctx, const FrameParams& p, bool maxt, uint32_t* vals);
+
 void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bool maxt,
                    agsx_splat_view* dump) {
     const uint64_t n = sc->n;
@@ -267,8 +298,9 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     ctx->ev = ctx->ev_ring[ctx->frames % agsx_ctx::kRing];
     ++ctx->frames;
 
+    const bool bucket = use_bucket();
     AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
-    AGSX_CUDA(cudaMemsetAsync(ctr, 0, counters_bytes(), st));
+    AGSX_CUDA(cudaMemsetAsync(ctr, 0, bucket ? tile_cnt_offset() + tiles * 4 : counters_bytes(), st));
     // the other frame-scoped buffers (ranges, chunk sums, per-tile P_it words)
     // are zeroed by K1 itself, so the kernels form one PDL chain
     const bool units = raster_uses_units(p, maxt);
@@ -278,7 +310,13 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     fz.tile_pit = units ? ptr<unsigned long long>(ctx->tile_pit) : nullptr;
     fz.chunks = ptr<uint32_t>(ctx->chunks);
     fz.n_tiles = static_cast<uint32_t>(tiles);
-    fz.n_chunks = n > 0 ? static_cast<uint32_t>(chunk_slots(n)) : 0u;
+    fz.n_chunks = n > 0 && !bucket ? static_cast<uint32_t>(chunk_slots(n)) : 0u;
+    BucketOut bk;
+    if (bucket) {
+        bk.tile_cnt = tile_cnt_of(ctx);
+        bk.hits = ptr<uint4>(ctx->bk_hits);
+        bk.gd = ptr<uint2>(ctx->bk_gd);
+    }
     if (n == 0) {  // no K1: the raster still reads the (empty) ranges
         AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
         if (units) AGSX_CUDA(cudaMemsetAsync(ctx->tile_pit.p, 0, tiles * 8, st));
@@ -289,10 +327,53 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     if (n > 0) {
         const int grid = static_cast<int>((n + 255) / 256);
         launch_pdl(k_preprocess, dim3(grid), dim3(256), 0, st, p, sc->view(), pl, ptr<uint32_t>(ctx->status),
-                   ptr<uint32_t>(ctx->dkeys), ctr, dump, fz);
+                   ptr<uint32_t>(ctx->dkeys), ctr, dump, fz, bk);
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[1], st));
+    ctx->f_bucket = bucket;
+    if (bucket) {
+        enqueue_bucket_sort(ctx, p, bk);
+    } else {
+        enqueue_depth_sort(ctx, n, tiles, p, pl);
+    }
+    uint32_t* vals = ptr<uint32_t>(ctx->pvals);
+    if (!bucket) vals = ctx->f_pvals;
+    enqueue_raster(ctx, p, maxt, vals);
+}
+
+// Tile-bucketed sort path (k_bucket.cu): K2 tile scan, K3 scatter, K4
+// per-tile sort.  Events: ev[2] after the scan, ev[3] after the scatter,
+// ev[4] after the per-tile sort (stage "pair_gen" = the scatter, "sort" =
+// scan + per-tile sort).
+void enqueue_bucket_sort(agsx_ctx* ctx, const FrameParams& p, const BucketOut& bk) {
+    cudaStream_t st = ctx->stream;
+    Counters* ctr = ptr<Counters>(ctx->ctr);
+    const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
+    const uint32_t T = static_cast<uint32_t>(tiles);
+    const int scan_grid = static_cast<int>((tiles + kTileScanPer - 1) / kTileScanPer);
+    launch_pdl(k_tile_scan, dim3(scan_grid), dim3(1024), 0, st, bk.tile_cnt, ptr<uint2>(ctx->ranges), T, ctr,
+               ctx->pair_capacity, ptr<uint64_t>(ctx->lb), ctx->epoch++, ptr<uint32_t>(ctx->big_list));
+    check_launch(ctx);
+    AGSX_CUDA(cudaEventRecord(ctx->ev[2], st));
+    launch_pdl(k_bucket_scatter, dim3(ctx->num_sms * 8), dim3(256), 0, st, p, planes_of(ctx), bk,
+               static_cast<const Counters*>(ctr), ptr<uint64_t>(ctx->ekeys));
+    check_launch(ctx);
+    AGSX_CUDA(cudaEventRecord(ctx->ev[3], st));
+    launch_pdl(k_tile_sort, dim3(ctx->num_sms * ctx->occ_tile_sort), dim3(256), 0, st, ptr<uint2>(ctx->ranges), T,
+               ptr<uint64_t>(ctx->ekeys), ptr<uint64_t>(ctx->ekeys2), ptr<uint32_t>(ctx->pvals), ctr,
+               static_cast<const uint32_t*>(ptr<uint32_t>(ctx->big_list)));
+    check_launch(ctx);
+    AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
+    ctx->f_tkeys = nullptr;
+    ctx->f_pvals = ptr<uint32_t>(ctx->pvals);
+}
+
+// Depth-then-tile radix path: K4a depth sort of the splats, K3 emission in
+// depth order, K4b stable tile sort, K5 ranges.
+void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FrameParams& p, const SplatPlanes& pl) {
+    cudaStream_t st = ctx->stream;
+    Counters* ctr = ptr<Counters>(ctx->ctr);
     // K4a: stable sort by depth bits (4 x 8-bit, histograms in one read);
     // pass 0 drops the sentinel keys of splats without tiles (the ordered
     // compaction) and sets m.
@@ -350,6 +431,16 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         check_launch(ctx);
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
+    ctx->f_tkeys = tk[cur];
+    ctx->f_pvals = pv[cur];
+}
+
+// K6 and the host egress behind it, then the counter readback.
+void enqueue_raster(agsx_ctx* ctx, const FrameParams& p, bool maxt, uint32_t* vals) {
+    cudaStream_t st = ctx->stream;
+    Counters* ctr = ptr<Counters>(ctx->ctr);
+    const SplatPlanes pl = planes_of(ctx);
+    const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
     // K6
     const bool banded = (ctx->f_band_host || ctx->f_band_host_u8) && raster_uses_units(p, maxt) && p.tiles_y > 0;
     const char* eg = std::getenv("AGSX_EGRESS");
@@ -369,7 +460,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         const int S = std::min(agsx_ctx::kFlagBands, p.tiles_y);
         const int rows_per = (p.tiles_y + S - 1) / S;
         uint8_t* u8 = ctx->f_band_host_u8 ? ptr<uint8_t>(ctx->img_u8) : nullptr;
-        launch_raster_units(ctx->num_sms * ctx->occ_raster, st, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1,
+        launch_raster_units(ctx->num_sms * ctx->occ_raster, st, p, ptr<uint2>(ctx->ranges), vals, pl.p0, pl.p1,
                             pl.p2, ctx->f_image, &ctr->tile_ctr[3], ptr<unsigned long long>(ctx->tile_pit), &ctr->p_it,
                             ctr->dbg, ctr->band_done, rows_per, u8);
         check_launch(ctx);
@@ -420,7 +511,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
             FrameParams pb = p;
             pb.unit_lo = 2u * static_cast<uint32_t>(r0 * p.tiles_x);
             pb.unit_hi = 2u * static_cast<uint32_t>(r1 * p.tiles_x);
-            launch_raster(ctx, pb, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ctx->f_image, nullptr, ctr,
+            launch_raster(ctx, pb, ptr<uint2>(ctx->ranges), vals, pl.p0, pl.p1, pl.p2, ctx->f_image, nullptr, ctr,
                           &ctr->tile_ctr[8 + b]);
             const size_t y0 = static_cast<size_t>(r0) * p.tile_size;
             const size_t y1 = std::min(static_cast<size_t>(r1) * p.tile_size, static_cast<size_t>(p.H));
@@ -447,7 +538,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         AGSX_CUDA(cudaEventRecord(ctx->copy_done, ctx->copy_stream));
         AGSX_CUDA(cudaStreamWaitEvent(st, ctx->copy_done, 0));
     } else {
-        launch_raster(ctx, p, ptr<uint2>(ctx->ranges), pv[cur], pl.p0, pl.p1, pl.p2, ctx->f_image,
+        launch_raster(ctx, p, ptr<uint2>(ctx->ranges), vals, pl.p0, pl.p1, pl.p2, ctx->f_image,
                       maxt ? ptr<uint32_t>(ctx->maxt) : nullptr, ctr);
         AGSX_CUDA(cudaEventRecord(ctx->ev[5], st));
     }
@@ -458,8 +549,6 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     k_counters_out<<<1, 64, 0, st>>>(reinterpret_cast<const uint32_t*>(ctr), ctx->h_ctr_dev,
                                      static_cast<int>(sizeof(Counters) / 4));
     check_launch(ctx);
-    ctx->f_tkeys = tk[cur];
-    ctx->f_pvals = pv[cur];
     ctx->f_tile_count = static_cast<int>(tiles);
     ctx->f_pit_tiles = raster_uses_units(p, maxt);
 }

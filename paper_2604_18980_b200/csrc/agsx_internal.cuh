@@ -317,6 +317,30 @@ __device__ __forceinline__ uint4 hit_record(const TileTest& t, const FrameParams
     return make_uint4(__float_as_uint(t.rx), __float_as_uint(t.ry), __float_as_uint(t.r2), kHitsRecompute);
 }
 
+// Calls f(tx, ty) for the intersected tiles of a splat in row-major order
+// from its hit record r (mask), or by re-running the test t for spans over
+// 64 tiles.
+template <class F>
+__device__ __forceinline__ void hit_tiles(const TileTest& t, const FrameParams& p, uint4 r, F&& f) {
+    if (r.w != kHitsRecompute) {
+        unsigned long long mask = static_cast<unsigned long long>(r.x) | (static_cast<unsigned long long>(r.y) << 32);
+        const int tx0 = static_cast<int>(r.z & 0xffffu), ty0 = static_cast<int>(r.z >> 16);
+        const int sw = static_cast<int>(r.w);
+        int row = 0, row_end = sw;  // bits arrive in increasing order: track the row, no division
+        while (mask) {
+            const int b = __ffsll(static_cast<long long>(mask)) - 1;
+            mask &= mask - 1;
+            while (b >= row_end) {
+                ++row;
+                row_end += sw;
+            }
+            f(tx0 + b - (row_end - sw), ty0 + row);
+        }
+        return;
+    }
+    for_each_tile_hit(t, p, f);
+}
+
 // Blend-side culling data for the rasterizer (not part of the reference; it
 // only lets the rasterizer skip, or take a fast path for, pixels whose
 // decision alpha >= tau is provable with a margin).  In

@@ -38,7 +38,7 @@ int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_came
         if (n) {
             k_preprocess<<<static_cast<int>((n + 255) / 256), 256, 0, ctx->stream>>>(
                 p, scene->view(), planes_of(ctx), ptr<uint32_t>(ctx->status), ptr<uint32_t>(ctx->dkeys), ctr,
-                ptr<agsx_splat_view>(ctx->dump), FrameZero{});
+                ptr<agsx_splat_view>(ctx->dump), FrameZero{}, BucketOut{});
             check_launch(ctx);
         }
         std::vector<uint32_t> st(n);
@@ -260,10 +260,13 @@ int agsx_fold_max_t(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* c
         uint32_t* dfold = ptr<uint32_t>(ctx->calib);
         AGSX_CUDA(cudaMemsetAsync(dfold, 0, static_cast<size_t>(2 * nb) * 4, ctx->stream));
         if (scene->n) {
+            // the frame's splats with tiles: {gid, depth} (bucketed path) or
+            // the depth order's ping-pong buffer the device chose
             const bool wide = depth_keys_wide_host(*ctx->h_ctr);  // finish_frame synchronised
+            const uint32_t* gid = ctx->f_bucket ? ptr<uint32_t>(ctx->bk_gd) : ptr<uint32_t>(wide ? ctx->dvals : ctx->dvals2);
+            const uint32_t* dep = ctx->f_bucket ? gid + 1 : ptr<uint32_t>(wide ? ctx->dkeys : ctx->dkeys2);
             k_fold_max_t<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
-                ptr<uint32_t>(wide ? ctx->dvals : ctx->dvals2), ptr<uint32_t>(wide ? ctx->dkeys : ctx->dkeys2),
-                &ptr<Counters>(ctx->ctr)->m,
+                gid, dep, ctx->f_bucket ? 2 : 1, &ptr<Counters>(ctx->ctr)->m,
                 ptr<uint32_t>(ctx->maxt), lut_shape->depth_min, lut_shape->depth_max, nb, dfold, dfold + nb);
             check_launch(ctx);
         }

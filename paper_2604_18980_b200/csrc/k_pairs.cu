@@ -51,10 +51,15 @@ __device__ __forceinline__ void emit_hits_rec(const FrameParams& p, const SplatP
         unsigned long long mask = static_cast<unsigned long long>(r.x) | (static_cast<unsigned long long>(r.y) << 32);
         const int tx0 = static_cast<int>(r.z & 0xffffu), ty0 = static_cast<int>(r.z >> 16);
         const int sw = static_cast<int>(r.w);
+        int row = 0, row_end = sw;  // bits arrive in increasing order: track the row, no division
         while (mask) {
             const int b = __ffsll(static_cast<long long>(mask)) - 1;
             mask &= mask - 1;
-            f(tx0 + b % sw, ty0 + b / sw);
+            while (b >= row_end) {
+                ++row;
+                row_end += sw;
+            }
+            f(tx0 + b - (row_end - sw), ty0 + row);
         }
         return;
     }

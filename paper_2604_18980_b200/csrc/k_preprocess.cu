@@ -85,7 +85,8 @@ __device__ __forceinline__ void eval_color(const DevScene& sc, uint64_t i, float
 
 __global__ void __launch_bounds__(256, AGSX_PRE_MINB)
 k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ status,
-             uint32_t* __restrict__ dkeys, Counters* ctr, agsx_splat_view* __restrict__ dump, FrameZero fz) {
+             uint32_t* __restrict__ dkeys, Counters* ctr, agsx_splat_view* __restrict__ dump, FrameZero fz,
+             BucketOut bk) {
     griddep_wait();
     // frame-scoped zeroing (the previous frame's readers have completed)
     for (uint64_t z = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; z < fz.n_tiles || z < fz.n_chunks;
@@ -101,6 +102,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
 
     bool alive = false, keep = false;
     float depth = 0.0f;
+    uint4 hit_rec = make_uint4(0u, 0u, 0u, 0u);
     if (i < sc.n) {
         const float4 po = sc.pos_op[i];
         const float4 q = sc.rot[i];
@@ -214,6 +216,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
             const float ixx = cyy * inv_det, ixy = -cxy * inv_det, iyy = cxx * inv_det;
             const TileTest tt = make_tile_test(m2x, m2y, cxx, cxy, cyy, ixx, ixy, iyy, opacity, th, p);
             const uint4 hits = hit_record(tt, p, cnt);
+            hit_rec = hits;
             keep = cnt > 0;
             float rgb[3] = {0.5f, 0.5f, 0.5f};
             if (keep || dump) {
@@ -234,8 +237,15 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
                 pl.p0[i] = make_float4(m2x, m2y, ixx, 2.0f * ixy);
                 pl.p1[i] = make_float4(iyy, opacity, qcut, qsafe);
                 pl.p2[i] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(pack_extent(ex, ey)));
-                reinterpret_cast<uint4*>(pl.p3)[i] = hits;
                 if (p.mode == AGSX_MODE_OBB) pl.p4[i] = make_float4(tt.v1x, tt.v1y, tt.a, tt.b);
+                if (bk.tile_cnt) {
+                    // tile histogram of the bucketed sort: one reduction per hit tile
+                    hit_tiles(tt, p, hits, [&](int tx, int ty) {
+                        atomicAdd(&bk.tile_cnt[static_cast<uint32_t>(ty * p.tiles_x + tx)], 1u);
+                    });
+                } else {
+                    reinterpret_cast<uint4*>(pl.p3)[i] = hits;
+                }
             }
             if (dump) {
                 agsx_splat_view v;
@@ -260,6 +270,22 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         status[i] = cnt | (alive ? kAliveBit : 0u);
     }
 
+    if (bk.tile_cnt) {
+        // compact list of the splats with tiles (order irrelevant: one
+        // atomic per warp), which is also m
+        const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+        uint32_t base = 0;
+        if (lane == 0 && kb) base = atomicAdd(&ctr->m, static_cast<uint32_t>(__popc(kb)));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) {
+            const uint32_t at = base + __popc(kb & ((1u << lane) - 1u));
+            bk.gd[at] = make_uint2(static_cast<uint32_t>(i), __float_as_uint(depth));
+            bk.hits[at] = hit_rec;
+        }
+        const uint32_t alive_cnt = __popc(__ballot_sync(0xffffffffu, alive));
+        if (alive_cnt && lane == 0) atomicAdd(&ctr->s, alive_cnt);
+        return;
+    }
     if (i < sc.n) dkeys[i] = keep ? __float_as_uint(depth) : 0xffffffffu;
     // range of the depth keys (positive floats: bit order = value order), so
     // the depth sort can skip its top digit when the keys span < 2^24.  Per

@@ -40,8 +40,37 @@ struct FrameZero {
     uint32_t* chunks = nullptr;              // chunk sums
     uint32_t n_tiles = 0, n_chunks = 0;
 };
+// Outputs of K1 for the tile-bucketed sort path (all null on the depth-sort
+// path): the per-tile pair histogram (fire-and-forget atomics per hit tile)
+// and a compact list of the splats with >= 1 tile (hit record + {Gaussian
+// id, depth bits}), in no particular order -- the per-tile sort makes the
+// final order deterministic.
+struct BucketOut {
+    uint32_t* tile_cnt = nullptr;  // tiles; zeroed before K1
+    uint4* hits = nullptr;         // P3 hit record per listed splat
+    uint2* gd = nullptr;           // {gid, depth bits} per listed splat
+};
 __global__ void k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* status,
-                             uint32_t* dkeys, Counters* ctr, agsx_splat_view* dump, FrameZero fz);
+                             uint32_t* dkeys, Counters* ctr, agsx_splat_view* dump, FrameZero fz, BucketOut bk);
+
+// ---- tile-bucketed sort path (k_bucket.cu) ------------------------------
+// K2: exclusive scan of the tile histogram (decoupled look-back, 8192 tiles
+// per CTA): ranges, the per-tile end offsets for the scatter (in place of the
+// counts), P / capacity, and the list of tiles above kWarpSortMax pairs.
+constexpr int kWarpSortMax = 256;   // pairs per tile sorted by one warp (keys in registers)
+constexpr int kCtaSortMax = 2048;  // ... by one CTA with the keys in registers / shared memory
+constexpr int kTileScanPer = 8192;  // tiles per scan CTA
+__global__ void k_tile_scan(uint32_t* cnt, uint2* ranges, uint32_t T, Counters* ctr, uint64_t capacity,
+                            uint64_t* lb, uint32_t epoch, uint32_t* big_list);
+// K3: scatter of (depth bits << 32 | gid) into each tile's segment (one
+// returning atomic per pair on the tile's end offset).
+__global__ void k_bucket_scatter(FrameParams p, SplatPlanes pl, BucketOut bk, const Counters* ctr,
+                                 uint64_t* ekeys);
+// K4: per-tile sort of the segment by the 64-bit (depth bits, gid) key --
+// the reference's stable (tile, depth, emission order) order -- and the
+// Gaussian ids of the sorted segment into vals.
+__global__ void k_tile_sort(uint2* ranges, uint32_t T, uint64_t* ekeys, uint64_t* ekeys2, uint32_t* vals,
+                            Counters* ctr, const uint32_t* big_list);
 __global__ void k_pack_scene(uint64_t n, int D, const float* mean, const float* scale,
                              const float* rot, const float* op, const float* sh, float4* pos_op,
                              float4* rotq, float4* scale_r, float2* sh_gb, float* sh_rest);
@@ -123,7 +152,7 @@ cudaError_t launch_raster_records(cudaStream_t st, const FrameParams& p, const u
                                   const float4* P0, const float4* P1, const float4* P2, float* image,
                                   uint32_t* counts, const uint64_t* offsets, agsx_blend_record* out);
 
-__global__ void k_fold_max_t(const uint32_t* order, const uint32_t* dkeys, const uint32_t* m_dev,
+__global__ void k_fold_max_t(const uint32_t* order, const uint32_t* dkeys, int stride, const uint32_t* m_dev,
                              const uint32_t* maxt, float dmin, float dmax, int nbins, uint32_t* folded,
                              uint32_t* observed);
 __global__ void k_sq_err_partial(const float* a, const float* b, uint64_t n, double* partial);
