@@ -37,8 +37,13 @@ PY_INC   := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_paths()['
 PYBIND   := $(shell $(PYTHON) -c "import pybind11;print(pybind11.get_include())")
 CORE     := $(PKG)/_core$(PY_EXT)
 
-all: $(LIBDIR)/libagsx.so $(LIBDIR)/libags.so $(CORE) $(LIBDIR)/render_cli oracle
+all: $(LIBDIR)/libagsx.so $(LIBDIR)/libags.so $(CORE) $(LIBDIR)/render_cli oracle scripts/_build/libcubsort.so
 .PHONY: all oracle clean
+
+# bench-only comparator (bench.py stages.sort.cub): cub::DeviceRadixSort on the same keys
+scripts/_build/libcubsort.so: scripts/cub_sort.cu
+	@mkdir -p scripts/_build
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -shared $< -o $@
 
 build/%.o: $(CSRC)/%.cu $(CU_HDRS)
 	@mkdir -p build
@@ -69,5 +74,5 @@ oracle:
 	@if [ -d /root/reference/proj/src ]; then $(MAKE) -C oracle ref; fi
 
 clean:
-	rm -rf build $(LIBDIR) $(PKG)/_core*.so
+	rm -rf build $(LIBDIR) $(PKG)/_core*.so scripts/_build
 	$(MAKE) -C oracle clean

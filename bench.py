@@ -135,13 +135,56 @@ def measured_peaks() -> dict:
 
 
 # ------------------------------------------------------ algorithmic bytes
-def stage_bytes(n, s, p, p_it, tiles, px):
-    """Algorithmic bytes per frame, SURVEY.md §8(d) (d = 1 SH coefficient)."""
+HBM_SPEC_GBS = 8000.0  # B200 HBM3e spec (BASELINE.md §2-3 reporting convention)
+
+
+def survey_bytes(n, s, p, p_it, tiles, px):
+    """SURVEY.md §8(d)'s per-stage formulas (d = 1 SH coefficient): the
+    reference's own formulation (6 passes of a 64-bit pair sort).  Kept as a
+    labelled comparison only; the roofline uses `moved_bytes`."""
     return {
         "preprocess": n * (44 + 12) + 4 * n + 44 * s,
         "pair_gen": 8 * n + 28 * s + 12 * p,
         "sort": 160 * p + 8 * tiles,
         "raster": 40 * p_it + 8 * tiles + 12 * px,
+    }
+
+
+def moved_bytes(n, m, p, p_it, tiles, px, depth_passes, bucketed):
+    """Bytes each stage's kernels must move in THIS formulation (SH degree 0,
+    n Gaussians, m splats with >= 1 tile, p pairs, tiles, px pixels).
+
+    Depth-then-tile path (default):
+      preprocess  K1 reads the 56 B scene SoA, writes status + depth key (8 B)
+                  per Gaussian and the 64 B P0..P3 planes per splat with tiles,
+                  zeroes ranges / P_it words (16 B per tile);
+      sort        depth pass 0 (upsweep + downsweep read 4 B keys of all n,
+                  8 B key+value written per splat), depth passes 1.. (4 B
+                  upsweep read + 8 B read + 8 B write per splat), the last
+                  pass's tile-count by-product (4 B gather + 4 B write per
+                  splat), 2 tile passes over the pairs (4 + 8 + 8 B each),
+                  the ranges (4 B read per pair, 8 B per tile);
+      pair_gen    K3 reads the depth order, counts and P3 records (24 B per
+                  splat) and writes 8 B per pair;
+      raster      per pair iterated the 4 B value + the 48 B P0/P1/P2 record,
+                  8 B range + 8 B P_it word per tile, the 12 B image pixel.
+    Tile-bucketed path (AGSX_SORT=bucket): K1 adds a 4 B reduction per pair
+    and writes a 24 B list entry per splat instead of P3 + depth key; the
+    scatter reads the list and does a 4 B atomic + 8 B write per pair; the
+    sort reads 8 B and writes 4 B per pair plus the 12 B-per-tile scan."""
+    raster = 52 * p_it + 16 * tiles + 12 * px
+    if bucketed:
+        return {
+            "preprocess": 56 * n + 4 * n + 48 * m + 24 * m + 8 * p + 16 * tiles,
+            "pair_gen": 24 * m + 8 * p + 8 * p,
+            "sort": 12 * tiles + 8 * p + 4 * p,
+            "raster": raster,
+        }
+    return {
+        "preprocess": 56 * n + 8 * n + 64 * m + 16 * tiles,
+        "pair_gen": 24 * m + 8 * p,
+        "sort": (8 * n + 8 * m) + max(depth_passes - 1, 0) * 20 * m + 8 * m + 2 * 20 * p + 4 * p + 8 * tiles,
+        "raster": raster,
     }
 
 
@@ -215,6 +258,60 @@ def _jsonable(o):
     raise TypeError(type(o).__name__)
 
 
+# ------------------------------------------------- CUB sort comparator
+def cub_comparator(r, scene, view, mode, k, bins, exact, iters=20):
+    """cub::DeviceRadixSort::SortPairs (the paper's sort, PAPER.md:44) on this
+    frame's pair set: 64-bit (tile << 32 | depth bits) keys with the Gaussian
+    id as value, bits [0, 32 + ceil(log2 T)), in the reference's emission
+    order (Gaussian id, tiles ascending).  Bench-only (scripts/cub_sort.cu);
+    compared with this pipeline's device-timed sort stage, and its sort +
+    pair_gen stages, on the AdaGScale on and off pair sets."""
+    import torch
+
+    so = os.path.join(ROOT, "scripts", "_build", "libcubsort.so")
+    if not os.path.exists(so):
+        return {"unavailable": "scripts/_build/libcubsort.so not built"}
+    lib = ctypes.CDLL(so)
+    lib.cub_sort_pairs_u64.restype = ctypes.c_int
+    lib.cub_sort_pairs_u64.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
+                                                               ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+    res = {}
+    for label, (md, kk, bb) in (("adagscale_on", (mode, k, bins)), ("adagscale_off", ("ellipse", 0.0, []))):
+        if label == "adagscale_on" and mode != "adagscale":
+            continue
+        for _ in range(5):
+            r.render_async(scene, view, md, kk, bb, exact=exact)
+        r.wait()
+        ours = r.stage_history(5).mean(axis=0)
+        tiles = r.frame_stats()["tiles"]
+        keys, gids = r.dump_sorted_pairs()
+        p = int(len(keys))
+        tb = max(1, int(np.ceil(np.log2(max(tiles, 2)))))
+        kd = torch.from_numpy(keys.view(np.int64)).cuda()
+        gd = torch.from_numpy(gids.astype(np.int64)).cuda()
+        order = torch.sort(gd, stable=True).indices  # emission order: Gaussian id, then tile (stable)
+        kin, vin = kd[order].contiguous(), gd[order].to(torch.int32).contiguous()
+        kout, vout = torch.empty_like(kin), torch.empty_like(vin)
+        ms = ctypes.c_float(0.0)
+        rc = lib.cub_sort_pairs_u64(kin.data_ptr(), vin.data_ptr(), kout.data_ptr(), vout.data_ptr(), p, 0,
+                                    32 + tb, iters, ctypes.byref(ms))
+        torch.cuda.synchronize()
+        same = bool(torch.equal(kout, kd) and torch.equal(vout.to(torch.int64), gd))
+        cub_ms = float(ms.value)
+        res[label] = {
+            "pairs": p, "key_bits": 32 + tb, "rc": rc,
+            "cub_ms": cub_ms, "cub_keys_per_s": p / (cub_ms * 1e-3) if cub_ms > 0 else None,
+            "ours_sort_ms": float(ours[2]), "ours_keys_per_s": p / (float(ours[2]) * 1e-3) if ours[2] > 0 else None,
+            "ours_sort_plus_pair_gen_ms": float(ours[1] + ours[2]),
+            "cub_output_equals_ours": same,
+        }
+        del kd, gd, order, kin, vin, kout, vout
+    # the last frame on the context is the configured one again
+    r.render_async(scene, view, mode, k, bins, exact=exact)
+    r.wait()
+    return res
+
+
 # ------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     os.environ["AGS_DEVICE"] = str(local_rank)  # device of the module-level render()
@@ -233,7 +330,7 @@ def run_ours(args, rank, world, local_rank):
     k = scaled_k(w) if mode == "adagscale" else 0.0
     bins = LUT_BINS if mode == "adagscale" else []
     scene = P.synth_scene(1, n, "veil", cameras=cams, width=w, height=h, focal=focal)
-    from paper_2604_18980_b200.multiview import gather_frames, partition_views, stereo_cameras
+    from paper_2604_18980_b200.multiview import partition_views, stereo_cameras
 
     # Work per rank: configs 1-3 -> rank r renders view r of the
     # camera set (weak scaling); config 4 -> stereo, eye r % 2 of view 0;
@@ -326,33 +423,40 @@ def run_ours(args, rank, world, local_rank):
         del r2
 
     # ---- frames gathered on rank 0 (NCCL over NVLink), N > 1 -----------------
+    # Through multiview.MultiViewRenderer.render_path, the code the gloo
+    # world-2 test runs (tests/test_multiview.py): each rank renders its block
+    # of views into frame slots (on rank 0 its slice of the preallocated path
+    # buffer), the other blocks arrive by point-to-point NCCL transfers in place.
     gather = None
     if dist is not None and not args.no_gather:
-        n_local = max(len(jobs), 1)
-        slots = torch.empty((n_local, h, w, 3), dtype=torch.float32, device="cuda")
+        from paper_2604_18980_b200.multiview import MultiViewRenderer, gpu_render_pipelined
+
+        rg = P.Renderer(local_rank)
+        mv = MultiViewRenderer(batch=gpu_render_pipelined([r, rg]), device=f"cuda:{local_rank}")
+        n_views = cams if args.config == "5" else world
+        kwg = dict(mode=mode, k=k, lut_bins=bins, exact=args.exact)
+        if args.config == "4":
+            kwg["camera"] = eyes[rank % 2]
+        path = torch.empty((n_views, h, w, 3), dtype=torch.float32, device="cuda") if rank == 0 else None
+        mv.render_path(scene, n_views, h, w, dst=0, out=path, **kwg)  # warm-up
         steps_g = max(2, min(args.steps, 10))
-        with torch.cuda.stream(stream):
-            for it in range(steps_g + 1):
-                if it == 1:
-                    barrier()
-                    ev0.record(stream)
-                for i, (v, cam) in enumerate(jobs):
-                    r.render_async_to(scene, v, slots[i].data_ptr(), mode, k, bins, exact=args.exact, camera=cam)
-                if args.config == "5":
-                    gather_frames(slots[: len(jobs)], cams, world, rank, None, 0)
-                else:
-                    gather_frames(slots[: len(jobs)], world, world, rank, None, 0)
-            ev1.record(stream)
-        r.wait()
         barrier()
-        tg = torch.tensor([ev0.elapsed_time(ev1) / steps_g], dtype=torch.float64, device="cuda")
+        t0 = time.perf_counter()
+        for _ in range(steps_g):
+            frames_g, stats_g = mv.render_path(scene, n_views, h, w, dst=0, out=path, **kwg)
+        barrier()
+        tg = torch.tensor([(time.perf_counter() - t0) / steps_g], dtype=torch.float64, device="cuda")
         dist.all_reduce(tg, op=dist.ReduceOp.MAX)
-        gms = float(tg.item())
-        gather = {"fps_with_gather": frames_per_step_total / (gms * 1e-3), "ms_per_step_render_plus_gather": gms,
-                  "ms_per_step_render": max_ms / args.steps,
-                  "bytes_to_rank0_per_step": int((frames_per_step_total - len(jobs)) * h * w * 12),
-                  "how": "frames rasterised into per-rank slots (render_async_to), torch.distributed.gather "
-                         "(NCCL) onto rank 0 each step, CUDA events on the render stream, max over ranks"}
+        gms = float(tg.item()) * 1e3
+        gather = {"fps_with_gather": n_views / (gms * 1e-3), "ms_per_step_render_plus_gather": gms,
+                  "ms_per_step_render": max_ms / args.steps, "views_per_step": n_views,
+                  "pairs_per_step": stats_g.pair_count,
+                  "bytes_to_rank0_per_step": int((n_views - len(partition_views(n_views, world, 0))) * h * w * 12),
+                  "how": "multiview.MultiViewRenderer.render_path over two contexts per rank: frames rasterised "
+                         "into slots (rank 0: its slice of the path buffer), point-to-point NCCL sends into "
+                         "rank 0's path buffer, stats all-reduced; host clock between device-synchronised "
+                         "barriers, max over ranks"}
+        del rg
 
     # ---- end to end through the public API (host image out, per step) ----
     e2e = None
@@ -458,27 +562,40 @@ def run_ours(args, rank, world, local_rank):
     peaks = measured_peaks()
     stage_ms = hist.mean(axis=0) if len(hist) else np.zeros(4)
     tiles = stats["tiles"]
-    sb = stage_bytes(n, stats["splat_count"], stats["pair_count"], stats["p_it"], tiles, w * h)
+    bucketed = bool(stats.get("bucketed_sort", 0))
+    sb = moved_bytes(n, stats["splats_with_tiles"], stats["pair_count"], stats["p_it"], tiles, w * h,
+                     stats.get("depth_passes", 3), bucketed)
+    svb = survey_bytes(n, stats["splat_count"], stats["pair_count"], stats["p_it"], tiles, w * h)
     names = ("preprocess", "pair_gen", "sort", "raster")
     stages = {}
     for i, nm in enumerate(names):
         gbs = sb[nm] / (stage_ms[i] * 1e-3) / 1e9 if stage_ms[i] > 0 else 0.0
+        sgbs = svb[nm] / (stage_ms[i] * 1e-3) / 1e9 if stage_ms[i] > 0 else 0.0
         stages[nm] = {"ms": float(stage_ms[i]), "algorithmic_bytes": int(sb[nm]), "achieved_gbs": gbs,
-                      "frac_hbm": gbs / peaks["hbm_gbs"]}
+                      "frac_hbm": gbs / peaks["hbm_gbs"], "frac_hbm_spec": gbs / HBM_SPEC_GBS,
+                      "survey_formula": {"bytes": int(svb[nm]), "achieved_gbs": sgbs,
+                                         "note": "SURVEY §8(d) bytes of the reference's formulation; not moved "
+                                                 "by these kernels"}}
     stages["sort"]["keys_per_s"] = stats["pair_count"] / (stage_ms[2] * 1e-3) if stage_ms[2] else 0.0
     stages["pair_gen"]["pairs_per_s"] = stats["pair_count"] / (stage_ms[1] * 1e-3) if stage_ms[1] else 0.0
+    bytes_def = ("moved bytes of this formulation (bench.moved_bytes: "
+                 + ("tile-bucketed sort" if bucketed else
+                    f"depth sort of the splats in {stats.get('depth_passes', 3)} passes + 2 tile passes") + ")")
     dom = int(np.argmax(stage_ms))
-    # ncu evidence of the same frame (profiles/ncu_frame.json, one --set full
-    # capture): DRAM bytes and warp instructions per frame per stage
+    # ncu evidence of this workload (profiles/ncu_frame_c<config>_<mode>.json,
+    # one --set full capture of the same frame by scripts/profile_summary.py):
+    # DRAM bytes and warp instructions per frame per stage; absent -> null
+    prof_path = os.path.join(ROOT, "profiles", f"ncu_frame_c{args.config}_{mode}.json")
     prof = {}
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_frame.json")) as f:
-            prof = json.load(f)["per_frame"]
+        with open(prof_path) as f:
+            pdoc = json.load(f)
+        if pdoc.get("sort_path", "depth") == ("bucket" if bucketed else "depth"):
+            prof = pdoc["per_frame"]
     except Exception:
         prof = {}
     for nm in names:
-        if nm in prof:
-            stages[nm]["ncu_dram_bytes"] = prof[nm]["dram_bytes"]
+        stages[nm]["ncu_dram_bytes"] = prof[nm]["dram_bytes"] if nm in prof else None
     props = torch.cuda.get_device_properties(local_rank)
     sm_mhz = clocks.get("sm_mhz") or 1965.0
     issue_peak = props.multi_processor_count * 4 * sm_mhz * 1e6  # warp-instructions / s
@@ -492,6 +609,11 @@ def run_ours(args, rank, world, local_rank):
                 "bound": "issue", "achieved": ach, "peak": issue_peak, "unit": "warp-inst/s", "frac": ach / issue_peak,
                 "warp_inst_per_frame": prof[nm]["warp_inst"],
                 "peak_def": f"{props.multi_processor_count} SMs x 4 SMSPs x 1 warp-inst/clk x {sm_mhz:.0f} MHz"}
+    if not args.no_cub:
+        stages["sort"]["cub"] = cub_comparator(r, scene, view, mode, k, bins, args.exact)
+        if "adagscale_on" in stages["sort"]["cub"] or "adagscale_off" in stages["sort"]["cub"]:
+            c0 = stages["sort"]["cub"].get("adagscale_on") or stages["sort"]["cub"].get("adagscale_off")
+            stages["sort"]["cub_keys_per_s"] = c0["cub_keys_per_s"]
     roofline = {
         "bound": "hbm",
         "kernel": names[dom],
@@ -499,11 +621,13 @@ def run_ours(args, rank, world, local_rank):
         "peak": peaks["hbm_gbs"],
         "unit": "GB/s",
         "frac": stages[names[dom]]["frac_hbm"],
+        "frac_spec_8tbs": stages[names[dom]]["frac_hbm_spec"],
         "traffic": prof.get(names[dom], {}).get("dram_bytes"),
-        "traffic_src": "profiles/ncu_frame.json (dram__bytes_read.sum + dram__bytes_write.sum, one ncu --set full "
-                       "capture of the same frame)" if names[dom] in prof else None,
+        "traffic_src": (os.path.relpath(prof_path, ROOT) + " (dram__bytes_read.sum + dram__bytes_write.sum, one "
+                        "ncu --set full capture of this workload)") if names[dom] in prof else None,
         "peak_src": peaks["src"],
         "algorithmic_bytes_per_launch": stages[names[dom]]["algorithmic_bytes"],
+        "bytes_def": bytes_def,
         "note": "raster is issue-bound (SURVEY §8(d)); HBM fraction reported as asked, issue roofline in "
                 "stages.raster.issue_roofline",
     }
@@ -512,14 +636,14 @@ def run_ours(args, rank, world, local_rank):
     cpu = None
     quality = None
     if not args.no_cpu and world == 1:
-        kind, threads, times, ref_out = cpu_reference(args.config, mode, args.cpu_frames, 0)
-        if times and times[0] is not None:
-            cpu_fps = 1.0 / (sum(times) / len(times))
-        else:
-            cpu_fps = None
+        # median of >= 5 repeats (the reference's cmd_bench convention,
+        # adagscale_main.cpp:343,364-367), stage_times summed per frame
+        kind, threads, times, ref_out = cpu_reference(args.config, mode, max(args.cpu_frames, 5), 1)
+        cpu_fps = 1.0 / statistics.median(times) if times and times[0] is not None else None
         cpu = {"value": cpu_fps, "unit": "frames/s", "cores": threads, "kind": kind,
-               "sample": f"{args.cpu_frames} full frame(s) of the same workload (view 0), reference "
-                         f"render() stage_times summed, {threads} threads"}
+               "sample": f"median of {len(times)} full frames of the same workload (view 0) after 1 warm-up, "
+                         f"reference render() stage_times summed, {threads} threads",
+               "frame_s": times}
         img = P.render(scene, 0, mode, k, bins, exact=args.exact)["image"]
         ref_img = ref_out["image"]
         d = img.astype(np.float64) - ref_img.astype(np.float64)
@@ -581,7 +705,8 @@ def main():
     ap.add_argument("--config", default="3", choices=sorted(CONFIGS))
     ap.add_argument("--mode", default="adagscale", choices=["adagscale", "ellipse", "aabb", "obb", "aabb_fixed3"])
     ap.add_argument("--exact", action="store_true", help="glibc-exact alpha (bit-identical images)")
-    ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--cpu-frames", type=int, default=5)
+    ap.add_argument("--no-cub", action="store_true", help="skip the cub::DeviceRadixSort comparator")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-off", action="store_true")

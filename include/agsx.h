@@ -207,9 +207,12 @@ int agsx_render_contributions(agsx_ctx* ctx, const agsx_scene* scene, const agsx
  * synchronises the stream. */
 int agsx_stage_history(agsx_ctx* ctx, float* stage_ms, int32_t max_frames, int32_t* out_frames);
 
-/* Counters of the most recent frame: {splat_count (survivors), splats with
- * >= 1 tile, pair_count, P_it (pairs iterated before tile saturation, the
- * rasterizer's work unit), overflow flag, tile count}; synchronises. */
+/* Counters of the most recent frame, the first n of: {splat_count
+ * (survivors), splats with >= 1 tile, pair_count, P_it (pairs iterated before
+ * tile saturation, the rasterizer's work unit), overflow flag, tile count,
+ * 8 rasterizer work counters (AGSX_RASTER_STATS=1), depth-sort passes (3 or
+ * 4; 0 on the tile-bucketed path), 1 if the tile-bucketed sort ran};
+ * synchronises. */
 int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n);
 
 /* Device pointer to the ctx-owned image of the most recent frame

@@ -383,9 +383,13 @@ int agsx_frame_stats(agsx_ctx* ctx, uint64_t* stats, int32_t n) {
             p_it = 0;
             for (const unsigned long long x : w) p_it += static_cast<uint32_t>(x);
         }
-        const uint64_t v[14] = {c.s, c.m, c.p, p_it, c.overflow, static_cast<uint64_t>(ctx->f_tile_count),
-                                c.dbg[0], c.dbg[1], c.dbg[2], c.dbg[3], c.dbg[4], c.dbg[5], c.dbg[6], c.dbg[7]};
-        for (int i = 0; i < n && i < 14; ++i) stats[i] = v[i];
+        // sort formulation of the frame: depth passes over the splats (3 or 4,
+        // depth-then-tile path) or 0 (tile-bucketed path)
+        const uint64_t depth_passes = ctx->f_bucket || c.m == 0 ? 0u : (depth_keys_wide_host(c) ? 4u : 3u);
+        const uint64_t v[16] = {c.s, c.m, c.p, p_it, c.overflow, static_cast<uint64_t>(ctx->f_tile_count),
+                                c.dbg[0], c.dbg[1], c.dbg[2], c.dbg[3], c.dbg[4], c.dbg[5], c.dbg[6], c.dbg[7],
+                                depth_passes, ctx->f_bucket ? 1u : 0u};
+        for (int i = 0; i < n && i < 16; ++i) stats[i] = v[i];
         return AGSX_OK;
     });
 }

@@ -456,15 +456,15 @@ public:
     }
 
     py::dict frame_stats() {
-        std::uint64_t v[14] = {};
-        const int rc = agsx_frame_stats(ctx_, v, 14);
+        std::uint64_t v[16] = {};
+        const int rc = agsx_frame_stats(ctx_, v, 16);
         if (rc != AGSX_OK) raise_status(rc, ctx_);
         py::dict d;
-        const char* names[14] = {"splat_count", "splats_with_tiles", "pair_count", "p_it", "overflow", "tiles",
+        const char* names[16] = {"splat_count", "splats_with_tiles", "pair_count", "p_it", "overflow", "tiles",
                                  "raster_iters", "raster_evals", "raster_fast", "raster_exact",
                                  "raster_iters_live_le32", "raster_iters_live_le64", "raster_iters_empty",
-                                 "raster_iters_no_live_pixel"};
-        for (int i = 0; i < 14; ++i) d[names[i]] = v[i];
+                                 "raster_iters_no_live_pixel", "depth_passes", "bucketed_sort"};
+        for (int i = 0; i < 16; ++i) d[names[i]] = v[i];
         return d;
     }
 

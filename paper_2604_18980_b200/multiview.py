@@ -12,8 +12,10 @@ Partitioning follows §8(e):
 * config 5 is a camera path split into contiguous blocks of views per rank;
 * config 4 is stereo, with the left eye on rank 0 and the right eye on rank 1.
 
-The rasteriser writes each frame straight into a slot of a rank-local frame tensor
-(``Renderer.render_async_to``), and the gather sends that tensor.
+The rasteriser writes each frame straight into a slot of a frame tensor
+(``Renderer.render_async_to``): on the destination rank that slot is already its
+place in the gathered camera path, and the other ranks' blocks are received
+in place by point-to-point transfers (no padding, no concatenation copy).
 """
 from __future__ import annotations
 
@@ -67,11 +69,21 @@ RenderInto = Callable[[object, int, object, dict], dict]
 """render_into(scene, view, frame_slot, kwargs) -> {"pair_count", "splat_count", "stage_ms"}"""
 
 
+def _order_after_torch(renderer):
+    """Make the renderer's stream wait for torch's current stream, so frame slots
+    handed out by the caching allocator are not still in use by queued torch work
+    when the rasteriser writes them."""
+    import torch
+
+    torch.cuda.ExternalStream(renderer.stream).wait_stream(torch.cuda.current_stream())
+
+
 def gpu_render_into(renderer) -> RenderInto:
     """A `RenderInto` over the CUDA path: the rasteriser writes the slot in place."""
 
     def fn(scene, view, slot, kw):
         cam = kw.get("camera")
+        _order_after_torch(renderer)
         renderer.render_async_to(scene, view, slot.data_ptr(), mode=kw.get("mode", "ellipse"), k=kw.get("k", 0.0),
                                  lut_bins=kw.get("lut_bins", []), exact=kw.get("exact", False), camera=cam)
         return renderer.wait()
@@ -88,6 +100,8 @@ def gpu_render_pipelined(renderers):
     def fn(scene, views, frames, kw):
         out = [None] * len(views)
         pending = {}  # renderer index -> view slot in flight
+        for r in renderers:
+            _order_after_torch(r)
         for i, v in enumerate(views):
             ri = i % len(renderers)
             r = renderers[ri]
@@ -120,10 +134,14 @@ class MultiViewRenderer:
         self.batch = batch
         self.device = device
 
-    def render_local(self, scene, views: Sequence[int], height: int, width: int, **kw):
+    def render_local(self, scene, views: Sequence[int], height: int, width: int, out=None, **kw):
+        """Render `views` into ``out`` (a ``[len(views), H, W, 3]`` float32 tensor,
+        allocated when None); returns ``(frames, stats)`` of this rank."""
         import torch
 
-        frames = torch.empty((max(len(views), 1), height, width, 3), dtype=torch.float32, device=self.device)
+        frames = out
+        if frames is None:
+            frames = torch.empty((max(len(views), 1), height, width, 3), dtype=torch.float32, device=self.device)
         stats = PathStats()
         per_view = (self.batch(scene, list(views), frames, kw) if self.batch is not None else
                     [self.render_into(scene, v, frames[i], kw) for i, v in enumerate(views)])
@@ -136,12 +154,17 @@ class MultiViewRenderer:
         return frames[: len(views)], stats
 
     def render_path(self, scene, n_views: int, height: int, width: int, group=None, dst: int = 0,
-                    gather: bool = True, **kw):
+                    gather: bool = True, out=None, **kw):
         """Render views [0, n_views) across the group; frames gathered on `dst`.
 
+        ``out`` (optional, on `dst`): a preallocated ``[n_views, H, W, 3]``
+        float32 tensor for the gathered path.  `dst` renders its own block
+        straight into its slice of it and receives every other block in place.
+
         Returns ``(frames, stats)``:
-        * ``frames`` is a ``[n_views, H, W, 3]`` tensor on `dst` (on its
-          device), or None on the other ranks and when ``gather`` is False;
+        * ``frames`` is the ``[n_views, H, W, 3]`` tensor on `dst` (on its
+          device), this rank's block when ``gather`` is False, or None on the
+          other ranks;
         * ``stats`` is a `PathStats` reduced over all ranks.
         """
         import torch
@@ -150,11 +173,19 @@ class MultiViewRenderer:
         world = dist.get_world_size(group) if dist.is_initialized() else 1
         rank = dist.get_rank(group) if dist.is_initialized() else 0
         views = partition_views(n_views, world, rank)
-        local, stats = self.render_local(scene, views, height, width, **kw)
-        frames = local if world == 1 else None
+        whole = None
+        if gather and rank == dst:
+            whole = out
+            if whole is None:
+                whole = torch.empty((n_views, height, width, 3), dtype=torch.float32, device=self.device)
+            elif tuple(whole.shape) != (n_views, height, width, 3) or whole.dtype != torch.float32:
+                raise ValueError("out must be a float32 [n_views, H, W, 3] tensor")
+        slot = whole[views[0]: views[0] + len(views)] if (whole is not None and views) else None
+        local, stats = self.render_local(scene, views, height, width, out=slot, **kw)
+        frames = whole if whole is not None else (local if not gather else None)
         if world > 1:
             if gather:
-                frames = gather_frames(local, n_views, world, rank, group, dst)
+                gather_frames(local, n_views, world, rank, group, dst, out=whole)
             red = torch.tensor([stats.frames, stats.pair_count, stats.splat_count], dtype=torch.float64,
                                device=self.device)
             mx = torch.tensor(stats.stage_ms_max, dtype=torch.float64, device=self.device)
@@ -165,23 +196,37 @@ class MultiViewRenderer:
         return frames, stats
 
 
-def gather_frames(local, n_views: int, world: int, rank: int, group=None, dst: int = 0):
+def gather_frames(local, n_views: int, world: int, rank: int, group=None, dst: int = 0, out=None):
     """Gather every rank's block of frames onto `dst` in camera-path order.
 
-    Ranks hold blocks of unequal length (`partition_views`), so each rank sends a
-    block padded to the largest one. `dst` then drops the padding."""
+    Point-to-point: each rank sends its block (exact size, `partition_views`)
+    and `dst` receives it straight into its slice of ``out`` (a ``[n_views,
+    H, W, 3]`` tensor; allocated when None).  `dst`'s own block is copied
+    only when it is not already that slice.  Returns ``out`` on `dst`, None
+    elsewhere."""
     import torch
     import torch.distributed as dist
 
-    counts = [len(partition_views(n_views, world, r)) for r in range(world)]
-    cap = max(counts)
-    h, w = local.shape[1], local.shape[2]
-    send = local
-    if local.shape[0] != cap:
-        send = torch.zeros((cap, h, w, 3), dtype=local.dtype, device=local.device)
-        send[: local.shape[0]] = local
-    recv = [torch.empty_like(send) for _ in range(world)] if rank == dst else None
-    dist.gather(send, gather_list=recv, dst=dst, group=group)
+    blocks = [partition_views(n_views, world, r) for r in range(world)]
     if rank != dst:
+        if blocks[rank]:
+            dist.send(local[: len(blocks[rank])].contiguous(), dst=_global_rank(group, dst), group=group)
         return None
-    return torch.cat([recv[r][: counts[r]] for r in range(world)], dim=0)
+    h, w = local.shape[1], local.shape[2]
+    if out is None:
+        out = torch.empty((n_views, h, w, 3), dtype=local.dtype, device=local.device)
+    mine = blocks[rank]
+    if mine and out[mine[0]: mine[0] + len(mine)].data_ptr() != local.data_ptr():
+        out[mine[0]: mine[0] + len(mine)].copy_(local[: len(mine)])
+    ops = [dist.P2POp(dist.irecv, out[b[0]: b[0] + len(b)], _global_rank(group, r), group)
+           for r, b in enumerate(blocks) if r != rank and b]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out
+
+
+def _global_rank(group, r: int) -> int:
+    import torch.distributed as dist
+
+    return r if group is None else dist.get_global_rank(group, r)

@@ -61,13 +61,19 @@ def _oracle_render_into():
     return port, scene, fn
 
 
-def _worker(rank, world, port_no, result_q):
+def _worker(rank, world, port_no, result_q, prealloc=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         _, scene, fn = _oracle_render_into()
         mv = MultiViewRenderer(fn, device="cpu")
-        frames, stats = mv.render_path(scene, SCENE["cameras"], SCENE["height"], SCENE["width"], mode="ellipse")
+        out = None
+        if prealloc and rank == 0:  # the bench's form: a preallocated path buffer on the destination
+            out = torch.full((SCENE["cameras"], SCENE["height"], SCENE["width"], 3), -1.0)
+        frames, stats = mv.render_path(scene, SCENE["cameras"], SCENE["height"], SCENE["width"], mode="ellipse",
+                                       out=out)
+        if out is not None:
+            assert frames.data_ptr() == out.data_ptr()  # gathered in place, no concatenation copy
         result_q.put((rank, None if frames is None else frames.numpy(), stats.frames, stats.pair_count,
                       stats.stage_ms_max))
     finally:
@@ -80,11 +86,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_gather_camera_path_world2_gloo():
+@pytest.mark.parametrize("prealloc", [False, True])
+def test_gather_camera_path_world2_gloo(prealloc):
+    """render_path over world 2 (5 views: uneven blocks 3 + 2), the code bench.py
+    runs for N > 1 (with the CUDA renderer and NCCL there)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port_no = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, q, prealloc)) for r in range(2)]
     for p in procs:
         p.start()
     results = {}
