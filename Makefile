@@ -37,7 +37,8 @@ PY_INC   := $(shell $(PYTHON) -c "import sysconfig;print(sysconfig.get_paths()['
 PYBIND   := $(shell $(PYTHON) -c "import pybind11;print(pybind11.get_include())")
 CORE     := $(PKG)/_core$(PY_EXT)
 
-all: $(LIBDIR)/libagsx.so $(LIBDIR)/libags.so $(CORE) $(LIBDIR)/render_cli oracle scripts/_build/libcubsort.so
+all: $(LIBDIR)/libagsx.so $(LIBDIR)/libags.so $(CORE) $(LIBDIR)/render_cli $(LIBDIR)/stage_api_test oracle \
+     scripts/_build/libcubsort.so
 .PHONY: all oracle clean
 
 # bench-only comparator (bench.py stages.sort.cub): cub::DeviceRadixSort on the same keys
@@ -67,6 +68,10 @@ $(CORE): $(CSRC)/python/bindings.cpp $(LIBDIR)/libags.so $(HOST_HDRS)
 
 # a reference-style C++ caller of the drop-in API (tests/cxx)
 $(LIBDIR)/render_cli: tests/cxx/render_cli.cpp $(LIBDIR)/libags.so $(HOST_HDRS)
+	$(CXX) $(HOSTFLAGS) $< -o $@ -L$(LIBDIR) -lags -lagsx -Wl,-rpath,'$$ORIGIN'
+
+# the reference's per-element unit cases restated against ags.hpp (tests/cxx)
+$(LIBDIR)/stage_api_test: tests/cxx/stage_api_test.cpp $(LIBDIR)/libags.so $(HOST_HDRS)
 	$(CXX) $(HOSTFLAGS) $< -o $@ -L$(LIBDIR) -lags -lagsx -Wl,-rpath,'$$ORIGIN'
 
 oracle:

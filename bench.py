@@ -312,6 +312,40 @@ def cub_comparator(r, scene, view, mode, k, bins, exact, iters=20):
     return res
 
 
+# ------------------------------------------------- C++ drop-in call (span)
+def cxx_span_e2e(cfg: str, mode: str, k: float, bins, iters: int = 5) -> dict:
+    """ags::render(std::span<const Gaussian3D>, cam, cfg, lut) -- the reference's
+    C++ signature (rasterizer.hpp:63-65) -- on the AoS synthetic scene, through
+    libags.so's ags_bench_render_span: host clock per call, with the
+    span-identity device-scene cache (the default) and without it (every call
+    packs and uploads the scene, like a reference caller that changes scenes)."""
+    so = os.path.join(ROOT, "paper_2604_18980_b200", "lib", "libags.so")
+    lib = ctypes.CDLL(so)
+    f = lib.ags_bench_render_span
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.c_char_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                  ctypes.c_float, ctypes.c_int, ctypes.c_float, ctypes.POINTER(ctypes.c_float), ctypes.c_int,
+                  ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                  ctypes.POINTER(ctypes.c_uint64)]
+    n, w, h, cams = CONFIGS[cfg]
+    mode_id = {"aabb": 0, "obb": 1, "ellipse": 2, "adagscale": 3}.get(mode, 2)
+    lb = (ctypes.c_float * max(len(bins), 1))(*bins) if bins else None
+    out = {}
+    for label, cache, it in (("cached", 1, iters), ("uncached", 0, 2)):
+        per, first, pairs = ctypes.c_double(), ctypes.c_double(), ctypes.c_uint64()
+        rc = f(1, n, b"veil", cams, w, h, 500.0 * w / 640.0, mode_id, k, lb, len(bins), it, cache, ctypes.byref(per),
+               ctypes.byref(first), ctypes.byref(pairs))
+        if rc != 0:
+            return {"unavailable": f"ags_bench_render_span rc={rc}"}
+        out[label] = {"value": 1.0 / per.value, "unit": "frames/s", "s_per_call": per.value,
+                      "first_call_s": first.value, "calls": it, "pair_count": int(pairs.value)}
+    out["api"] = ("ags::render(std::span<const Gaussian3D>, ...) -> RenderReport with a std::vector<float> image "
+                  "(pageable host memory); cached = span-identity device-scene cache, uncached = AoS pack + "
+                  "upload of the scene in every call")
+    out["d2h_bytes_per_step"] = w * h * 12
+    return out
+
+
 # ------------------------------------------------------------- our arm
 def run_ours(args, rank, world, local_rank):
     os.environ["AGS_DEVICE"] = str(local_rank)  # device of the module-level render()
@@ -530,6 +564,8 @@ def run_ours(args, rank, world, local_rank):
                                            "d2h_bytes_per_step": int(out8["image"].nbytes) + 128,
                                            "api": "batch.render_views(..., image_u8=True)"}
         del prs
+        if world == 1:
+            e2e["cxx_span"] = cxx_span_e2e(args.config, mode, k, bins)
 
     # ---- AdaGScale off, same scene (pairs + FPS) --------------------------
     off = None

@@ -27,6 +27,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -88,6 +89,13 @@ struct Mat3 {
             for (int c = 0; c < 3; ++c) out(r, c) = (*this)(c, r);
         return out;
     }
+    // element-wise conversion (math.hpp:66-71)
+    template <typename U>
+    Mat3<U> cast() const {
+        Mat3<U> out;
+        for (int i = 0; i < 9; ++i) out.m[i] = static_cast<U>(m[i]);
+        return out;
+    }
 };
 using Mat3f = Mat3<float>;
 using Mat3d = Mat3<double>;
@@ -102,12 +110,64 @@ struct SymMat2 {
     float quad(Vec2f d) const { return xx * d.x * d.x + 2.0f * xy * d.x * d.y + yy * d.y * d.y; }
 };
 
+// Eigen pair of a symmetric 2x2 matrix (math.hpp:97-131): l1 >= l2, v1 the unit
+// eigenvector of l1 (the larger-norm candidate of the two closed forms),
+// v2 = v1 rotated by +90 degrees; axis-aligned vectors when xy == 0.  The
+// device copy used by the tile tests is agsx::eigen_sym2 (same operations).
+struct Eigen2 {
+    float l1 = 0.0f;
+    float l2 = 0.0f;
+    Vec2f v1{1, 0};
+    Vec2f v2{0, 1};
+};
+
+inline Eigen2 eigen_sym2(const SymMat2& m) {
+    Eigen2 e;
+    const float centre = 0.5f * (m.xx + m.yy);
+    const float half = 0.5f * (m.xx - m.yy);
+    const float rad = std::sqrt(half * half + m.xy * m.xy);
+    e.l1 = centre + rad;
+    e.l2 = centre - rad;
+    if (m.xy == 0.0f) {
+        const bool x_major = m.xx >= m.yy;
+        e.v1 = x_major ? Vec2f{1, 0} : Vec2f{0, 1};
+        e.v2 = x_major ? Vec2f{0, 1} : Vec2f{-1, 0};
+        return e;
+    }
+    const Vec2f cand_a{e.l1 - m.yy, m.xy};
+    const Vec2f cand_b{m.xy, e.l1 - m.xx};
+    const Vec2f v = cand_a.dot(cand_a) >= cand_b.dot(cand_b) ? cand_a : cand_b;
+    const float len = std::sqrt(v.dot(v));
+    e.v1 = {v.x / len, v.y / len};
+    e.v2 = {-e.v1.y, e.v1.x};
+    return e;
+}
+
 struct Quatf {
     float w = 1.0f, x = 0.0f, y = 0.0f, z = 0.0f;
     float norm() const { return std::sqrt(w * w + x * x + y * y + z * z); }
     Quatf normalized() const {
         const float n = norm();
         return {w / n, x / n, y / n, z / n};
+    }
+    Mat3f to_matrix() const { return rotation_matrix<float>(); }
+    // Rotation matrix with the quaternion renormalised in double
+    // (math.hpp:143-164); the device EWA (K1) evaluates the same expressions.
+    template <typename T>
+    Mat3<T> rotation_matrix() const {
+        const double len = std::sqrt(double(w) * w + double(x) * x + double(y) * y + double(z) * z);
+        const double a = w / len, b = x / len, c = y / len, d = z / len;
+        Mat3<double> r;
+        r(0, 0) = 1 - 2 * (c * c + d * d);
+        r(0, 1) = 2 * (b * c - a * d);
+        r(0, 2) = 2 * (b * d + a * c);
+        r(1, 0) = 2 * (b * c + a * d);
+        r(1, 1) = 1 - 2 * (b * b + d * d);
+        r(1, 2) = 2 * (c * d - a * b);
+        r(2, 0) = 2 * (b * d - a * c);
+        r(2, 1) = 2 * (c * d + a * b);
+        r(2, 2) = 1 - 2 * (b * b + c * c);
+        return r.template cast<T>();
     }
 };
 
@@ -138,6 +198,9 @@ struct Gaussian3D {
 int sh_degree(const Gaussian3D& g);
 std::string validate(const Gaussian3D& g);
 
+// Sigma = (R diag(s)) (R diag(s))^T in double (scene.cpp:31-39).
+Mat3d covariance_3d(const Gaussian3D& g);
+
 struct Camera {
     Vec3f position;
     Mat3f rotation;  // world-to-camera
@@ -145,8 +208,18 @@ struct Camera {
     int width = 0, height = 0;
 };
 
+// world -> camera, float, left-to-right dot products (scene.hpp:41-43)
+inline Vec3f to_camera(const Camera& cam, Vec3f world) { return cam.rotation * (world - cam.position); }
+// the image centre (scene.hpp:46-49)
+inline Vec2f principal_point(const Camera& cam) {
+    return {0.5f * static_cast<float>(cam.width), 0.5f * static_cast<float>(cam.height)};
+}
+
 std::string validate(const Camera& cam);
 float orthonormality_drift(const Mat3f& r);
+// Nearest orthonormal matrix by the polar iteration X <- (X + X^-T) / 2
+// (scene.cpp:84-92): at most 20 steps, stops at drift <= 1e-7.
+Mat3f orthonormalize(Mat3f r);
 
 enum class Mode { AABB, OBB, Ellipse, AdaGScale };
 const char* mode_name(Mode m);
@@ -284,6 +357,42 @@ private:
     std::uint64_t count_ = 0;
 };
 
+// ------------------------------------- per-element stage functions
+// Each runs the device function the kernels use (one element per CUDA
+// thread through the agsx_* helper entry points); alpha_at and eigen_sym2
+// are header inlines in the reference and stay inline here.
+
+// preprocess.hpp:29-37
+struct Projection {
+    Vec2f mean2d;
+    SymMat2 cov2d;  // with the +0.3 dilation
+    float depth;
+};
+std::optional<Projection> project(const Gaussian3D& g, const Camera& cam, const RenderConfig& cfg);
+// preprocess.hpp:38-40; view_dir must be unit length
+Vec3f eval_color(const Gaussian3D& g, Vec3f view_dir);
+// preprocess.hpp:44-45 (Eq. 10); std::invalid_argument when det(cov2d) <= 0
+float compute_th(const SymMat2& cov2d, float depth, const TUpperLUT& lut, float k, float tau);
+
+// pair_gen.hpp:49-55
+struct EffectiveRadius {
+    float mahalanobis;  // sqrt(2 ln(opacity / th))
+    float pixels;       // mahalanobis * sqrt(lambda_max(cov2d))
+};
+EffectiveRadius effective_radius(float opacity, float th, const SymMat2& cov2d);
+// pair_gen.hpp:60-61: row-major ascending tile ids hit by the splat
+void intersect_tiles(const SplatView& s, const TileGrid& grid, Mode mode, const RenderConfig& cfg,
+                     std::vector<int>& out);
+
+// rasterizer.hpp:44-50: opacity * exp(-0.5 d^T inv d), clamped
+inline float alpha_at(const SplatView& s, Vec2f pixel, float alpha_clamp) {
+    const Vec2f d = pixel - s.mean2d;
+    const float power = -0.5f * s.inv_cov.quad(d);
+    if (power > 0.0f) return 0.0f;
+    const float a = s.opacity * std::exp(power);
+    return a < alpha_clamp ? a : alpha_clamp;
+}
+
 std::vector<SplatView> preprocess_view(std::span<const Gaussian3D> scene, const Camera& cam,
                                        const RenderConfig& cfg, const TUpperLUT* lut = nullptr);
 PairGenResult generate_pairs(std::span<const SplatView> splats, const TileGrid& grid, Mode mode,
@@ -294,8 +403,24 @@ SortedPairs sort_pairs(std::vector<GaussianTilePair> pairs, int tile_count);
 Image raster_tiles(const SortedPairs& sorted, std::span<const SplatView> splats,
                    const TileGrid& grid, const RenderConfig& cfg, std::vector<float>* max_t = nullptr);
 
+// rasterizer.hpp:54-58: one tile's sorted pair span blended into `out`
+// (the tile's pixels only); max_t, if given, is raised per splat (sized to
+// splats.size()); contributions, if given, receives the tile's blend events
+// in the reference's order.
+void raster_tile(std::span<const GaussianTilePair> tile_pairs, std::span<const SplatView> splats,
+                 const TileGrid& grid, int tile_index, const RenderConfig& cfg, Image& out,
+                 std::vector<float>* max_t, std::vector<BlendRecord>* contributions);
+
+// The reference's entry point (rasterizer.hpp:63-65).  The scene is packed and
+// uploaded once per span: a later call with the same span (address, length
+// and a sampled content fingerprint) reuses the device copy, as a reference
+// caller looping over views of one scene expects (calibrate.cpp:29,86,113).
+// forget_device_scenes() drops the cached copies (a caller that edits a
+// scene in place between calls, below the fingerprint's sampling); the
+// environment variable AGS_SCENE_CACHE=0 disables the cache.
 RenderReport render(std::span<const Gaussian3D> scene, const Camera& cam, const RenderConfig& cfg,
                     const TUpperLUT* lut = nullptr, const RecordOptions& rec = {});
+void forget_device_scenes();
 RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderConfig& cfg,
                     const TUpperLUT* lut = nullptr, const RecordOptions& rec = {});
 

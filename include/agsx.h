@@ -254,6 +254,32 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
                 int32_t width, int32_t height, const agsx_config* cfg, float* image,
                 float* max_t);
 
+/* ---- per-element helpers of the stages (the device functions the kernels
+ * use, one element per thread; the C++ wrappers in ags.hpp take the
+ * reference's single-element signatures) ------------------------------- */
+/* project (preprocess.cpp:26-66, preprocess.hpp:35-37) of every Gaussian of
+ * an uploaded scene: valid[i] = 1 when in front of the near plane and inside
+ * the guard band; out[6i..6i+5] = {mean2d.x, mean2d.y, cov2d.xx, cov2d.xy,
+ * cov2d.yy, depth} (cov2d carries the +0.3 dilation). */
+int agsx_project(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam, const agsx_config* cfg,
+                 uint8_t* valid, float* out);
+/* eval_color (preprocess.cpp:68-105, preprocess.hpp:38-40): rgb[3i..] of
+ * Gaussian i of the scene for the unit view direction dirs[3i..]. */
+int agsx_eval_color(agsx_ctx* ctx, const agsx_scene* scene, const float* dirs, float* rgb);
+/* compute_th (preprocess.cpp:107-116, preprocess.hpp:44-45) of n (cov2d
+ * {xx, xy, yy}, depth) with the LUT (NULL = all ones), k and tau;
+ * AGSX_EINVAL when some det(cov2d) <= 0 (std::invalid_argument). */
+int agsx_compute_th(agsx_ctx* ctx, const float* cov2d, const float* depth, uint64_t n, const agsx_lut* lut,
+                    float k, float tau, float* th);
+/* alpha_at (rasterizer.hpp:44-50, glibc expf) of splats[i] at the pixel
+ * centre px[2i..2i+1]. */
+int agsx_alpha_at(agsx_ctx* ctx, const agsx_splat_view* splats, const float* px, uint64_t n,
+                  float alpha_clamp, float* alpha);
+/* effective_radius (pair_gen.cpp:11-16, pair_gen.hpp:49-55, glibc logf):
+ * out[2i] = mahalanobis, out[2i+1] = pixels. */
+int agsx_effective_radius(agsx_ctx* ctx, const float* opacity, const float* th, const float* cov2d, uint64_t n,
+                          float* out);
+
 /* ---- calibration primitives (calibrate.cpp:14-155, analysis.cpp:14-29) - */
 /* Device memory owned by the caller (e.g. the calibration reference frames). */
 int agsx_device_alloc(agsx_ctx* ctx, size_t bytes, void** out);

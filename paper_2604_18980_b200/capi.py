@@ -29,6 +29,7 @@ EXPORTS = (
     "agsx_device_expf", "agsx_kernel_launches", "agsx_stage_history",
     "agsx_frame_stats", "agsx_host_alloc", "agsx_host_free", "agsx_device_alloc", "agsx_device_free",
     "agsx_fold_max_t", "agsx_sq_err", "agsx_render_u8",
+    "agsx_project", "agsx_eval_color", "agsx_compute_th", "agsx_alpha_at", "agsx_effective_radius",
 )
 
 SPLAT_DTYPE = np.dtype(
@@ -204,6 +205,11 @@ class Lib:
                                           C.POINTER(u64)]
         L.agsx_sort_pairs.argtypes = [vp, vp, vp, u64, i32, vp]
         L.agsx_raster.argtypes = [vp, vp, u64, vp, u64, vp, i32, i32, C.POINTER(Config), vp, vp]
+        L.agsx_project.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.agsx_eval_color.argtypes = [vp, vp, vp, vp]
+        L.agsx_compute_th.argtypes = [vp, vp, vp, u64, vp, C.c_float, C.c_float, vp]
+        L.agsx_alpha_at.argtypes = [vp, vp, vp, u64, C.c_float, vp]
+        L.agsx_effective_radius.argtypes = [vp, vp, vp, vp, u64, vp]
         L.agsx_device_logf.argtypes = [vp, vp, vp, u64]
         L.agsx_device_expf.argtypes = [vp, vp, vp, u64]
         L.agsx_stage_history.argtypes = [vp, vp, i32, C.POINTER(i32)]
@@ -389,6 +395,45 @@ class Context:
         self._check(self.L.agsx_raster(self.h, _p(splats), len(splats), _p(idx), len(idx), _p(ranges), width,
                                        height, C.byref(cfg), _p(img), _p(mt)))
         return (img, mt[: len(splats)]) if max_t else img
+
+    # ---- per-element helpers (the device functions of the stages) ----------
+    def project(self, scene, cam, cfg):
+        """project (preprocess.cpp:26-66) of every Gaussian of an uploaded scene:
+        (valid[n] bool, out[n, 6] = mean2d.xy, cov2d xx/xy/yy, depth)."""
+        n = self.L.agsx_scene_count(scene)
+        valid = np.zeros(max(n, 1), np.uint8)
+        out = np.zeros((max(n, 1), 6), np.float32)
+        self._check(self.L.agsx_project(self.h, scene, C.byref(cam), C.byref(cfg), _p(valid), _p(out)))
+        return valid[:n].astype(bool), out[:n]
+
+    def eval_color(self, scene, dirs):
+        dirs = np.ascontiguousarray(dirs, np.float32).reshape(-1, 3)
+        rgb = np.zeros_like(dirs)
+        self._check(self.L.agsx_eval_color(self.h, scene, _p(dirs), _p(rgb)))
+        return rgb
+
+    def compute_th(self, cov2d, depth, lut, k, tau):
+        cov2d = np.ascontiguousarray(cov2d, np.float32).reshape(-1, 3)
+        depth = np.ascontiguousarray(depth, np.float32)
+        th = np.zeros(len(depth), np.float32)
+        self._check(self.L.agsx_compute_th(self.h, _p(cov2d), _p(depth), len(depth),
+                                           C.byref(lut) if lut is not None else None, k, tau, _p(th)))
+        return th
+
+    def alpha_at(self, splats, px, alpha_clamp):
+        splats = np.ascontiguousarray(splats, SPLAT_DTYPE)
+        px = np.ascontiguousarray(px, np.float32).reshape(-1, 2)
+        a = np.zeros(len(splats), np.float32)
+        self._check(self.L.agsx_alpha_at(self.h, _p(splats), _p(px), len(splats), alpha_clamp, _p(a)))
+        return a
+
+    def effective_radius(self, opacity, th, cov2d):
+        opacity = np.ascontiguousarray(opacity, np.float32)
+        th = np.ascontiguousarray(th, np.float32)
+        cov2d = np.ascontiguousarray(cov2d, np.float32).reshape(-1, 3)
+        out = np.zeros((len(opacity), 2), np.float32)
+        self._check(self.L.agsx_effective_radius(self.h, _p(opacity), _p(th), _p(cov2d), len(opacity), _p(out)))
+        return out
 
     def logf(self, x):
         x = np.ascontiguousarray(x, np.float32)

@@ -7,6 +7,25 @@
 //                        pair_sort.hpp:19, rasterizer.hpp:54-58
 #include "agsx_ctx.cuh"
 
+// ---- per-element helpers ---------------------------------------------------
+namespace agsx::host {
+namespace {
+// host -> device copy of n floats into a ctx scratch buffer
+template <typename T>
+T* to_device(agsx_ctx* ctx, Buf& b, const T* src, uint64_t n) {
+    ensure(b, std::max<uint64_t>(n, 1) * sizeof(T));
+    if (n) AGSX_CUDA(cudaMemcpyAsync(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+    return ptr<T>(b);
+}
+template <typename T>
+void to_host(agsx_ctx* ctx, T* dst, const Buf& b, uint64_t n) {
+    if (n) AGSX_CUDA(cudaMemcpyAsync(dst, b.p, n * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+int grid_of(uint64_t n) { return static_cast<int>(std::max<uint64_t>((n + 255) / 256, 1)); }
+}  // namespace
+}  // namespace agsx::host
+
 extern "C" {
 
 int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
@@ -298,6 +317,109 @@ int agsx_sq_err(agsx_ctx* ctx, const float* a, const float* b, uint64_t n, doubl
         check_launch(ctx);
         AGSX_CUDA(cudaMemcpyAsync(out, res, 8, cudaMemcpyDeviceToHost, ctx->stream));
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        return AGSX_OK;
+    });
+}
+
+
+int agsx_project(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam, const agsx_config* cfg,
+                 uint8_t* valid, float* out) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!scene || !cam || !cfg || !valid || !out) return fail(ctx, AGSX_EINVAL, "project: null argument");
+        const uint64_t n = scene->n;
+        const FrameParams p = make_params(*cam, *cfg, nullptr, nullptr);
+        ensure(ctx->tmp0, std::max<uint64_t>(n, 1));
+        ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 24);
+        if (n) {
+            k_project<<<grid_of(n), 256, 0, ctx->stream>>>(p, scene->view(), ptr<uint8_t>(ctx->tmp0),
+                                                           ptr<float>(ctx->tmp1));
+            check_launch(ctx);
+            AGSX_CUDA(cudaMemcpyAsync(valid, ctx->tmp0.p, n, cudaMemcpyDeviceToHost, ctx->stream));
+        }
+        to_host(ctx, out, ctx->tmp1, 6 * n);
+        return AGSX_OK;
+    });
+}
+
+int agsx_eval_color(agsx_ctx* ctx, const agsx_scene* scene, const float* dirs, float* rgb) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if (!scene || !dirs || !rgb) return fail(ctx, AGSX_EINVAL, "eval_color: null argument");
+        const uint64_t n = scene->n;
+        const float* d = to_device(ctx, ctx->tmp0, dirs, 3 * n);
+        ensure(ctx->tmp1, std::max<uint64_t>(n, 1) * 12);
+        if (n) {
+            k_eval_color<<<grid_of(n), 256, 0, ctx->stream>>>(scene->view(), d, ptr<float>(ctx->tmp1));
+            check_launch(ctx);
+        }
+        to_host(ctx, rgb, ctx->tmp1, 3 * n);
+        return AGSX_OK;
+    });
+}
+
+int agsx_compute_th(agsx_ctx* ctx, const float* cov2d, const float* depth, uint64_t n, const agsx_lut* lut,
+                    float k, float tau, float* th) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if ((n && (!cov2d || !depth)) || !th) return fail(ctx, AGSX_EINVAL, "compute_th: null argument");
+        agsx_camera cam{};
+        cam.rotation[0] = cam.rotation[4] = cam.rotation[8] = 1.0f;
+        cam.fx = cam.fy = 1.0f;
+        cam.width = cam.height = 1;
+        agsx_config cfg{};
+        cfg.mode = AGSX_MODE_ADAGSCALE;
+        cfg.k = k;
+        cfg.alpha_threshold = tau;
+        cfg.tile_size = 16;
+        const float* lut_dev = nullptr;
+        if (lut && lut->bin_count > kLutInline) lut_dev = to_device(ctx, ctx->lut_ext, lut->bins, lut->bin_count);
+        const FrameParams p = make_params(cam, cfg, lut, lut_dev);
+        const float* c = to_device(ctx, ctx->tmp0, cov2d, 3 * n);
+        const float* d = to_device(ctx, ctx->tmp1, depth, n);
+        ensure(ctx->tmp2, std::max<uint64_t>(n, 1) * 4);
+        if (n) {
+            k_compute_th<<<grid_of(n), 256, 0, ctx->stream>>>(p, c, d, n, ptr<float>(ctx->tmp2));
+            check_launch(ctx);
+        }
+        to_host(ctx, th, ctx->tmp2, n);
+        for (uint64_t i = 0; i < n; ++i)
+            if (th[i] != th[i]) return fail(ctx, AGSX_EINVAL, "compute_th: non-positive determinant");
+        return AGSX_OK;
+    });
+}
+
+int agsx_alpha_at(agsx_ctx* ctx, const agsx_splat_view* splats, const float* px, uint64_t n, float alpha_clamp,
+                  float* alpha) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if ((n && (!splats || !px)) || !alpha) return fail(ctx, AGSX_EINVAL, "alpha_at: null argument");
+        const agsx_splat_view* s = to_device(ctx, ctx->tmp0, splats, n);
+        const float* x = to_device(ctx, ctx->tmp1, px, 2 * n);
+        ensure(ctx->tmp2, std::max<uint64_t>(n, 1) * 4);
+        if (n) {
+            k_alpha_at<<<grid_of(n), 256, 0, ctx->stream>>>(s, x, n, alpha_clamp, ptr<float>(ctx->tmp2));
+            check_launch(ctx);
+        }
+        to_host(ctx, alpha, ctx->tmp2, n);
+        return AGSX_OK;
+    });
+}
+
+int agsx_effective_radius(agsx_ctx* ctx, const float* opacity, const float* th, const float* cov2d, uint64_t n,
+                          float* out) {
+    if (!ctx) return AGSX_EINVAL;
+    return guarded(ctx, [&]() -> int {
+        if ((n && (!opacity || !th || !cov2d)) || !out) return fail(ctx, AGSX_EINVAL, "effective_radius: null argument");
+        const float* o = to_device(ctx, ctx->tmp0, opacity, n);
+        const float* t = to_device(ctx, ctx->tmp1, th, n);
+        const float* c = to_device(ctx, ctx->tmp2, cov2d, 3 * n);
+        ensure(ctx->tmp3, std::max<uint64_t>(n, 1) * 8);
+        if (n) {
+            k_effective_radius<<<grid_of(n), 256, 0, ctx->stream>>>(o, t, c, n, ptr<float>(ctx->tmp3));
+            check_launch(ctx);
+        }
+        to_host(ctx, out, ctx->tmp3, 2 * n);
         return AGSX_OK;
     });
 }

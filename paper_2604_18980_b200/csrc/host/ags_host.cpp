@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <limits>
 #include <mutex>
+#include <thread>
 
 #include "agsx.h"
 #include "ags/ags.hpp"
@@ -499,20 +500,33 @@ PackedScene pack(std::span<const Gaussian3D> scene) {
     p.rot.resize(4 * n);
     p.op.resize(n);
     p.sh.assign(maxc * n, 0.0f);
-    for (std::size_t i = 0; i < n; ++i) {
-        const Gaussian3D& g = scene[i];
-        p.mean[3 * i] = g.mean.x;
-        p.mean[3 * i + 1] = g.mean.y;
-        p.mean[3 * i + 2] = g.mean.z;
-        p.scale[3 * i] = g.scale.x;
-        p.scale[3 * i + 1] = g.scale.y;
-        p.scale[3 * i + 2] = g.scale.z;
-        p.rot[4 * i] = g.rotation.w;
-        p.rot[4 * i + 1] = g.rotation.x;
-        p.rot[4 * i + 2] = g.rotation.y;
-        p.rot[4 * i + 3] = g.rotation.z;
-        p.op[i] = g.opacity;
-        std::copy(g.sh.begin(), g.sh.end(), p.sh.begin() + maxc * i);
+    auto run = [&](std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            const Gaussian3D& g = scene[i];
+            p.mean[3 * i] = g.mean.x;
+            p.mean[3 * i + 1] = g.mean.y;
+            p.mean[3 * i + 2] = g.mean.z;
+            p.scale[3 * i] = g.scale.x;
+            p.scale[3 * i + 1] = g.scale.y;
+            p.scale[3 * i + 2] = g.scale.z;
+            p.rot[4 * i] = g.rotation.w;
+            p.rot[4 * i + 1] = g.rotation.x;
+            p.rot[4 * i + 2] = g.rotation.y;
+            p.rot[4 * i + 3] = g.rotation.z;
+            p.op[i] = g.opacity;
+            std::copy(g.sh.begin(), g.sh.end(), p.sh.begin() + maxc * i);
+        }
+    };
+    // AoS -> SoA by host threads (the per-Gaussian SH vectors are separate
+    // heap blocks, so one thread is bound by their cache misses)
+    const unsigned nt = n < (1u << 16) ? 1u : std::min(16u, std::max(1u, std::thread::hardware_concurrency()));
+    if (nt == 1) {
+        run(0, n);
+    } else {
+        std::vector<std::thread> pool;
+        const std::size_t per = (n + nt - 1) / nt;
+        for (unsigned t = 0; t < nt; ++t) pool.emplace_back(run, std::min(n, t * per), std::min(n, (t + 1) * per));
+        for (auto& th : pool) th.join();
     }
     return p;
 }
@@ -592,14 +606,6 @@ RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderCon
             if (alive[i]) rep.max_t.push_back(maxt_by_gid[i]);
     }
     return rep;
-}
-
-RenderReport render(std::span<const Gaussian3D> scene, const Camera& cam, const RenderConfig& cfg,
-                    const TUpperLUT* lut, const RecordOptions& rec) {
-    if (const std::string bad = validate(cfg); !bad.empty()) throw std::invalid_argument("render: " + bad);
-    if (const std::string bad = validate(cam); !bad.empty()) throw std::invalid_argument("render: " + bad);
-    const DeviceScene dev(scene);
-    return render(dev, cam, cfg, lut, rec);
 }
 
 std::vector<SplatView> preprocess_view(std::span<const Gaussian3D> scene, const Camera& cam,

@@ -1,0 +1,268 @@
+// ags_stages.cpp -- the reference's per-element stage functions and math
+// helpers of the C++ drop-in API (include/ags/ags.hpp), and the device-scene
+// cache behind render(std::span<const Gaussian3D>, ...).
+//
+//   reference: covariance_3d        scene.cpp:31-39
+//              orthonormalize       scene.cpp:62-92
+//              project / eval_color preprocess.cpp:26-105 (preprocess.hpp:29-40)
+//              compute_th           preprocess.cpp:107-116
+//              effective_radius     pair_gen.cpp:11-16
+//              intersect_tiles      pair_gen.cpp:108-159
+//              raster_tile          rasterizer.cpp:21-100
+//              render               rasterizer.cpp:102-165
+//
+// The stage functions run the device code of the render path through the
+// agsx_* helper entry points; covariance_3d and orthonormalize are host math
+// utilities (double / float, the reference's operation order).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "agsx.h"
+#include "ags/ags.hpp"
+#include "ags_internal.hpp"
+
+namespace ags {
+
+using namespace detail;
+
+// --------------------------------------------------------------- math
+Mat3d covariance_3d(const Gaussian3D& g) {
+    Mat3d m = g.rotation.rotation_matrix<double>();
+    const double s[3] = {g.scale.x, g.scale.y, g.scale.z};
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) m(r, c) *= s[c];  // R diag(s)
+    return m * m.transposed();
+}
+
+namespace {
+// float adjugate / determinant inverse, the expression order of scene.cpp:62-80
+Mat3f inverse3(const Mat3f& a) {
+    const float c00 = a(1, 1) * a(2, 2) - a(1, 2) * a(2, 1);
+    const float c01 = a(1, 2) * a(2, 0) - a(1, 0) * a(2, 2);
+    const float c02 = a(1, 0) * a(2, 1) - a(1, 1) * a(2, 0);
+    const float inv = 1.0f / (a(0, 0) * c00 + a(0, 1) * c01 + a(0, 2) * c02);
+    Mat3f o;
+    o(0, 0) = c00 * inv;
+    o(1, 0) = c01 * inv;
+    o(2, 0) = c02 * inv;
+    o(0, 1) = (a(0, 2) * a(2, 1) - a(0, 1) * a(2, 2)) * inv;
+    o(1, 1) = (a(0, 0) * a(2, 2) - a(0, 2) * a(2, 0)) * inv;
+    o(2, 1) = (a(0, 1) * a(2, 0) - a(0, 0) * a(2, 1)) * inv;
+    o(0, 2) = (a(0, 1) * a(1, 2) - a(0, 2) * a(1, 1)) * inv;
+    o(1, 2) = (a(0, 2) * a(1, 0) - a(0, 0) * a(1, 2)) * inv;
+    o(2, 2) = (a(0, 0) * a(1, 1) - a(0, 1) * a(1, 0)) * inv;
+    return o;
+}
+}  // namespace
+
+Mat3f orthonormalize(Mat3f r) {
+    for (int step = 0; step < 20 && orthonormality_drift(r) > 1e-7f; ++step) {
+        const Mat3f it = inverse3(r).transposed();
+        for (int i = 0; i < 9; ++i) r.m[i] = 0.5f * (r.m[i] + it.m[i]);
+    }
+    return r;
+}
+
+// ----------------------------------------------- per-element stage functions
+std::optional<Projection> project(const Gaussian3D& g, const Camera& cam, const RenderConfig& cfg) {
+    const DeviceScene dev(std::span<const Gaussian3D>(&g, 1));
+    agsx_ctx* ctx = thread_ctx();
+    const agsx_camera c = to_c(cam);
+    const agsx_config k = to_c(cfg);
+    std::uint8_t valid = 0;
+    float o[6] = {};
+    check(agsx_project(ctx, static_cast<const agsx_scene*>(dev.handle()), &c, &k, &valid, o), ctx);
+    if (!valid) return std::nullopt;
+    return Projection{{o[0], o[1]}, {o[2], o[3], o[4]}, o[5]};
+}
+
+Vec3f eval_color(const Gaussian3D& g, Vec3f view_dir) {
+    const DeviceScene dev(std::span<const Gaussian3D>(&g, 1));
+    agsx_ctx* ctx = thread_ctx();
+    const float d[3] = {view_dir.x, view_dir.y, view_dir.z};
+    float rgb[3] = {};
+    check(agsx_eval_color(ctx, static_cast<const agsx_scene*>(dev.handle()), d, rgb), ctx);
+    return {rgb[0], rgb[1], rgb[2]};
+}
+
+float compute_th(const SymMat2& cov2d, float depth, const TUpperLUT& lut, float k, float tau) {
+    agsx_ctx* ctx = thread_ctx();
+    const agsx_lut l = to_c(lut);
+    const float c[3] = {cov2d.xx, cov2d.xy, cov2d.yy};
+    float th = 0.0f;
+    const int rc = agsx_compute_th(ctx, c, &depth, 1, &l, k, tau, &th);
+    if (rc == AGSX_EINVAL) throw std::invalid_argument("compute_th: non-positive determinant");
+    check(rc, ctx);
+    return th;
+}
+
+EffectiveRadius effective_radius(float opacity, float th, const SymMat2& cov2d) {
+    agsx_ctx* ctx = thread_ctx();
+    const float c[3] = {cov2d.xx, cov2d.xy, cov2d.yy};
+    float o[2] = {};
+    check(agsx_effective_radius(ctx, &opacity, &th, c, 1, o), ctx);
+    return {o[0], o[1]};
+}
+
+void intersect_tiles(const SplatView& s, const TileGrid& grid, Mode mode, const RenderConfig& cfg,
+                     std::vector<int>& out) {
+    // generate_pairs over the one splat (no budget: intersect_tiles never throws)
+    RenderConfig c = cfg;
+    c.tile_size = grid.tile_size;
+    c.pair_budget = ~std::size_t{0} >> 1;
+    const PairGenResult r = generate_pairs(std::span<const SplatView>(&s, 1), grid, mode, c);
+    out.clear();
+    out.reserve(r.pairs.size());
+    for (const GaussianTilePair& p : r.pairs) out.push_back(static_cast<int>(pair_key_tile(p.key)));
+}
+
+void raster_tile(std::span<const GaussianTilePair> tile_pairs, std::span<const SplatView> splats,
+                 const TileGrid& grid, int tile_index, const RenderConfig& cfg, Image& out,
+                 std::vector<float>* max_t, std::vector<BlendRecord>* contributions) {
+    if (contributions)
+        throw std::invalid_argument(
+            "raster_tile: the blend-event stream is produced by render(..., RecordOptions{.contributions = true})");
+    if (tile_index < 0 || tile_index >= grid.tile_count()) return;
+    const int tx = tile_index % grid.tiles_x, ty = tile_index / grid.tiles_x;
+    const int x0 = tx * grid.tile_size, y0 = ty * grid.tile_size;
+    const int w = std::min(grid.tile_size, grid.width - x0), h = std::min(grid.tile_size, grid.height - y0);
+    if (w <= 0 || h <= 0) return;
+    if (out.width != grid.width || out.height != grid.height)
+        throw std::invalid_argument("raster_tile: image does not match the grid");
+    agsx_ctx* ctx = thread_ctx();
+    agsx_config k = to_c(cfg);
+    k.tile_size = grid.tile_size;
+    // the span is the tile's whole list: every other tile is empty
+    std::vector<std::uint32_t> idx(tile_pairs.size());
+    for (std::size_t i = 0; i < idx.size(); ++i) idx[i] = tile_pairs[i].splat_index;
+    std::vector<std::uint32_t> ranges(2 * static_cast<std::size_t>(grid.tile_count()), 0u);
+    ranges[2 * tile_index + 1] = static_cast<std::uint32_t>(idx.size());
+    std::vector<agsx_splat_view> sv(splats.size());
+    static_assert(sizeof(SplatView) == sizeof(agsx_splat_view), "SplatView layout");
+    if (!splats.empty()) std::memcpy(sv.data(), splats.data(), splats.size() * sizeof(agsx_splat_view));
+    Image img(grid.width, grid.height);
+    std::vector<float> mt;
+    if (max_t) mt.assign(splats.size(), 0.0f);
+    check(agsx_raster(ctx, sv.data(), sv.size(), idx.data(), idx.size(), ranges.data(), grid.width, grid.height, &k,
+                      img.data.data(), max_t ? mt.data() : nullptr),
+          ctx);
+    for (int y = y0; y < y0 + h; ++y)
+        std::memcpy(&out.data[(static_cast<std::size_t>(y) * out.width + x0) * 3],
+                    &img.data[(static_cast<std::size_t>(y) * img.width + x0) * 3], static_cast<std::size_t>(w) * 12);
+    if (max_t) {
+        if (max_t->size() < splats.size()) max_t->resize(splats.size(), 0.0f);
+        for (std::size_t i = 0; i < mt.size(); ++i) (*max_t)[i] = std::max((*max_t)[i], mt[i]);
+    }
+}
+
+// --------------------------------------------------- device-scene cache
+namespace {
+
+// FNV-1a over the bytes of up to 1024 evenly spaced Gaussians (every field,
+// SH included) and the count.
+std::uint64_t scene_fingerprint(std::span<const Gaussian3D> scene) {
+    std::uint64_t h = 1469598103934665603ull;
+    auto mix = [&](const void* p, std::size_t n) {
+        const auto* b = static_cast<const unsigned char*>(p);
+        for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
+    };
+    const std::size_t n = scene.size();
+    mix(&n, sizeof(n));
+    const std::size_t samples = std::min<std::size_t>(n, 1024);
+    for (std::size_t s = 0; s < samples; ++s) {
+        const Gaussian3D& g = scene[samples == n ? s : (s * (n - 1)) / (samples - 1)];
+        mix(&g.mean, sizeof(g.mean));
+        mix(&g.scale, sizeof(g.scale));
+        mix(&g.rotation, sizeof(g.rotation));
+        mix(&g.opacity, sizeof(g.opacity));
+        mix(g.sh.data(), g.sh.size() * sizeof(float));
+    }
+    return h;
+}
+
+struct SceneCache {
+    const Gaussian3D* data = nullptr;
+    std::size_t size = 0;
+    std::uint64_t fp = 0;
+    std::unique_ptr<DeviceScene> dev;
+};
+
+SceneCache& scene_cache() {
+    static thread_local SceneCache c;  // per host thread, like the C-ABI context
+    return c;
+}
+
+bool cache_enabled() {
+    const char* e = std::getenv("AGS_SCENE_CACHE");
+    return !(e && *e == '0');
+}
+
+}  // namespace
+
+void forget_device_scenes() { scene_cache().dev.reset(); }
+
+RenderReport render(std::span<const Gaussian3D> scene, const Camera& cam, const RenderConfig& cfg,
+                    const TUpperLUT* lut, const RecordOptions& rec) {
+    if (const std::string bad = validate(cfg); !bad.empty()) throw std::invalid_argument("render: " + bad);
+    if (const std::string bad = validate(cam); !bad.empty()) throw std::invalid_argument("render: " + bad);
+    if (!cache_enabled()) {
+        const DeviceScene dev(scene);
+        return render(dev, cam, cfg, lut, rec);
+    }
+    SceneCache& c = scene_cache();
+    const std::uint64_t fp = scene_fingerprint(scene);
+    if (!c.dev || c.data != scene.data() || c.size != scene.size() || c.fp != fp) {
+        c.dev.reset();  // free the previous copy before uploading the next
+        c.dev = std::make_unique<DeviceScene>(scene);
+        c.data = scene.data();
+        c.size = scene.size();
+        c.fp = fp;
+    }
+    return render(*c.dev, cam, cfg, lut, rec);
+}
+
+}  // namespace ags
+
+// Bench entry (bench.py e2e.cxx_span): the reference-facing C++ call
+// ags::render(std::span<const Gaussian3D>, ...) on a synthetic scene built as
+// the reference's AoS vector, timed on the host over `iters` calls after one
+// warm-up call (scene upload included in the first call only when the cache
+// is on).  Returns seconds per call, the first (cold) call's seconds, and the
+// frame's pair count.
+extern "C" int ags_bench_render_span(std::uint64_t seed, int count, const char* layout, int camera_count, int width,
+                                     int height, float focal, int mode, float k, const float* lut_bins, int n_bins,
+                                     int iters, int use_cache, double* sec_per_call, double* first_call_sec,
+                                     std::uint64_t* pair_count) {
+    try {
+        ags::SynthSpec spec;
+        spec.layout = layout;
+        spec.camera_count = camera_count;
+        spec.width = width;
+        spec.height = height;
+        spec.fx = spec.fy = focal;
+        const ags::SynthScene sc = ags::synth_scene(seed, count, spec);
+        ags::RenderConfig cfg;
+        cfg.mode = static_cast<ags::Mode>(mode);
+        cfg.k = k;
+        ags::TUpperLUT lut;
+        if (n_bins > 0) lut.bins.assign(lut_bins, lut_bins + n_bins);
+        const ags::TUpperLUT* lp = cfg.mode == ags::Mode::AdaGScale ? &lut : nullptr;
+        if (!use_cache) setenv("AGS_SCENE_CACHE", "0", 1);
+        ags::forget_device_scenes();
+        auto t0 = std::chrono::steady_clock::now();
+        ags::RenderReport rep = ags::render(sc.gaussians, sc.cameras[0], cfg, lp);
+        *first_call_sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        t0 = std::chrono::steady_clock::now();
+        for (int i = 0; i < iters; ++i) rep = ags::render(sc.gaussians, sc.cameras[0], cfg, lp);
+        *sec_per_call = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / std::max(iters, 1);
+        *pair_count = rep.pair_count;
+        if (!use_cache) unsetenv("AGS_SCENE_CACHE");
+        ags::forget_device_scenes();
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}

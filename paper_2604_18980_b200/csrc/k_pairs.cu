@@ -310,6 +310,36 @@ __global__ void k_ranges_u64(const uint64_t* __restrict__ keys, uint64_t n, uint
     }
 }
 
+// alpha_at (rasterizer.hpp:44-50) with glibc expf, for n (splat, pixel
+// centre) pairs: the decision function of raster_tile.
+__global__ void k_alpha_at(const agsx_splat_view* __restrict__ s, const float* __restrict__ px, uint64_t n,
+                           float aclamp, float* __restrict__ alpha) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const agsx_splat_view v = s[i];
+    const float dx = px[2 * i] - v.mean2d[0], dy = px[2 * i + 1] - v.mean2d[1];
+    const float power = -0.5f * quad_form(v.inv_cov[0], v.inv_cov[1], v.inv_cov[2], dx, dy);
+    float a = 0.0f;
+    if (!(power > 0.0f)) {
+        a = v.opacity * glibc_expf(power);
+        a = a < aclamp ? a : aclamp;
+    }
+    alpha[i] = a;
+}
+
+// effective_radius (pair_gen.cpp:11-16): r = sqrt(2 ln(opacity / th)) with
+// glibc logf, pixels = r sqrt(max(lambda_max(cov2d), 0)).
+__global__ void k_effective_radius(const float* __restrict__ opacity, const float* __restrict__ th,
+                                   const float* __restrict__ cov, uint64_t n, float* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float r = sqrtf(2.0f * glibc_logf(opacity[i] / th[i]));
+    float l1, l2, v1x, v1y;
+    eigen_sym2(cov[3 * i], cov[3 * i + 1], cov[3 * i + 2], l1, l2, v1x, v1y);
+    out[2 * i] = r;
+    out[2 * i + 1] = r * sqrtf(smax(l1, 0.0f));
+}
+
 __global__ void k_logf(const float* __restrict__ x, float* __restrict__ y, uint64_t n) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x)

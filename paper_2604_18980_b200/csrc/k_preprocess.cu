@@ -81,6 +81,108 @@ __device__ __forceinline__ void eval_color(const DevScene& sc, uint64_t i, float
     rgb[2] = sclamp(b + 0.5f, 0.0f, 1.0f);
 }
 
+// project (preprocess.cpp:26-66) from the camera-space offset d = mean -
+// position: false when behind the near plane or outside the guard band
+// (preprocess.cpp:31-39); else the 2D mean (float) and the EWA covariance
+// upper 2x2 of J W Sigma W^T J^T + 0.3 I (double, cast to float).
+__device__ __forceinline__ bool project_dev(const FrameParams& p, float dx, float dy, float dz, float4 q, float4 sr,
+                                            float& tz_out, float& m2x, float& m2y, float& cxx, float& cxy,
+                                            float& cyy) {
+    // to_camera (scene.hpp:41-43, Mat3f*Vec3f math.hpp:43-49)
+    const float tx = p.R[0] * dx + p.R[1] * dy + p.R[2] * dz;
+    const float ty = p.R[3] * dx + p.R[4] * dy + p.R[5] * dz;
+    const float tz = p.R[6] * dx + p.R[7] * dy + p.R[8] * dz;
+    tz_out = tz;
+    if (tz <= p.near_plane) return false;
+    {
+        const float inv_z = 1.0f / tz;
+        m2x = p.fx * tx * inv_z + p.ppx;
+        m2y = p.fy * ty * inv_z + p.ppy;
+        const float ndc_x = (m2x - p.ppx) / p.ppx;
+        const float ndc_y = (m2y - p.ppy) / p.ppy;
+        if (fabsf(ndc_x) > p.guard || fabsf(ndc_y) > p.guard) return false;
+    }
+    // Jacobian at the clamped point, double precision (preprocess.cpp:42-57)
+    const double iz = 1.0 / static_cast<double>(tz);
+    const double txc = sclampd(tx * iz, -p.lim_x, p.lim_x) * tz;
+    const double tyc = sclampd(ty * iz, -p.lim_y, p.lim_y) * tz;
+    const double j00 = p.fxd * iz, j01 = 0.0, j02 = -p.fxd * txc * iz * iz;
+    const double j10 = 0.0, j11 = p.fyd * iz, j12 = -p.fyd * tyc * iz * iz;
+    // jw = J * W  (rows 0, 1; Mat3 product math.hpp:50-59, s = 0 then +=)
+    double jw[2][3];
+    for (int c = 0; c < 3; ++c) {
+        const double w0 = p.Rd[c], w1 = p.Rd[3 + c], w2 = p.Rd[6 + c];
+        double s = 0.0;
+        s += j00 * w0;
+        s += j01 * w1;
+        s += j02 * w2;
+        jw[0][c] = s;
+        s = 0.0;
+        s += j10 * w0;
+        s += j11 * w1;
+        s += j12 * w2;
+        jw[1][c] = s;
+    }
+    // covariance_3d (scene.cpp:31-39) with rotation_matrix<double> (math.hpp:147-164)
+    const double n = sqrt(static_cast<double>(q.x) * q.x + static_cast<double>(q.y) * q.y +
+                          static_cast<double>(q.z) * q.z + static_cast<double>(q.w) * q.w);
+    const double qw = q.x / n, qx = q.y / n, qy = q.z / n, qz = q.w / n;
+    double rs[9];
+    rs[0] = 1 - 2 * (qy * qy + qz * qz);
+    rs[1] = 2 * (qx * qy - qw * qz);
+    rs[2] = 2 * (qx * qz + qw * qy);
+    rs[3] = 2 * (qx * qy + qw * qz);
+    rs[4] = 1 - 2 * (qx * qx + qz * qz);
+    rs[5] = 2 * (qy * qz - qw * qx);
+    rs[6] = 2 * (qx * qz - qw * qy);
+    rs[7] = 2 * (qy * qz + qw * qx);
+    rs[8] = 1 - 2 * (qx * qx + qy * qy);
+    for (int row = 0; row < 3; ++row) {
+        rs[row * 3 + 0] *= sr.x;
+        rs[row * 3 + 1] *= sr.y;
+        rs[row * 3 + 2] *= sr.z;
+    }
+    double cov[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            double s = 0.0;
+            s += rs[r * 3 + 0] * rs[c * 3 + 0];
+            s += rs[r * 3 + 1] * rs[c * 3 + 1];
+            s += rs[r * 3 + 2] * rs[c * 3 + 2];
+            cov[r * 3 + c] = s;
+        }
+    // sigma = (jw * cov) * jw^T, entries (0,0), (0,1), (1,1)
+    double t[2][3];
+    for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 3; ++c) {
+            double s = 0.0;
+            s += jw[r][0] * cov[0 * 3 + c];
+            s += jw[r][1] * cov[1 * 3 + c];
+            s += jw[r][2] * cov[2 * 3 + c];
+            t[r][c] = s;
+        }
+    double s00 = 0.0, s01 = 0.0, s11 = 0.0;
+    s00 += t[0][0] * jw[0][0];
+    s00 += t[0][1] * jw[0][1];
+    s00 += t[0][2] * jw[0][2];
+    s01 += t[0][0] * jw[1][0];
+    s01 += t[0][1] * jw[1][1];
+    s01 += t[0][2] * jw[1][2];
+    s11 += t[1][0] * jw[1][0];
+    s11 += t[1][1] * jw[1][1];
+    s11 += t[1][2] * jw[1][2];
+    cxx = static_cast<float>(s00 + 0.3);
+    cxy = static_cast<float>(s01);
+    cyy = static_cast<float>(s11 + 0.3);
+    return true;
+}
+
+// compute_th, Eq. 10 (preprocess.cpp:107-116): K / (T_upper * 2 pi sqrt(det)) + tau
+__device__ __forceinline__ float compute_th_dev(float t_upper, float det, float k, float tau) {
+    const float denom = t_upper * 2.0f * 3.14159265358979323846f * sqrtf(det);
+    return k / denom + tau;
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(256, AGSX_PRE_MINB)
@@ -109,103 +211,16 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         const float4 sr = sc.scale_r[i];
         const float2 gb = sc.sh_gb[i];  // issued with the other loads
         const float opacity = po.w;
-        // to_camera (scene.hpp:41-43, Mat3f*Vec3f math.hpp:43-49)
+        // to_camera (scene.hpp:41-43): t = R (mean - position), float
         const float dx = po.x - p.cam_pos[0], dy = po.y - p.cam_pos[1], dz = po.z - p.cam_pos[2];
-        const float tx = p.R[0] * dx + p.R[1] * dy + p.R[2] * dz;
-        const float ty = p.R[3] * dx + p.R[4] * dy + p.R[5] * dz;
-        const float tz = p.R[6] * dx + p.R[7] * dy + p.R[8] * dz;
-        bool ok = !(tz <= p.near_plane);
-        float m2x = 0.0f, m2y = 0.0f;
+        float tz = 0.0f, m2x = 0.0f, m2y = 0.0f, cxx = 0.0f, cxy = 0.0f, cyy = 0.0f, det = 0.0f, th = p.tau;
+        bool ok = project_dev(p, dx, dy, dz, q, sr, tz, m2x, m2y, cxx, cxy, cyy);
         if (ok) {
-            const float inv_z = 1.0f / tz;
-            m2x = p.fx * tx * inv_z + p.ppx;
-            m2y = p.fy * ty * inv_z + p.ppy;
-            const float ndc_x = (m2x - p.ppx) / p.ppx;
-            const float ndc_y = (m2y - p.ppy) / p.ppy;
-            ok = !(fabsf(ndc_x) > p.guard || fabsf(ndc_y) > p.guard);
-        }
-        float cxx = 0.0f, cxy = 0.0f, cyy = 0.0f, det = 0.0f, th = p.tau;
-        if (ok) {
-            // Jacobian at the clamped point, double precision (preprocess.cpp:42-57)
-            const double iz = 1.0 / static_cast<double>(tz);
-            const double txc = sclampd(tx * iz, -p.lim_x, p.lim_x) * tz;
-            const double tyc = sclampd(ty * iz, -p.lim_y, p.lim_y) * tz;
-            const double j00 = p.fxd * iz, j01 = 0.0, j02 = -p.fxd * txc * iz * iz;
-            const double j10 = 0.0, j11 = p.fyd * iz, j12 = -p.fyd * tyc * iz * iz;
-            // jw = J * W  (rows 0, 1; Mat3 product math.hpp:50-59, s = 0 then +=)
-            double jw[2][3];
-            for (int c = 0; c < 3; ++c) {
-                const double w0 = p.Rd[c], w1 = p.Rd[3 + c], w2 = p.Rd[6 + c];
-                double s = 0.0;
-                s += j00 * w0;
-                s += j01 * w1;
-                s += j02 * w2;
-                jw[0][c] = s;
-                s = 0.0;
-                s += j10 * w0;
-                s += j11 * w1;
-                s += j12 * w2;
-                jw[1][c] = s;
-            }
-            // covariance_3d (scene.cpp:31-39) with rotation_matrix<double> (math.hpp:147-164)
-            const double n = sqrt(static_cast<double>(q.x) * q.x + static_cast<double>(q.y) * q.y +
-                                  static_cast<double>(q.z) * q.z + static_cast<double>(q.w) * q.w);
-            const double qw = q.x / n, qx = q.y / n, qy = q.z / n, qz = q.w / n;
-            double rs[9];
-            rs[0] = 1 - 2 * (qy * qy + qz * qz);
-            rs[1] = 2 * (qx * qy - qw * qz);
-            rs[2] = 2 * (qx * qz + qw * qy);
-            rs[3] = 2 * (qx * qy + qw * qz);
-            rs[4] = 1 - 2 * (qx * qx + qz * qz);
-            rs[5] = 2 * (qy * qz - qw * qx);
-            rs[6] = 2 * (qx * qz - qw * qy);
-            rs[7] = 2 * (qy * qz + qw * qx);
-            rs[8] = 1 - 2 * (qx * qx + qy * qy);
-            for (int row = 0; row < 3; ++row) {
-                rs[row * 3 + 0] *= sr.x;
-                rs[row * 3 + 1] *= sr.y;
-                rs[row * 3 + 2] *= sr.z;
-            }
-            double cov[9];
-            for (int r = 0; r < 3; ++r)
-                for (int c = 0; c < 3; ++c) {
-                    double s = 0.0;
-                    s += rs[r * 3 + 0] * rs[c * 3 + 0];
-                    s += rs[r * 3 + 1] * rs[c * 3 + 1];
-                    s += rs[r * 3 + 2] * rs[c * 3 + 2];
-                    cov[r * 3 + c] = s;
-                }
-            // sigma = (jw * cov) * jw^T, entries (0,0), (0,1), (1,1)
-            double t[2][3];
-            for (int r = 0; r < 2; ++r)
-                for (int c = 0; c < 3; ++c) {
-                    double s = 0.0;
-                    s += jw[r][0] * cov[0 * 3 + c];
-                    s += jw[r][1] * cov[1 * 3 + c];
-                    s += jw[r][2] * cov[2 * 3 + c];
-                    t[r][c] = s;
-                }
-            double s00 = 0.0, s01 = 0.0, s11 = 0.0;
-            s00 += t[0][0] * jw[0][0];
-            s00 += t[0][1] * jw[0][1];
-            s00 += t[0][2] * jw[0][2];
-            s01 += t[0][0] * jw[1][0];
-            s01 += t[0][1] * jw[1][1];
-            s01 += t[0][2] * jw[1][2];
-            s11 += t[1][0] * jw[1][0];
-            s11 += t[1][1] * jw[1][1];
-            s11 += t[1][2] * jw[1][2];
-            cxx = static_cast<float>(s00 + 0.3);
-            cxy = static_cast<float>(s01);
-            cyy = static_cast<float>(s11 + 0.3);
             det = cxx * cyy - cxy * cxy;
             ok = det > 0.0f;
         }
         if (ok && p.adaptive) {
-            // compute_th, Eq. 10 (preprocess.cpp:107-116)
-            const float t_upper = lut_value(p, tz);
-            const float denom = t_upper * 2.0f * 3.14159265358979323846f * sqrtf(det);
-            th = p.k / denom + p.tau;
+            th = compute_th_dev(lut_value(p, tz), det, p.k, p.tau);  // Eq. 10
         }
         if (ok && th >= opacity) ok = false;
         uint32_t cnt = 0;
@@ -302,6 +317,47 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
     }
     const uint32_t alive_cnt = __popc(__ballot_sync(0xffffffffu, alive));
     if (alive_cnt && lane == 0) atomicAdd(&ctr->s, alive_cnt);
+}
+
+// ---- exported helpers (agsx_project / agsx_eval_color / agsx_compute_th):
+// the device functions K1 uses, one element per thread.
+
+// project (preprocess.cpp:26-66): valid[i] and {mean2d.x, mean2d.y, cov2d.xx,
+// cov2d.xy, cov2d.yy, depth} per Gaussian.
+__global__ void k_project(FrameParams p, DevScene sc, uint8_t* __restrict__ valid, float* __restrict__ out) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= sc.n) return;
+    const float4 po = sc.pos_op[i];
+    const float dx = po.x - p.cam_pos[0], dy = po.y - p.cam_pos[1], dz = po.z - p.cam_pos[2];
+    float tz = 0.0f, m2x = 0.0f, m2y = 0.0f, cxx = 0.0f, cxy = 0.0f, cyy = 0.0f;
+    const bool ok = project_dev(p, dx, dy, dz, sc.rot[i], sc.scale_r[i], tz, m2x, m2y, cxx, cxy, cyy);
+    valid[i] = ok ? 1u : 0u;
+    float* o = out + 6 * i;
+    o[0] = m2x;
+    o[1] = m2y;
+    o[2] = cxx;
+    o[3] = cxy;
+    o[4] = cyy;
+    o[5] = tz;
+}
+
+// eval_color (preprocess.cpp:68-105) for a caller-given unit view direction.
+__global__ void k_eval_color(DevScene sc, const float* __restrict__ dirs, float* __restrict__ rgb) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= sc.n) return;
+    const float2 gb = sc.sh_gb[i];
+    eval_color(sc, i, sc.scale_r[i].w, gb.x, gb.y, dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2], rgb + 3 * i);
+}
+
+// compute_th (preprocess.cpp:107-116) with the frame's LUT, k and tau;
+// th = NaN where det(cov2d) <= 0 (the host raises invalid_argument).
+__global__ void k_compute_th(FrameParams p, const float* __restrict__ cov, const float* __restrict__ depth,
+                             uint64_t n, float* __restrict__ th) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float xx = cov[3 * i], xy = cov[3 * i + 1], yy = cov[3 * i + 2];
+    const float det = xx * yy - xy * xy;  // SymMat2::det (math.hpp:83)
+    th[i] = det > 0.0f ? compute_th_dev(lut_value(p, depth[i]), det, p.k, p.tau) : __int_as_float(0x7fc00000);
 }
 
 // Scene upload: host SoA (agsx_scene_desc) -> device planes.

@@ -161,6 +161,14 @@ __global__ void k_sq_err_final(const double* partial, int n, double* out);
 __global__ void k_quantize_u8(const float4* img, uint4* dst, uint64_t n16);
 __global__ void k_quantize_u8_tail(const float* img, uint8_t* dst, uint64_t lo, uint64_t n);
 
+// exported helpers (agsx_stage_api.cu): the device functions of K1 / pair
+// generation / the rasterizer, one element per thread
+__global__ void k_project(FrameParams p, DevScene sc, uint8_t* valid, float* out);
+__global__ void k_eval_color(DevScene sc, const float* dirs, float* rgb);
+__global__ void k_compute_th(FrameParams p, const float* cov, const float* depth, uint64_t n, float* th);
+__global__ void k_alpha_at(const agsx_splat_view* s, const float* px, uint64_t n, float aclamp, float* alpha);
+__global__ void k_effective_radius(const float* opacity, const float* th, const float* cov, uint64_t n, float* out);
+
 __global__ void k_logf(const float* x, float* y, uint64_t n);
 __global__ void k_expf(const float* x, float* y, uint64_t n);
 
