@@ -274,7 +274,8 @@ def cub_comparator(r, scene, view, mode, k, bins, exact, iters=20):
     lib = ctypes.CDLL(so)
     lib.cub_sort_pairs_u64.restype = ctypes.c_int
     lib.cub_sort_pairs_u64.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_uint64, ctypes.c_int, ctypes.c_int,
-                                                               ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
+                                                               ctypes.c_int, ctypes.POINTER(ctypes.c_float),
+                                                               ctypes.c_void_p]
     res = {}
     for label, (md, kk, bb) in (("adagscale_on", (mode, k, bins)), ("adagscale_off", ("ellipse", 0.0, []))):
         if label == "adagscale_on" and mode != "adagscale":
@@ -293,8 +294,9 @@ def cub_comparator(r, scene, view, mode, k, bins, exact, iters=20):
         kin, vin = kd[order].contiguous(), gd[order].to(torch.int32).contiguous()
         kout, vout = torch.empty_like(kin), torch.empty_like(vin)
         ms = ctypes.c_float(0.0)
+        # on torch's current stream: ordered after the gathers that built kin / vin
         rc = lib.cub_sort_pairs_u64(kin.data_ptr(), vin.data_ptr(), kout.data_ptr(), vout.data_ptr(), p, 0,
-                                    32 + tb, iters, ctypes.byref(ms))
+                                    32 + tb, iters, ctypes.byref(ms), torch.cuda.current_stream().cuda_stream)
         torch.cuda.synchronize()
         same = bool(torch.equal(kout, kd) and torch.equal(vout.to(torch.int64), gd))
         cub_ms = float(ms.value)

@@ -10,10 +10,11 @@
 
 extern "C" int cub_sort_pairs_u64(const uint64_t* keys_in, const uint32_t* vals_in, uint64_t* keys_out,
                                   uint32_t* vals_out, uint64_t n, int begin_bit, int end_bit, int iters,
-                                  float* ms_per_sort) {
+                                  float* ms_per_sort, void* stream) {
+    // `stream` is the caller's (torch's current) stream, so the sort is
+    // ordered after the kernels that prepared keys_in / vals_in
     if (n > 0x7fffffffull) return 1;
-    cudaStream_t st;
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return 2;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     size_t temp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, temp, keys_in, keys_out, vals_in, vals_out, static_cast<int>(n),
                                     begin_bit, end_bit, st);
@@ -37,6 +38,5 @@ extern "C" int cub_sort_pairs_u64(const uint64_t* keys_in, const uint32_t* vals_
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(d_temp);
-    cudaStreamDestroy(st);
     return e == cudaSuccess ? 0 : 4;
 }
