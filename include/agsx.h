@@ -15,6 +15,9 @@
  *   AGSX_ECUDA         3  -> std::runtime_error
  *   AGSX_ENOMEM        4  -> std::runtime_error (std::bad_alloc)
  *   AGSX_ECAPACITY     5  caller buffer too small; required size returned
+ *   AGSX_EFRAME_LOST   6  -> std::runtime_error: an earlier frame of an async
+ *                         chain (frames enqueued since the last wait)
+ *                         overflowed the pair arena and was not rasterised
  *
  * Threading: one agsx_ctx per host thread per GPU; a ctx owns one CUDA
  * stream and grow-only device arenas.  Scenes are immutable once uploaded
@@ -38,7 +41,8 @@ enum {
     AGSX_EPAIR_BUDGET = 2,
     AGSX_ECUDA = 3,
     AGSX_ENOMEM = 4,
-    AGSX_ECAPACITY = 5
+    AGSX_ECAPACITY = 5,
+    AGSX_EFRAME_LOST = 6
 };
 
 /* ags::Mode (scene.hpp:60); values equal the reference enum order. */

@@ -859,7 +859,8 @@ typedef struct {
 
 static void raster_tile(const ago_splat* splats, const uint32_t* idx,
                         uint32_t begin, uint32_t end, const grid_t* g, int tile,
-                        const ago_config* cfg, float* image, float* max_t, blend_sink* sink) {
+                        const ago_config* cfg, float* image, float* max_t, blend_sink* sink,
+                        uint64_t* p_it) {
     const int tx = tile % g->tiles_x, ty = tile / g->tiles_x;
     const int x0 = tx * g->tile_size, y0 = ty * g->tile_size;
     const int w = mini_(g->tile_size, g->width - x0);
@@ -873,6 +874,7 @@ static void raster_tile(const ago_splat* splats, const uint32_t* idx,
     int active = npx;
     for (uint32_t p = begin; p < end; ++p) {
         if (active == 0) break;
+        if (p_it) ++*p_it; /* pairs the tile loop visits (rasterizer.cpp:55-56) */
         const ago_splat* s = &splats[idx[p]];
         for (int iy = 0; iy < h; ++iy) {
             const float py = (float)(y0 + iy) + 0.5f;
@@ -917,13 +919,13 @@ static void raster_tile(const ago_splat* splats, const uint32_t* idx,
 
 static void raster_all(const ago_splat* splats, uint64_t n_splats, const uint32_t* splat_index,
                        const uint32_t* ranges, int32_t width, int32_t height, const ago_config* cfg,
-                       float* image, float* max_t, blend_sink* sink) {
+                       float* image, float* max_t, blend_sink* sink, uint64_t* p_it) {
     const grid_t g = make_grid(width, height, cfg->tile_size);
     if (max_t) memset(max_t, 0, sizeof(float) * n_splats);
     memset(image, 0, sizeof(float) * 3 * (size_t)width * height);
     for (int t = 0; t < g.tiles_x * g.tiles_y; ++t) /* tile-index order (rasterizer.cpp:155-161) */
         raster_tile(splats, splat_index, ranges[2 * t], ranges[2 * t + 1], &g, t,
-                    cfg, image, max_t, sink);
+                    cfg, image, max_t, sink, p_it);
 }
 
 int ago_raster(const ago_splat* splats, uint64_t n_splats,
@@ -933,7 +935,18 @@ int ago_raster(const ago_splat* splats, uint64_t n_splats,
                float* max_t) {
     (void)keys;
     (void)n_pairs;
-    raster_all(splats, n_splats, splat_index, ranges, width, height, cfg, image, max_t, NULL);
+    raster_all(splats, n_splats, splat_index, ranges, width, height, cfg, image, max_t, NULL, NULL);
+    return AGO_OK;
+}
+
+/* P_it: the pairs raster_tile visits before every pixel of its tile is
+ * saturated (the `active == 0` break, rasterizer.cpp:55-56), summed over the
+ * tiles -- the raster's work measure. */
+int ago_raster_pit(const ago_splat* splats, uint64_t n_splats, const uint32_t* splat_index,
+                   const uint32_t* ranges, int32_t width, int32_t height, const ago_config* cfg,
+                   float* image, uint64_t* p_it) {
+    *p_it = 0;
+    raster_all(splats, n_splats, splat_index, ranges, width, height, cfg, image, NULL, NULL, p_it);
     return AGO_OK;
 }
 
@@ -963,7 +976,7 @@ static int render_impl(const ago_scene* scene, const ago_camera* cam,
                             keys, idx, total, counts, &total);
     uint32_t* ranges = (uint32_t*)malloc(sizeof(uint32_t) * 2 * (size_t)g.tiles_x * g.tiles_y);
     ago_sort_pairs(keys, idx, total, g.tiles_x * g.tiles_y, ranges);
-    raster_all(splats, ns, idx, ranges, cam->width, cam->height, cfg, image, max_t, sink);
+    raster_all(splats, ns, idx, ranges, cam->width, cam->height, cfg, image, max_t, sink, NULL);
     *pair_count = total;
     *splat_count = ns;
     if (stage_s) stage_s[0] = stage_s[1] = stage_s[2] = stage_s[3] = 0.0;

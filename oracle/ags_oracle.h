@@ -125,6 +125,11 @@ int ago_raster(const ago_splat* splats, uint64_t n_splats,
                uint64_t n_pairs, const uint32_t* ranges, int32_t width,
                int32_t height, const ago_config* cfg, float* image,
                float* max_t);
+/* the same raster, and P_it: the pairs every tile's loop visits before all
+ * of its pixels are saturated (rasterizer.cpp:55-56), summed over tiles. */
+int ago_raster_pit(const ago_splat* splats, uint64_t n_splats, const uint32_t* splat_index,
+                   const uint32_t* ranges, int32_t width, int32_t height, const ago_config* cfg,
+                   float* image, uint64_t* p_it);
 
 /* render (rasterizer.cpp:102-165).  image: H*W*3; max_t optional (scene
  * count entries; indexed by *compacted* splat index).  stage_s: 4 doubles

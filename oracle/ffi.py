@@ -187,6 +187,9 @@ class Oracle:
             C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
             C.c_int32, C.c_int32, C.POINTER(Config), C.c_void_p, C.c_void_p,
         ]
+        if hasattr(L, "ago_raster_pit"):  # the C restatement only
+            L.ago_raster_pit.argtypes = [C.c_void_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                         C.POINTER(Config), C.c_void_p, C.POINTER(C.c_uint64)]
         L.ago_render.argtypes = [
             C.POINTER(SceneDesc), C.POINTER(Camera), C.POINTER(Config),
             C.POINTER(Lut), C.c_void_p, C.POINTER(C.c_uint64),
@@ -292,6 +295,20 @@ class Oracle:
         if rc:
             raise OracleError(rc, "raster")
         return (img, mt[: len(splats)]) if max_t else img
+
+    def raster_pit(self, splats, idx, ranges, width, height, cfg):
+        """P_it of the raster (rasterizer.cpp:55-56): pairs visited before each
+        tile saturates, summed over the tiles; returns (image, p_it)."""
+        splats = np.ascontiguousarray(splats, SPLAT_DTYPE)
+        img = np.zeros((height, width, 3), np.float32)
+        idx = np.ascontiguousarray(idx, np.uint32)
+        ranges = np.ascontiguousarray(ranges, np.uint32)
+        pit = C.c_uint64()
+        rc = self.lib.ago_raster_pit(_p(splats), len(splats), _p(idx), _p(ranges), width, height, C.byref(cfg),
+                                     _p(img), C.byref(pit))
+        if rc:
+            raise OracleError(rc, "raster_pit")
+        return img, pit.value
 
     def render(self, scene: SoAScene, cam, cfg, lut=None, max_t=False):
         img = np.zeros((cam.height, cam.width, 3), np.float32)

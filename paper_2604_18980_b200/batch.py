@@ -38,23 +38,79 @@ def merge_rows(parts: Sequence[list]) -> list:
     return out
 
 
-def pair_report(local_report: LocalReport, n_views: int, group=None) -> list:
+def merge_folds(folds: Sequence[dict]) -> dict:
+    """Merge build_lut folds of view blocks (``Renderer.fold_max_t``) into the
+    LUT of all the views: per bin the max of max_t over the blocks, 1.0 where
+    no block saw a blended splat (calibrate.cpp:14-41). Max is associative,
+    so the result equals the single-process LUT bit for bit."""
+    folds = [f for f in folds if f]
+    if not folds:
+        raise ValueError("no folds to merge")
+    nb = len(folds[0]["folded"])
+    bins = []
+    for b in range(nb):
+        seen = [f["folded"][b] for f in folds if f["observed"][b]]
+        bins.append(max(seen) if seen else 1.0)
+    return {"lut_bins": bins, "lut_depth_min": folds[0]["depth_min"], "lut_depth_max": folds[0]["depth_max"]}
+
+
+def pair_report(local_report: LocalReport, n_views: int, group=None, fold=None) -> list:
     """The whole path's report: views [0, n_views) split over the group's ranks.
 
     Every rank returns the merged rows. ``local_report`` is usually
-    ``lambda views: renderer.pair_report(scene, specs, views=list(views), ...)``.
+    ``lambda views, **lut: renderer.pair_report(scene, specs, views=list(views), **lut)``.
+
+    AdaGScale rows need one T-upper LUT built from ALL the views, as the
+    reference builds it (analysis.cpp:265-275). A rank's own block would give
+    another LUT, so rows that depend on the world size. With
+    ``fold(views) -> dict`` (``Renderer.fold_max_t``), every rank folds its own
+    block, the folds are all-gathered and merged (``merge_folds``), and
+    ``local_report(views, lut_bins=..., lut_depth_min=..., lut_depth_max=...)``
+    receives the merged LUT. Without ``fold``, ``local_report(views)`` is
+    called as is: pass a LUT yourself, or use ``device_pair_report``.
     """
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     views = partition_views(n_views, world, rank)
-    mine = local_report(views) if views else []
+    lut = None
+    if fold is not None:
+        mine_fold = fold(views) if views else None
+        if world == 1:
+            lut = merge_folds([mine_fold])
+        else:
+            folds = [None] * world
+            dist.all_gather_object(folds, mine_fold, group=group)
+            lut = merge_folds(folds)
+    if not views:
+        mine = []
+    elif lut is not None:
+        mine = local_report(views, **lut)
+    else:
+        mine = local_report(views)
     if world == 1:
         return merge_rows([mine])
     parts = [None] * world
     dist.all_gather_object(parts, mine, group=group)
     return merge_rows(parts)
+
+
+def device_pair_report(renderer, scene, specs, n_views: int | None = None, group=None, lut_bins=None,
+                       lut_depth_min: float = 0.0, lut_depth_max: float = 100.0) -> list:
+    """``pair_report`` (analysis.cpp:259-312) of ``scene``'s first ``n_views``
+    views on the group's GPUs, one ``Renderer`` per rank. Without ``lut_bins``,
+    AdaGScale specs get the LUT built from all the views across the ranks."""
+    n = scene.camera_count if n_views is None else n_views
+    needs_lut = any(str(s[0]) == "adagscale" for s in specs) and not lut_bins
+    fixed = {} if needs_lut or not lut_bins else {
+        "lut_bins": list(lut_bins), "lut_depth_min": lut_depth_min, "lut_depth_max": lut_depth_max}
+
+    def local(views, **lut):
+        return renderer.pair_report(scene, specs, views=list(views), **(lut or fixed))
+
+    fold = (lambda views: renderer.fold_max_t(scene, list(views))) if needs_lut else None
+    return pair_report(local, n, group=group, fold=fold)
 
 
 def render_views(renderers, scene, views: Sequence[int], on_frame=None, **kw) -> list:

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libagsx.so")
 
-OK, EINVAL, EPAIR_BUDGET, ECUDA, ENOMEM, ECAPACITY = 0, 1, 2, 3, 4, 5
+OK, EINVAL, EPAIR_BUDGET, ECUDA, ENOMEM, ECAPACITY, EFRAME_LOST = 0, 1, 2, 3, 4, 5, 6
 MODES = {"aabb": 0, "obb": 1, "ellipse": 2, "adagscale": 3}
 FLAG_EXACT_ALPHA = 1
 
@@ -307,6 +307,12 @@ class Context:
     def render_async(self, scene, cam, cfg, lut=None):
         self._check(self.L.agsx_render_async(self.h, scene, C.byref(cam), C.byref(cfg),
                                              C.byref(lut) if lut is not None else None))
+
+    def render_async_host(self, scene, cam, cfg, lut, image):
+        """agsx_render_async_host: the frame lands in `image` (float32 H x W x 3,
+        host memory) by agsx_render_wait; `image` must stay alive until then."""
+        self._check(self.L.agsx_render_async_host(self.h, scene, C.byref(cam), C.byref(cfg),
+                                                  C.byref(lut) if lut is not None else None, _p(image)))
 
     def wait(self):
         f = Frame()

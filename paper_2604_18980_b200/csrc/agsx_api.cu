@@ -53,8 +53,10 @@ int agsx_create(int device, agsx_ctx** out) {
         ctx->occ_tile_sort = std::max(ctx->occ_tile_sort, 1);
         for (auto& set : ctx->ev_ring)
             for (auto& e : set) AGSX_CUDA(cudaEventCreate(&e));
-        AGSX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ctr), sizeof(Counters)));
-        std::memset(ctx->h_ctr, 0, sizeof(Counters));
+        // the counter block + the two async-chain words behind it (ChainWords)
+        AGSX_CUDA(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_ctr), sizeof(Counters) + sizeof(ChainWords)));
+        std::memset(static_cast<void*>(ctx->h_ctr), 0, sizeof(Counters) + sizeof(ChainWords));
+        ensure(ctx->chain, sizeof(ChainWords), /*zero=*/true);
         AGSX_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->h_ctr_dev), ctx->h_ctr, 0));
         return AGSX_OK;
     });
@@ -75,7 +77,7 @@ void agsx_destroy(agsx_ctx* ctx) {
                    &ctx->dvals, &ctx->dkeys2, &ctx->dvals2, &ctx->dcounts, &ctx->chunks, &ctx->img_u8, &ctx->tkeys, &ctx->pvals, &ctx->tkeys2,
                    &ctx->pvals2, &ctx->ranges, &ctx->image, &ctx->lb, &ctx->ctr, &ctx->hist,
                    &ctx->maxt, &ctx->dump, &ctx->lut_ext, &ctx->tile_pit, &ctx->calib, &ctx->sort_counts, &ctx->tmp0, &ctx->tmp1, &ctx->tmp2,
-                   &ctx->tmp3, &ctx->tmp4, &ctx->bk_hits, &ctx->bk_gd, &ctx->ekeys, &ctx->ekeys2, &ctx->big_list})
+                   &ctx->tmp3, &ctx->tmp4, &ctx->bk_hits, &ctx->bk_gd, &ctx->ekeys, &ctx->ekeys2, &ctx->big_list, &ctx->chain})
         release(*b);
     for (auto& set : ctx->ev_ring)
         for (auto& e : set)
@@ -164,40 +166,6 @@ int agsx_render_async(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera*
                       const agsx_config* cfg, const agsx_lut* lut) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int { return start_frame(ctx, scene, cam, cfg, lut, false); });
-}
-
-// Experiment hook (not in agsx.h): the enqueued frame captured once as a CUDA
-// graph and replayed `iters` times; *ms = device time per replay.
-extern "C" int agsx_debug_graph_replay(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
-                                       const agsx_config* cfg, const agsx_lut* lut, int iters, float* ms) {
-    if (!ctx) return AGSX_EINVAL;
-    return guarded(ctx, [&]() -> int {
-        int rc = start_frame(ctx, scene, cam, cfg, lut, false);  // sizes the arenas
-        if (rc) return rc;
-        rc = finish_frame(ctx, nullptr);
-        if (rc) return rc;
-        cudaGraph_t g;
-        AGSX_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        enqueue_frame(ctx, scene, ctx->f_params, false, nullptr);
-        AGSX_CUDA(cudaStreamEndCapture(ctx->stream, &g));
-        cudaGraphExec_t ge;
-        AGSX_CUDA(cudaGraphInstantiate(&ge, g, 0));
-        cudaEvent_t a, b;
-        AGSX_CUDA(cudaEventCreate(&a));
-        AGSX_CUDA(cudaEventCreate(&b));
-        for (int i = 0; i < 3; ++i) AGSX_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        AGSX_CUDA(cudaEventRecord(a, ctx->stream));
-        for (int i = 0; i < iters; ++i) AGSX_CUDA(cudaGraphLaunch(ge, ctx->stream));
-        AGSX_CUDA(cudaEventRecord(b, ctx->stream));
-        AGSX_CUDA(cudaEventSynchronize(b));
-        AGSX_CUDA(cudaEventElapsedTime(ms, a, b));
-        *ms /= iters;
-        cudaEventDestroy(a);
-        cudaEventDestroy(b);
-        cudaGraphExecDestroy(ge);
-        cudaGraphDestroy(g);
-        return AGSX_OK;
-    });
 }
 
 int agsx_render_async_to(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
@@ -290,6 +258,8 @@ int agsx_render_contributions(agsx_ctx* ctx, const agsx_scene* scene, const agsx
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
         if (!cfg || !count) return fail(ctx, AGSX_EINVAL, "render_contributions: null config or count");
+        if (cfg->tile_size > 64)  // the tile's T and C live in shared memory
+            return fail(ctx, AGSX_EINVAL, "render_contributions: tile_size above 64 is not supported");
         agsx_config c = *cfg;
         c.flags |= AGSX_FLAG_EXACT_ALPHA;  // the stream records the reference's alpha values
         const bool maxt = out && out->max_t;

@@ -85,9 +85,10 @@ struct agsx_ctx {
     Buf ranges, image, lb, ctr, hist, maxt, dump, lut_ext, tile_pit, calib;
     Buf tmp0, tmp1, tmp2, tmp3, tmp4;
     Buf bk_hits, bk_gd, ekeys, ekeys2, big_list;  // tile-bucketed sort path
+    Buf chain;  // ChainWords of the frames enqueued since the last wait (never zeroed per frame)
     uint64_t pair_capacity = 0;
 
-    Counters* h_ctr = nullptr;  // pinned
+    Counters* h_ctr = nullptr;  // pinned; ChainWords follow it
     uint32_t* h_ctr_dev = nullptr;  // its device-mapped alias
     static constexpr int kRing = 64;  // frames of stage events kept for timing
     cudaEvent_t ev_ring[kRing][6] = {};
@@ -96,6 +97,7 @@ struct agsx_ctx {
 
     // most recent fused frame
     bool have_frame = false;
+    bool pending = false;  // a frame is enqueued and not yet waited for
     const agsx_scene* f_scene = nullptr;
     agsx_camera f_cam{};
     agsx_config f_cfg{};
@@ -205,6 +207,7 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
                 const agsx_lut* lut, bool maxt, float* host_image = nullptr, float* device_target = nullptr,
                 uint8_t* host_u8 = nullptr);
 int finish_frame(agsx_ctx* ctx, agsx_frame* out);
+int refuse_if_host_frame(agsx_ctx* ctx, const char* what);
 int quantize_to_host(agsx_ctx* ctx, uint8_t* image_u8);
 cudaError_t shared_copy_stream(int device, cudaStream_t* out);
 

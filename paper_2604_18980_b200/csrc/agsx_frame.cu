@@ -117,7 +117,8 @@ bool raster_uses_units(const FrameParams& p, bool maxt) {
 void launch_raster(agsx_ctx* ctx, const FrameParams& p, const uint2* ranges, const uint32_t* vals,
                    const float4* P0, const float4* P1, const float4* P2, float* image,
                    uint32_t* maxt, Counters* ctr, uint32_t* unit_ctr) {
-    const int grid = p.tiles_x * p.tiles_y;
+    const int nsub = (p.tile_size + 63) / 64;  // 64x64 blocks per tile (k_raster)
+    const int grid = p.tiles_x * p.tiles_y * nsub * nsub;
     if (grid == 0) return;
     const bool exact = (p.flags & AGSX_FLAG_EXACT_ALPHA) != 0;
     if (raster_uses_units(p, maxt != nullptr)) {
@@ -229,8 +230,6 @@ int prepare(agsx_ctx* ctx, const agsx_camera* cam, const agsx_config* cfg, const
     if (!bad.empty()) return fail(ctx, AGSX_EINVAL, "render: " + bad);
     if (cfg->mode == AGSX_MODE_ADAGSCALE && lut == nullptr)
         return fail(ctx, AGSX_EINVAL, "preprocess_view: adagscale mode requires a T-upper LUT");
-    if (cfg->tile_size > 64)
-        return fail(ctx, AGSX_EINVAL, "tile_size > 64 is not supported by the device rasterizer");
     const float* lut_dev = nullptr;
     if (lut && lut->bin_count > kLutInline) {
         ensure(ctx->lut_ext, lut->bin_count * sizeof(float));
@@ -267,8 +266,22 @@ bool depth_keys_wide_host(const Counters& c) {
     return c.kmax >= kmin && c.kmax - kmin >= (1u << 24);
 }
 
-__global__ void k_counters_out(const uint32_t* __restrict__ src, uint32_t* dst, int words) {
+// The frame's counter block to the mapped host words, plus the async-chain
+// words: this frame overflowed the pair arena when its pairs did not all fit
+// (K3 skipped emission); the chain count keeps that after the next frame's
+// memset, so a wait on a later frame still sees it.
+__global__ void k_counters_out(const uint32_t* __restrict__ src, uint32_t* dst, int words, ChainWords* chain) {
     for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+    if (threadIdx.x == 0) {
+        const Counters* c = reinterpret_cast<const Counters*>(src);
+        const uint32_t over = (c->overflow != 0u || c->p_eff != c->p) ? 1u : 0u;
+        ChainWords w = *chain;
+        w.overflowed += over;
+        w.frames += 1u;
+        *chain = w;
+        dst[words] = w.overflowed;
+        dst[words + 1] = w.frames;
+    }
 }
 
 // write_image quantisation of n floats (src, dst 16-byte aligned) on stream st
@@ -547,7 +560,7 @@ void enqueue_raster(agsx_ctx* ctx, const FrameParams& p, bool maxt, uint32_t* va
     // a small D2H copy would queue in the copy engine behind another frame's
     // 191 MB of image bands, and this frame would finish only after that one.
     k_counters_out<<<1, 64, 0, st>>>(reinterpret_cast<const uint32_t*>(ctr), ctx->h_ctr_dev,
-                                     static_cast<int>(sizeof(Counters) / 4));
+                                     static_cast<int>(sizeof(Counters) / 4), ptr<ChainWords>(ctx->chain));
     check_launch(ctx);
     ctx->f_tile_count = static_cast<int>(tiles);
     ctx->f_pit_tiles = raster_uses_units(p, maxt);
@@ -557,6 +570,7 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
                 const agsx_lut* lut, bool maxt, float* host_image, float* device_target, uint8_t* host_u8) {
     if (!sc) return fail(ctx, AGSX_EINVAL, "render: null scene");
     if (sc->device != ctx->device) return fail(ctx, AGSX_EINVAL, "scene lives on another device");
+    if (const int rc = refuse_if_host_frame(ctx, "render")) return rc;
     FrameParams p;
     const int rc = prepare(ctx, cam, cfg, lut, p);
     if (rc) return rc;
@@ -565,6 +579,7 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
                          cfg->mode == AGSX_MODE_OBB, cfg->pair_budget);
     if (maxt) ensure(ctx->maxt, std::max<uint64_t>(sc->n, 1) * 4);
     ctx->have_frame = true;
+    ctx->pending = true;
     ctx->f_scene = sc;
     ctx->f_cam = *cam;
     ctx->f_cfg = *cfg;
@@ -620,20 +635,51 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     return AGSX_OK;
 }
 
+// A frame whose host image is still being written (render_async_host[_u8],
+// not yet waited for) owns the context's buffers and counters: no other work
+// may be enqueued on the context until agsx_render_wait.
+int refuse_if_host_frame(agsx_ctx* ctx, const char* what) {
+    if (ctx->pending && (ctx->f_host_dst || ctx->f_host_dst_u8))
+        return fail(ctx, AGSX_EINVAL,
+                    std::string(what) + ": a host frame is in flight on this context; call agsx_render_wait first");
+    return AGSX_OK;
+}
+
 // Wait for the enqueued frame; grow the pair arena and re-run on overflow.
+// Frames enqueued before it since the last wait (an async chain) cannot be
+// re-run: if one of them overflowed, the wait fails with AGSX_EFRAME_LOST.
 int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
-    if (!ctx->have_frame) return fail(ctx, AGSX_EINVAL, "no frame in flight");
+    if (!ctx->have_frame || !ctx->pending) return fail(ctx, AGSX_EINVAL, "no frame in flight");
     for (int attempt = 0; attempt < 4; ++attempt) {
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         const Counters c = *ctx->h_ctr;
+        const ChainWords chain = *reinterpret_cast<const ChainWords*>(ctx->h_ctr + 1);
+        const bool last_over = c.overflow != 0u || c.p_eff != c.p;
+        // the chain is over: its words start again for the next one (and for a re-run)
+        AGSX_CUDA(cudaMemsetAsync(ctx->chain.p, 0, sizeof(ChainWords), ctx->stream));
+        const uint32_t lost = chain.overflowed - (last_over ? 1u : 0u);
+        if (attempt == 0 && lost > 0) {
+            ctx->pending = false;
+            AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+            return fail(ctx, AGSX_EFRAME_LOST,
+                        std::to_string(lost) + " of the " + std::to_string(chain.frames) +
+                            " frames enqueued since the last wait overflowed the pair arena (capacity " +
+                            std::to_string(ctx->pair_capacity) +
+                            " pairs) and were not rasterised; wait for each frame, or render one frame first to "
+                            "size the arena");
+        }
         const uint64_t pairs = c.p == 0xffffffffu ? UINT64_MAX : c.p;
         if (pairs > ctx->f_cfg.pair_budget) {
+            ctx->pending = false;
             return fail(ctx, AGSX_EPAIR_BUDGET,
                         "pair count " + (pairs == UINT64_MAX ? std::string(">= 2^32") : std::to_string(pairs)) +
                             " exceeds budget " + std::to_string(ctx->f_cfg.pair_budget));
         }
-        if (c.overflow || c.p_eff != c.p) {
-            if (pairs >= (1ull << 31)) return fail(ctx, AGSX_ENOMEM, "pair count exceeds 2^31");
+        if (last_over) {
+            if (pairs >= (1ull << 31)) {
+                ctx->pending = false;
+                return fail(ctx, AGSX_ENOMEM, "pair count exceeds 2^31");
+            }
             ctx->pair_capacity = std::min<uint64_t>(pairs + pairs / 8 + 1024, ctx->f_cfg.pair_budget);
             const uint64_t tiles = static_cast<uint64_t>(ctx->f_params.tiles_x) * ctx->f_params.tiles_y;
             ensure_frame_buffers(ctx, ctx->f_scene->n, tiles,
@@ -642,6 +688,7 @@ int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
             enqueue_frame(ctx, ctx->f_scene, ctx->f_params, ctx->f_maxt, nullptr);
             continue;
         }
+        ctx->pending = false;
         ctx->pairs_per_splat = c.m ? static_cast<double>(c.p) / c.m : 0.0;
         if (out) {
             out->pair_count = c.p;
@@ -655,6 +702,7 @@ int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
         }
         return AGSX_OK;
     }
+    ctx->pending = false;
     return fail(ctx, AGSX_ECUDA, "pair arena did not converge");
 }
 

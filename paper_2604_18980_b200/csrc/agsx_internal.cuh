@@ -505,6 +505,17 @@ struct Counters {
     uint32_t band_done[32];  // units finished per egress row slot (banded host egress)
 };
 
+// Per-context words that survive the per-frame counter memset: how many of the
+// frames enqueued since the last wait overflowed the pair arena (their pairs
+// were not emitted, so their images are not the frame's), and how many frames
+// that chain holds.  Updated by the counter readback at the end of every frame
+// and read back behind the Counters block; finish_frame clears them.
+struct ChainWords {
+    uint32_t overflowed;
+    uint32_t frames;
+    uint32_t pad[2];
+};
+
 // The depth keys of a frame span >= 2^24 (key - kmin needs a 4th 8-bit
 // pass); false when there are no keys.
 __device__ __forceinline__ bool depth_keys_wide(uint32_t kmin_c, uint32_t kmax) {

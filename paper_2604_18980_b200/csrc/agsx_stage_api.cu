@@ -33,6 +33,7 @@ int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_came
                          uint64_t* out_count) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
+        if (const int rc = refuse_if_host_frame(ctx, "preprocess_view")) return rc;
         if (!scene) return fail(ctx, AGSX_EINVAL, "null scene");
         // preprocess_view validates only the LUT requirement (preprocess.cpp:121-125)
         if (cfg->mode == AGSX_MODE_ADAGSCALE && lut == nullptr)
@@ -83,6 +84,7 @@ int agsx_generate_pairs(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n
                         uint64_t* out_total) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
+        if (const int rc = refuse_if_host_frame(ctx, "generate_pairs")) return rc;
         if (cfg->tile_size < 1) return fail(ctx, AGSX_EINVAL, "tile_size must be >= 1");
         agsx_config c = *cfg;
         c.mode = mode;
@@ -140,6 +142,7 @@ int agsx_sort_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* splat_index, uint64
                     int32_t tile_count, uint32_t* ranges) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
+        if (const int rc = refuse_if_host_frame(ctx, "sort_pairs")) return rc;
         if (tile_count < 0) return fail(ctx, AGSX_EINVAL, "negative tile count");
         if (n >= (1ull << 32)) return fail(ctx, AGSX_EINVAL, "too many pairs");
         ensure(ctx->tmp0, std::max<uint64_t>(n, 1) * 8);
@@ -194,8 +197,8 @@ int agsx_raster(agsx_ctx* ctx, const agsx_splat_view* splats, uint64_t n_splats,
                 int32_t height, const agsx_config* cfg, float* image, float* max_t) {
     if (!ctx) return AGSX_EINVAL;
     return guarded(ctx, [&]() -> int {
-        if (cfg->tile_size < 1 || cfg->tile_size > 64)
-            return fail(ctx, AGSX_EINVAL, "tile_size must be in [1, 64]");
+        if (const int rc = refuse_if_host_frame(ctx, "raster_tile")) return rc;
+        if (cfg->tile_size < 1) return fail(ctx, AGSX_EINVAL, "tile_size must be >= 1");
         if (width <= 0 || height <= 0) return fail(ctx, AGSX_EINVAL, "image dimensions must be positive");
         agsx_camera cam{};
         cam.width = width;

@@ -701,11 +701,19 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
     if (tid < 32) sTab[tid] = kExp2fTab[tid];
     if (tid == 0) sPit = 0;
 
-    const int tile = blockIdx.x;
+    // Tiles above 64x64 pixels are split into 64x64 blocks, one CTA each,
+    // every block walking the whole pair range of its tile: a pixel's value
+    // depends only on the tile's pair sequence (rasterizer.cpp:56-90; the
+    // early stop is an optimisation), so the blocks are independent.
     const int ts = p.tile_size;
+    const int bs = imin(ts, 64);
+    const int nsub = (ts + 63) / 64;
+    const int tile = static_cast<int>(blockIdx.x) / (nsub * nsub);
+    const int sub = static_cast<int>(blockIdx.x) % (nsub * nsub);
     const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
     const int x0 = tx * ts, y0 = ty * ts;
     const int w = imin(ts, p.W - x0), h = imin(ts, p.H - y0);
+    const int sx0 = (sub % nsub) * bs, sy0 = (sub / nsub) * bs;
 
     int lx[PPT], ly[PPT];
     float px[PPT], py[PPT], T[PPT], Cr[PPT], Cg[PPT], Cb[PPT];
@@ -714,8 +722,8 @@ k_raster(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __rest
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         const int lp = tid + k * 256;
-        lx[k] = lp % ts;
-        ly[k] = lp < ts * ts ? lp / ts : ts;
+        lx[k] = sx0 + lp % bs;
+        ly[k] = lp < bs * bs ? sy0 + lp / bs : ts;
         px[k] = static_cast<float>(x0 + lx[k]) + 0.5f;
         py[k] = static_cast<float>(y0 + ly[k]) + 0.5f;
         T[k] = 1.0f;

@@ -382,6 +382,43 @@ public:
         return out;
     }
 
+    // build_lut's fold (calibrate.cpp:14-41) over `views`: the per-depth-bin
+    // max of max_t and whether the bin saw a blended splat.  The fold is a max,
+    // so the folds of view blocks merge exactly into the fold of all views
+    // (batch.pair_report across ranks).
+    py::dict fold_max_t(Scene& scene, std::vector<int> views, int threads) {
+        if (views.empty())
+            for (int v = 0; v < static_cast<int>(scene.cameras.size()); ++v) views.push_back(v);
+        std::vector<agsx_camera> cams;
+        for (int v : views) cams.push_back(view_of(scene, v));
+        ags::RenderConfig def;
+        def.thread_count = threads;
+        const agsx_config cfg = ags::detail::to_c(def);
+        const ags::TUpperLUT shape;
+        const agsx_lut l{shape.depth_min, shape.depth_max, static_cast<int32_t>(shape.bins.size()), nullptr};
+        std::vector<float> folded(shape.bins.size(), 0.0f);
+        std::vector<std::uint8_t> observed(shape.bins.size(), 0);
+        agsx_scene* dev = device_scene(scene);
+        {
+            py::gil_scoped_release nogil;
+            std::lock_guard<std::mutex> g(mu_);
+            for (const agsx_camera& c : cams) {
+                const int rc = agsx_fold_max_t(ctx_, dev, &c, &cfg, &l, folded.data(), observed.data());
+                if (rc != AGSX_OK) {
+                    py::gil_scoped_acquire gil;
+                    raise_status(rc, ctx_);
+                }
+            }
+        }
+        py::dict out;
+        out["folded"] = folded;
+        std::vector<bool> obs(observed.begin(), observed.end());
+        out["observed"] = obs;
+        out["depth_min"] = shape.depth_min;
+        out["depth_max"] = shape.depth_max;
+        return out;
+    }
+
     // psnr (analysis.cpp:14-25) of two device frames of n floats, numerator
     // reduced on the GPU (row f3; e.g. torch tensors of a gathered path).
     double psnr_device(std::uintptr_t a, std::uintptr_t b, std::uint64_t n) {
@@ -801,6 +838,8 @@ PYBIND11_MODULE(_core, m) {
         .def("pair_report", &Renderer::pair_report, py::arg("scene"), py::arg("specs"),
              py::arg("views") = std::vector<int>{}, py::arg("lut_bins") = std::vector<float>{},
              py::arg("lut_depth_min") = 0.0f, py::arg("lut_depth_max") = 100.0f, py::arg("threads") = 0)
+        .def("fold_max_t", &Renderer::fold_max_t, py::arg("scene"), py::arg("views") = std::vector<int>{},
+             py::arg("threads") = 0)
         .def("psnr_device", &Renderer::psnr_device, py::arg("a"), py::arg("b"), py::arg("n"))
         .def("calibrate", &Renderer::calibrate, py::arg("scene"), py::arg("target_drop"), py::arg("calib_views") = 16,
              py::arg("threads") = 0)

@@ -23,6 +23,7 @@ for v in ${VARIANTS:-bucket depth}; do
            touch paper_2604_18980_b200/csrc/k_bucket.cu; make -s EXTRA_NVCC=-DAGSX_TS_MATCH -j16 > $OUT/make_match.log 2>&1
            timeout 300 python bench.py --steps 20 --no-cpu --no-e2e --no-inflight > $OUT/b_$v.json 2> $OUT/b_$v.err
            touch paper_2604_18980_b200/csrc/k_bucket.cu; make -s -j16 > /dev/null 2>&1 ;;
+    bucket) AGSX_SORT=bucket timeout 300 python bench.py --steps 20 --no-cpu --no-e2e --no-inflight > $OUT/b_$v.json 2> $OUT/b_$v.err ;;
     *) timeout 300 python bench.py --steps 20 --no-cpu --no-e2e --no-inflight > $OUT/b_$v.json 2> $OUT/b_$v.err ;;
   esac
   summ $OUT/b_$v.json || tail -3 $OUT/b_$v.err

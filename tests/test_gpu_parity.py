@@ -691,6 +691,23 @@ def test_pair_report_matches_reference(ref):
         assert abs(g["psnr_drop_db"] - drop) < 1e-9
     csv = P.pair_report_csv(got)
     assert csv.splitlines()[0].startswith("mode,k,pair_count,reduction_vs_ellipse_pct")
+    # no LUT given: the reference builds it from all the views (analysis.cpp:265-275);
+    # batch.device_pair_report folds view blocks and merges them (here one rank)
+    from paper_2604_18980_b200.batch import device_pair_report
+
+    r = P.Renderer(0)
+    want = ref.pair_report(o, 3, specs)
+    for got in (r.pair_report(s, specs, views=[0, 1, 2]), device_pair_report(r, s, specs, 3)):
+        for g, (pc, red, drop) in zip(got, want):
+            assert g["pair_count"] == int(pc)
+            assert g["reduction_pct"] == red
+            assert abs(g["psnr_drop_db"] - drop) < 1e-9
+    # the merged fold of two view blocks is the fold of all views
+    from paper_2604_18980_b200.batch import merge_folds
+
+    whole = merge_folds([r.fold_max_t(s, [0, 1, 2])])
+    split = merge_folds([r.fold_max_t(s, [0, 1]), r.fold_max_t(s, [2])])
+    assert whole == split
     assert P.format_double(100.0) == "100" and P.format_double(0.5) == "0.5"
 
 
@@ -852,3 +869,105 @@ def test_per_element_helpers_match_oracle(ctx, port):
     for i in range(len(sel)):
         m = np.float32(np.sqrt(np.float32(2.0 * libm.logf(float(np.float32(sel["opacity"][i] / sel["th"][i]))))))
         assert m.view(np.uint32) == er[i, 0].view(np.uint32), i
+
+
+def test_async_chain_overflow_mid_chain_fails_at_wait(port):
+    """Frames enqueued back to back (render_async, no wait in between) share
+    one counter block; a frame in the middle of the chain that overflows the
+    pair arena skips emission and cannot be re-run once later frames ran.
+    The wait must report it (AGSX_EFRAME_LOST) instead of returning the last
+    frame's counts; an overflowing LAST frame is re-run as before."""
+    ctx = capi.Context(0)  # fresh context: arena at its first guess max(12 N, 2^20)
+    try:
+        o = port.synth_scene(2, 2000, "slab", cameras=2, width=640, height=480, focal=500.0)
+        o.scale[:] *= 40.0  # P >> 2^20 at 640x480
+        dev = ctx.upload(o.mean, o.scale, o.rotation, o.opacity, o.sh)
+        big = to_gpu_cam(o.cameras[0])
+        small = to_gpu_cam(o.cameras[0])
+        small.width, small.height = 16, 16  # one tile: at most N pairs
+        ctx.render_async(dev, big, gpu_cfg("aabb"))   # overflows (emission skipped)
+        ctx.render_async(dev, small, gpu_cfg("aabb"))  # fits
+        with pytest.raises(capi.AgsxError) as e:
+            ctx.wait()
+        assert e.value.code == capi.EFRAME_LOST, e.value
+        with pytest.raises(capi.AgsxError) as e:  # nothing in flight any more
+            ctx.wait()
+        assert e.value.code == capi.EINVAL
+        # the chain words were cleared: a fitting chain waits cleanly
+        ctx.render_async(dev, small, gpu_cfg("aabb"))
+        ctx.render_async(dev, small, gpu_cfg("aabb"))
+        st = ctx.wait()
+        assert st["pair_count"] <= 2000
+        # an overflowing last frame is grown and re-run (bit-exact vs the oracle)
+        ctx.render_async(dev, small, gpu_cfg("aabb"))
+        ctx.render_async(dev, big, gpu_cfg("aabb"))
+        st = ctx.wait()
+        want = port.render(o, o.cameras[0], port.config("aabb"))
+        assert st["pair_count"] == want["pair_count"] > (1 << 20)
+    finally:
+        ctx.close()
+
+
+def test_host_frame_in_flight_refused_at_the_c_abi(port):
+    """while a render_async_host frame is in flight its host image
+    and counters belong to it; every other frame entry on the context (sync
+    render, async, stage hooks) is refused with EINVAL until agsx_render_wait."""
+    ctx = capi.Context(0)
+    try:
+        o = port.synth_scene(4, 500, "veil", cameras=2, width=200, height=136, focal=150.0)
+        dev = ctx.upload(o.mean, o.scale, o.rotation, o.opacity, o.sh)
+        cam = to_gpu_cam(o.cameras[0])
+        img = np.zeros((136, 200, 3), np.float32)
+        ctx.render_async_host(dev, cam, gpu_cfg("ellipse", exact=True), None, img)
+        for call in (lambda: ctx.render(dev, cam, gpu_cfg("ellipse")),
+                     lambda: ctx.render_async(dev, cam, gpu_cfg("ellipse")),
+                     lambda: ctx.render_async_host(dev, cam, gpu_cfg("ellipse"), None, img),
+                     lambda: ctx.preprocess_view(dev, cam, gpu_cfg("ellipse"))):
+            with pytest.raises(capi.AgsxError) as e:
+                call()
+            assert e.value.code == capi.EINVAL
+        st = ctx.wait()
+        want = port.render(o, o.cameras[0], port.config("ellipse"))
+        assert st["pair_count"] == want["pair_count"]
+        assert np.array_equal(img.view(np.uint32), want["image"].view(np.uint32))
+        ctx.render(dev, cam, gpu_cfg("ellipse"))  # accepted again
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("mode", ["ellipse", "adagscale"])
+def test_p_it_matches_reference_semantics(ctx, port, mode):
+    """frame_stats()['p_it'] (the raster work measure behind the
+    bench's raster bytes) against the oracle's P_it -- the
+    pairs raster_tile visits before all pixels of its tile are saturated
+    (rasterizer.cpp:55-56), summed over tiles. Exact rasteriser: equal. Default
+    rasteriser (hardware ex2 blend, so T may cross the floor one pair
+    earlier or later on a handful of pixels): within 0.1 %."""
+    oscene, dev = scene_pair(port, ctx, 11, 20000, "veil", 2, 640, 480, 500.0)
+    ocam = oscene.cameras[0]
+    bins = LUT_BINS if mode == "adagscale" else None
+    k = K1080 * (500.0 / 1500.0) ** 2 if mode == "adagscale" else 0.0
+    ocfg = port.config(mode, k=k)
+    splats = port.preprocess(oscene, ocam, ocfg, port.lut(bins) if bins else None)
+    keys, idx, counts = port.generate_pairs(splats, ocam.width, ocam.height, ocfg.mode, ocfg)
+    tiles = ((ocam.width + 15) // 16) * ((ocam.height + 15) // 16)
+    skeys, sidx, ranges = port.sort_pairs(keys, idx, tiles)
+    _, want = port.raster_pit(splats, sidx, ranges, ocam.width, ocam.height, ocfg)
+    assert 0 < want <= len(skeys)
+    glut = capi.make_lut(bins) if bins else None
+    ctx.render(dev, to_gpu_cam(ocam), gpu_cfg(mode, k, exact=True), glut)
+    assert ctx.frame_stats()["p_it"] == want
+    ctx.render(dev, to_gpu_cam(ocam), gpu_cfg(mode, k), glut)
+    got = ctx.frame_stats()["p_it"]
+    assert abs(got - want) <= max(2, want // 1000), (got, want)
+
+
+def test_tile_sizes_above_64(ctx, port):
+    """the reference's raster_tile takes any tile_size >= 1 and
+    falls back to heap buffers above 64x64 pixels (rasterizer.cpp:35-47).
+    Here such a tile is split into 64x64 blocks that walk the same pair
+    range; keys, ranges and the image stay bit-exact."""
+    oscene, dev = scene_pair(port, ctx, 53, 600, "slab", 2, 321, 257, 200.0)
+    for ts in (64, 80, 128, 200):
+        check_frame(ctx, port, oscene, dev, 0, "ellipse", background=(0.2, 0.2, 0.2), tile_size=ts)
+        check_frame(ctx, port, oscene, dev, 0, "aabb", tile_size=ts)

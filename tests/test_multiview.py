@@ -131,6 +131,22 @@ def _report_worker(rank, world, port_no, q):
                     for i, (m, k) in enumerate((("ellipse", 0.0), ("adagscale", 0.5)))]
 
         q.put((rank, pair_report(local, 7)))
+
+        # AdaGScale rows: one LUT over ALL views, whatever the world size
+        # (analysis.cpp:265-275): the ranks' build_lut folds are merged by max
+        def fold(views):  # stand-in fold: bin b sees view v when (v + b) % 3 == 0
+            return {"folded": [max([0.01 * (v + 1) * (b + 1) for v in views if (v + b) % 3 == 0], default=0.0)
+                               for b in range(20)],
+                    "observed": [any((v + b) % 3 == 0 for v in views) for b in range(20)],
+                    "depth_min": 0.0, "depth_max": 100.0}
+
+        def local_lut(views, lut_bins, lut_depth_min, lut_depth_max):
+            rows = local(views)
+            for r in rows:
+                r["pair_count"] = int(1e6 * sum(lut_bins))  # depends on the LUT only
+            return rows
+
+        q.put((rank, pair_report(local_lut, 7, fold=fold)))
     finally:
         dist.destroy_process_group()
 
@@ -142,10 +158,23 @@ def test_pair_report_merges_view_blocks_world2_gloo():
     procs = [ctx.Process(target=_report_worker, args=(r, 2, port_no, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=300) for _ in procs)
+    got = [q.get(timeout=300) for _ in range(2 * len(procs))]
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    res = {}
+    lut_rows = {}
+    for rank, rows in got:
+        (lut_rows if rank in res else res)[rank] = rows
+    from paper_2604_18980_b200.batch import merge_folds
+
+    whole = merge_folds([{"folded": [max([0.01 * (v + 1) * (b + 1) for v in range(7) if (v + b) % 3 == 0],
+                                         default=0.0) for b in range(20)],
+                          "observed": [any((v + b) % 3 == 0 for v in range(7)) for b in range(20)],
+                          "depth_min": 0.0, "depth_max": 100.0}])
+    for rows in lut_rows.values():  # every rank reported with the all-view LUT
+        # both ranks' blocks contribute (views 0-3 and 4-6), merged rows sum them
+        assert rows[0]["pair_count"] == 2 * int(1e6 * sum(whole["lut_bins"]))
     for rows in res.values():  # same merged rows on both ranks
         assert [r["mode"] for r in rows] == ["ellipse", "adagscale"]
         assert rows[0]["views"] == 7
