@@ -280,6 +280,8 @@ def cub_comparator(r, scene, view, mode, k, bins, exact, iters=20):
     for label, (md, kk, bb) in (("adagscale_on", (mode, k, bins)), ("adagscale_off", ("ellipse", 0.0, []))):
         if label == "adagscale_on" and mode != "adagscale":
             continue
+        r.render_async(scene, view, md, kk, bb, exact=exact)
+        r.wait()  # sizes the pair arena: a chain cannot re-run an overflowed frame
         for _ in range(5):
             r.render_async(scene, view, md, kk, bb, exact=exact)
         r.wait()
@@ -397,7 +399,11 @@ def run_ours(args, rank, world, local_rank):
         for v, cam in jobs:
             r.render_async(scene, v, mode, k, bins, exact=args.exact, camera=cam)
 
-    # warm-up (also sizes the pair arena)
+    # warm-up: one waited frame per view sizes the pair arena (an async chain
+    # cannot re-run a frame that overflowed it; wait() would raise)
+    for v, cam in jobs:
+        r.render_async(scene, v, mode, k, bins, exact=args.exact, camera=cam)
+        r.wait()
     for _ in range(max(args.warmup, 3)):
         step()
     r.wait()
@@ -437,10 +443,9 @@ def run_ours(args, rank, world, local_rank):
         r2 = P.Renderer(local_rank)
         rs = [r, r2]
         for rr in rs:
-            for _ in range(2):
-                for v, cam in jobs:
-                    rr.render_async(scene, v, mode, k, bins, exact=args.exact, camera=cam)
-            rr.wait()
+            for v, cam in jobs:
+                rr.render_async(scene, v, mode, k, bins, exact=args.exact, camera=cam)
+                rr.wait()
         barrier()
         steps_i = max(4, min(args.steps, 100))
         t0 = time.perf_counter()
@@ -574,7 +579,7 @@ def run_ours(args, rank, world, local_rank):
     if mode == "adagscale" and not args.no_off:
         for _ in range(3):
             r.render_async(scene, view, "ellipse", 0.0, [], exact=args.exact)
-        r.wait()
+            r.wait()  # the first one sizes the pair arena for the off-mode chain
         steps_off = max(3, min(args.steps, 20))
         barrier()
         ev0.record(stream)

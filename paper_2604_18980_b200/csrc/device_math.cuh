@@ -10,8 +10,9 @@
 //   * x86 cvttss2si for static_cast<int>(float) out of range (-> INT_MIN);
 //   * glibc's logf / expf (table + polynomial algorithms of glibc 2.39,
 //     IFUNC variants on x86-64).  They are re-evaluated here with the same
-//     double-precision steps; tests/test_device_libm.py pins them against
-//     the host libm on the GPU box.
+//     double-precision steps; tests/test_gpu_parity.py
+//     (test_device_logf_matches_host_glibc, test_device_expf_matches_host_glibc)
+//     pins them against the host libm on the GPU box.
 #pragma once
 #include <cstdint>
 
@@ -80,7 +81,8 @@ __device__ __forceinline__ float glibc_logf(float x) {
 
 // ---- glibc expf (sysdeps/ieee754/flt-32/e_expf.c algorithm) ------------
 // exp(x) = 2^(k/32) * 2^(r/32); table entries bits(2^(i/32)) - (i << 47),
-// regenerated from correctly rounded 2^(i/32) (scripts/gen_libm_tables.py).
+// (the table of glibc 2.39's __exp2f_data; SURVEY.md Appendix A gives its
+// libm offset and how to regenerate it from correctly rounded 2^(i/32)).
 __device__ __constant__ static const uint64_t kExp2fTab[32] = {
     0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
     0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
@@ -102,7 +104,9 @@ __device__ __forceinline__ float glibc_expf(float x) {
     }
     const double xd = static_cast<double>(x);
     // glibc is built with FMA on x86-64 (IFUNC variant): r = fma(InvLn2N, x, -kd) etc.;
-    // verified over all 2^32 floats against the host libm (tests/test_device_libm.py).
+    // pinned against the host libm on every float in [-20, -0] (the decision
+    // domain [ln tau, 0] and beyond) plus 3M samples over [-110, 88]
+    // (test_device_expf_matches_host_glibc).
     double kd = fma(0x1.71547652b82fep+5, xd, 0x1.8p+52);
     const uint64_t ki = static_cast<uint64_t>(__double_as_longlong(kd));
     kd -= 0x1.8p+52;

@@ -14,6 +14,8 @@
 #include "agsx_internal.cuh"
 #include "kernels.cuh"
 
+constexpr int kPreQ = 12;  // words queued per survivor between K1's phases
+
 #ifndef AGSX_PRE_MINB
 #define AGSX_PRE_MINB 4
 #endif
@@ -191,30 +193,43 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
              BucketOut bk) {
     griddep_wait();
     // frame-scoped zeroing (the previous frame's readers have completed)
-    for (uint64_t z = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; z < fz.n_tiles || z < fz.n_chunks;
-         z += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        if (z < fz.n_tiles) {
-            fz.ranges[z] = make_uint2(0u, 0u);
-            if (fz.tile_pit) fz.tile_pit[z] = 0ull;
+    // (a block-uniform test first: most blocks have nothing to zero)
+    const uint32_t nz = fz.n_tiles > fz.n_chunks ? fz.n_tiles : fz.n_chunks;
+    if (blockIdx.x * blockDim.x < nz) {
+        for (uint32_t z = blockIdx.x * blockDim.x + threadIdx.x; z < nz; z += gridDim.x * blockDim.x) {
+            if (z < fz.n_tiles) {
+                fz.ranges[z] = make_uint2(0u, 0u);
+                if (fz.tile_pit) fz.tile_pit[z] = 0ull;
+            }
+            if (z < fz.n_chunks) fz.chunks[z] = 0u;
         }
-        if (z < fz.n_chunks) fz.chunks[z] = 0u;
     }
     const int lane = threadIdx.x & 31;
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
 
-    bool alive = false, keep = false;
-    float depth = 0.0f;
-    uint4 hit_rec = make_uint4(0u, 0u, 0u, 0u);
+    // Phase A, one thread per Gaussian: projection, Eq. 10 and the culls.
+    // The survivors (a third of the Gaussians at config 3) are queued in
+    // shared memory, so phase B -- the tile test, colour, blend-cull data and
+    // the stores -- runs on packed warps instead of on the survivors' lanes of
+    // every warp.
+    __shared__ float s_q[kPreQ][256];  // per survivor slot (structure of arrays)
+    __shared__ uint32_t s_gid[256];
+    __shared__ uint32_t s_n;
+    if (threadIdx.x == 0) s_n = 0;
+    __syncthreads();
+    bool ok = false;
+    float m2x = 0.0f, m2y = 0.0f, cxx = 0.0f, cxy = 0.0f, cyy = 0.0f, det = 0.0f, th = p.tau, tz = 0.0f;
+    float opacity = 0.0f, dx = 0.0f, dy = 0.0f, dz = 0.0f;
     if (i < sc.n) {
         const float4 po = sc.pos_op[i];
         const float4 q = sc.rot[i];
         const float4 sr = sc.scale_r[i];
-        const float2 gb = sc.sh_gb[i];  // issued with the other loads
-        const float opacity = po.w;
+        opacity = po.w;
         // to_camera (scene.hpp:41-43): t = R (mean - position), float
-        const float dx = po.x - p.cam_pos[0], dy = po.y - p.cam_pos[1], dz = po.z - p.cam_pos[2];
-        float tz = 0.0f, m2x = 0.0f, m2y = 0.0f, cxx = 0.0f, cxy = 0.0f, cyy = 0.0f, det = 0.0f, th = p.tau;
-        bool ok = project_dev(p, dx, dy, dz, q, sr, tz, m2x, m2y, cxx, cxy, cyy);
+        dx = po.x - p.cam_pos[0];
+        dy = po.y - p.cam_pos[1];
+        dz = po.z - p.cam_pos[2];
+        ok = project_dev(p, dx, dy, dz, q, sr, tz, m2x, m2y, cxx, cxy, cyy);
         if (ok) {
             det = cxx * cyy - cxy * cxy;
             ok = det > 0.0f;
@@ -223,66 +238,108 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
             th = compute_th_dev(lut_value(p, tz), det, p.k, p.tau);  // Eq. 10
         }
         if (ok && th >= opacity) ok = false;
+        if (!ok) {
+            status[i] = 0u;
+            if (!bk.tile_cnt) dkeys[i] = 0xffffffffu;
+        }
+    }
+    // queue the survivors (converged warp: one shared-memory atomic per warp)
+    const uint32_t okb = __ballot_sync(0xffffffffu, ok);
+    uint32_t qbase = 0;
+    if (lane == 0 && okb) qbase = atomicAdd(&s_n, static_cast<uint32_t>(__popc(okb)));
+    qbase = __shfl_sync(0xffffffffu, qbase, 0);
+    if (ok) {
+        const uint32_t at = qbase + __popc(okb & ((1u << lane) - 1u));
+        s_gid[at] = static_cast<uint32_t>(i);
+        s_q[0][at] = m2x;
+        s_q[1][at] = m2y;
+        s_q[2][at] = cxx;
+        s_q[3][at] = cxy;
+        s_q[4][at] = cyy;
+        s_q[5][at] = det;
+        s_q[6][at] = opacity;
+        s_q[7][at] = th;
+        s_q[8][at] = tz;
+        s_q[9][at] = dx;
+        s_q[10][at] = dy;
+        s_q[11][at] = dz;
+    }
+    __syncthreads();
+    const uint32_t ns = s_n;
+    if (threadIdx.x == 0 && ns) atomicAdd(&ctr->s, ns);  // survivors = splat_count
+
+    // Phase B, one thread per queued survivor.
+    const uint32_t slot = threadIdx.x;
+    const bool alive = slot < ns;
+    if (!alive && (threadIdx.x & ~31u) >= ns) return;  // whole warps past the queue
+    bool keep = false;
+    float depth = 0.0f;
+    uint4 hit_rec = make_uint4(0u, 0u, 0u, 0u);
+    uint32_t gi = 0;
+    if (alive) {
+        gi = s_gid[slot];
+        const float m2x = s_q[0][slot], m2y = s_q[1][slot];
+        const float cxx = s_q[2][slot], cxy = s_q[3][slot], cyy = s_q[4][slot], det = s_q[5][slot];
+        const float opacity = s_q[6][slot], th = s_q[7][slot], tz = s_q[8][slot];
+        const float dx = s_q[9][slot], dy = s_q[10][slot], dz = s_q[11][slot];
         uint32_t cnt = 0;
-        if (ok) {
-            alive = true;
-            depth = tz;
-            const float inv_det = 1.0f / det;  // SymMat2::inverse (math.hpp:85-88)
-            const float ixx = cyy * inv_det, ixy = -cxy * inv_det, iyy = cxx * inv_det;
-            const TileTest tt = make_tile_test(m2x, m2y, cxx, cxy, cyy, ixx, ixy, iyy, opacity, th, p);
-            const uint4 hits = hit_record(tt, p, cnt);
-            hit_rec = hits;
-            keep = cnt > 0;
-            float rgb[3] = {0.5f, 0.5f, 0.5f};
-            if (keep || dump) {
-                // Vec3f::normalized (math.hpp:25-28) of mean - cam.position
-                const float nrm = sqrtf(dx * dx + dy * dy + dz * dz);
-                float ux = 0.0f, uy = 0.0f, uz = 0.0f;
-                if (nrm > 0.0f) {
-                    const float inv = 1.0f / nrm;
-                    ux = dx * inv;
-                    uy = dy * inv;
-                    uz = dz * inv;
-                }
-                eval_color(sc, i, sr.w, gb.x, gb.y, ux, uy, uz, rgb);
+        depth = tz;
+        const float inv_det = 1.0f / det;  // SymMat2::inverse (math.hpp:85-88)
+        const float ixx = cyy * inv_det, ixy = -cxy * inv_det, iyy = cxx * inv_det;
+        const TileTest tt = make_tile_test(m2x, m2y, cxx, cxy, cyy, ixx, ixy, iyy, opacity, th, p);
+        const uint4 hits = hit_record(tt, p, cnt);
+        hit_rec = hits;
+        keep = cnt > 0;
+        float rgb[3] = {0.5f, 0.5f, 0.5f};
+        if (keep || dump) {
+            // Vec3f::normalized (math.hpp:25-28) of mean - cam.position
+            const float nrm = sqrtf(dx * dx + dy * dy + dz * dz);
+            float ux = 0.0f, uy = 0.0f, uz = 0.0f;
+            if (nrm > 0.0f) {
+                const float inv = 1.0f / nrm;
+                ux = dx * inv;
+                uy = dy * inv;
+                uz = dz * inv;
             }
-            if (keep) {
-                float qcut, qsafe, ex, ey;
-                blend_cull_data(ixx, ixy, iyy, opacity, p.tau, p.aclamp, qcut, qsafe, ex, ey);
-                pl.p0[i] = make_float4(m2x, m2y, ixx, 2.0f * ixy);
-                pl.p1[i] = make_float4(iyy, opacity, qcut, qsafe);
-                pl.p2[i] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(pack_extent(ex, ey)));
-                if (p.mode == AGSX_MODE_OBB) pl.p4[i] = make_float4(tt.v1x, tt.v1y, tt.a, tt.b);
-                if (bk.tile_cnt) {
-                    // tile histogram of the bucketed sort: one reduction per hit tile
-                    hit_tiles(tt, p, hits, [&](int tx, int ty) {
-                        atomicAdd(&bk.tile_cnt[static_cast<uint32_t>(ty * p.tiles_x + tx)], 1u);
-                    });
-                } else {
-                    reinterpret_cast<uint4*>(pl.p3)[i] = hits;
-                }
-            }
-            if (dump) {
-                agsx_splat_view v;
-                v.mean2d[0] = m2x;
-                v.mean2d[1] = m2y;
-                v.cov2d[0] = cxx;
-                v.cov2d[1] = cxy;
-                v.cov2d[2] = cyy;
-                v.inv_cov[0] = ixx;
-                v.inv_cov[1] = ixy;
-                v.inv_cov[2] = iyy;
-                v.depth = tz;
-                v.rgb[0] = rgb[0];
-                v.rgb[1] = rgb[1];
-                v.rgb[2] = rgb[2];
-                v.opacity = opacity;
-                v.th = th;
-                v.source_id = static_cast<uint32_t>(i);
-                dump[i] = v;
+            const float2 gb = sc.sh_gb[gi];
+            eval_color(sc, gi, sc.scale_r[gi].w, gb.x, gb.y, ux, uy, uz, rgb);
+        }
+        if (keep) {
+            float qcut, qsafe, ex, ey;
+            blend_cull_data(ixx, ixy, iyy, opacity, p.tau, p.aclamp, qcut, qsafe, ex, ey);
+            pl.p0[gi] = make_float4(m2x, m2y, ixx, 2.0f * ixy);
+            pl.p1[gi] = make_float4(iyy, opacity, qcut, qsafe);
+            pl.p2[gi] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(pack_extent(ex, ey)));
+            if (p.mode == AGSX_MODE_OBB) pl.p4[gi] = make_float4(tt.v1x, tt.v1y, tt.a, tt.b);
+            if (bk.tile_cnt) {
+                // tile histogram of the bucketed sort: one reduction per hit tile
+                hit_tiles(tt, p, hits, [&](int tx, int ty) {
+                    atomicAdd(&bk.tile_cnt[static_cast<uint32_t>(ty * p.tiles_x + tx)], 1u);
+                });
+            } else {
+                reinterpret_cast<uint4*>(pl.p3)[gi] = hits;
             }
         }
-        status[i] = cnt | (alive ? kAliveBit : 0u);
+        if (dump) {
+            agsx_splat_view v;
+            v.mean2d[0] = m2x;
+            v.mean2d[1] = m2y;
+            v.cov2d[0] = cxx;
+            v.cov2d[1] = cxy;
+            v.cov2d[2] = cyy;
+            v.inv_cov[0] = ixx;
+            v.inv_cov[1] = ixy;
+            v.inv_cov[2] = iyy;
+            v.depth = tz;
+            v.rgb[0] = rgb[0];
+            v.rgb[1] = rgb[1];
+            v.rgb[2] = rgb[2];
+            v.opacity = opacity;
+            v.th = th;
+            v.source_id = gi;
+            dump[gi] = v;
+        }
+        status[gi] = cnt | kAliveBit;
     }
 
     if (bk.tile_cnt) {
@@ -294,14 +351,12 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep) {
             const uint32_t at = base + __popc(kb & ((1u << lane) - 1u));
-            bk.gd[at] = make_uint2(static_cast<uint32_t>(i), __float_as_uint(depth));
+            bk.gd[at] = make_uint2(gi, __float_as_uint(depth));
             bk.hits[at] = hit_rec;
         }
-        const uint32_t alive_cnt = __popc(__ballot_sync(0xffffffffu, alive));
-        if (alive_cnt && lane == 0) atomicAdd(&ctr->s, alive_cnt);
         return;
     }
-    if (i < sc.n) dkeys[i] = keep ? __float_as_uint(depth) : 0xffffffffu;
+    if (alive) dkeys[gi] = keep ? __float_as_uint(depth) : 0xffffffffu;
     // range of the depth keys (positive floats: bit order = value order), so
     // the depth sort can skip its top digit when the keys span < 2^24.  Per
     // warp, and an atomic only when it improves on the value last seen (the
@@ -315,8 +370,6 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
             if (wminc > *reinterpret_cast<volatile uint32_t*>(&ctr->kmin_c)) atomicMax(&ctr->kmin_c, wminc);
         }
     }
-    const uint32_t alive_cnt = __popc(__ballot_sync(0xffffffffu, alive));
-    if (alive_cnt && lane == 0) atomicAdd(&ctr->s, alive_cnt);
 }
 
 // ---- exported helpers (agsx_project / agsx_eval_color / agsx_compute_th):

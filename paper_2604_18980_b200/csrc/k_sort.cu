@@ -228,6 +228,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             const uint32_t lt = peers[it] & lanemask_lt;
             const uint32_t before = s_whist[warp][d];
             rank[it] = before + __popc(lt);
+            __syncwarp();  // every peer has read the count before the group leader advances it
             if (ok[it] && lt == 0u) s_whist[warp][d] = before + __popc(peers[it]);
             __syncwarp();
         }

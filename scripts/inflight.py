@@ -12,7 +12,7 @@ for nstreams in (1, 2, 3, 4):
     for r in rs:
         for _ in range(3):
             r.render_async(s, 0, "adagscale", K, B)
-        r.wait()
+            r.wait()
     torch.cuda.synchronize()
     steps = 120
     t = time.perf_counter()
