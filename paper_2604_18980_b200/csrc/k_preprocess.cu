@@ -14,7 +14,7 @@
 #include "agsx_internal.cuh"
 #include "kernels.cuh"
 
-constexpr int kPreQ = 12;  // words queued per survivor between K1's phases
+constexpr int kPreQ = 16;  // words per survivor slot: the queue between K1's phases, then the row-edge table
 
 #ifndef AGSX_PRE_MINB
 #define AGSX_PRE_MINB 4
@@ -287,7 +287,13 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         const float inv_det = 1.0f / det;  // SymMat2::inverse (math.hpp:85-88)
         const float ixx = cyy * inv_det, ixy = -cxy * inv_det, iyy = cxx * inv_det;
         const TileTest tt = make_tile_test(m2x, m2y, cxx, cxy, cyy, ixx, ixy, iyy, opacity, th, p);
+        // the slot's queued words are in registers now: its column of s_q
+        // becomes this thread's row-edge table (hit_mask_hoisted)
+#ifdef AGSX_K1_HOIST
+        const uint4 hits = hit_record(tt, p, cnt, &s_q[0][slot], 256);
+#else
         const uint4 hits = hit_record(tt, p, cnt);
+#endif
         hit_rec = hits;
         keep = cnt > 0;
         float rgb[3] = {0.5f, 0.5f, 0.5f};
