@@ -11,6 +11,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -23,6 +24,17 @@
 #include <vector>
 
 #include "kernels.cuh"
+
+// NVTX ranges (stage tracing) around the host side of a frame,
+// named after the reference's stage_times keys (rasterizer.cpp:126-163):
+// agsx.render / preprocess / pair_gen / sort / raster / wait.  NVTX3 is
+// header-only; without a tool attached a range costs a few ns.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 namespace agsx::host {
 
@@ -77,6 +89,7 @@ struct agsx_ctx {
     int num_sms = 148;
     int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1, occ_emit_big = 1, occ_raster = 1, occ_tile_sort = 1;
     double pairs_per_splat = 0.0;  // previous frame's P / M (picks the emit stage)
+    uint64_t last_m = 0;           // previous frame's splats with tiles (sizes the scatter grid)
     Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
     // device arenas (grow-only)

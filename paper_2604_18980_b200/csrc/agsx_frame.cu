@@ -186,7 +186,7 @@ void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pi
     ensure(ctx->chunks, 2 * chunk_slots(n) * 4);
     ensure(ctx->ranges, std::max<uint64_t>(tiles, 1) * 8);
     ensure(ctx->image, std::max<uint64_t>(pixels, 1) * 12);
-    ensure(ctx->ctr, tile_cnt_offset() + std::max<uint64_t>(tiles, 1) * 4 + 16);
+    ensure(ctx->ctr, tile_cnt_offset() + std::max<uint64_t>(tiles, 1) * 4 * kTileSlices + 16);
     if (use_bucket()) {
         ensure(ctx->bk_hits, std::max<uint64_t>(n, 1) * 16);
         ensure(ctx->bk_gd, std::max<uint64_t>(n, 1) * 8);
@@ -202,7 +202,8 @@ void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pi
     if (use_bucket()) {
         ensure(ctx->ekeys, cap * 8);
         ensure(ctx->ekeys2, cap * 8);
-    } else {
+    }
+    if (!use_bucket()) {
         ensure(ctx->tkeys, cap * 4);
         ensure(ctx->tkeys2, cap * 4);
         ensure(ctx->pvals2, cap * 4);
@@ -298,7 +299,7 @@ void launch_quantize(agsx_ctx* ctx, const float* src, uint8_t* dst, uint64_t n, 
     }
 }
 
-void enqueue_bucket_sort(agsx_ctx* ctx, const FrameParams& p, const BucketOut& bk);
+void enqueue_bucket_sort(agsx_ctx* ctx, uint64_t n, const FrameParams& p, const BucketOut& bk);
 void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FrameParams& p, const SplatPlanes& pl);
 void enqueue_raster(agsx_ctx* ctx, const FrameParams& p, bool maxt, uint32_t* vals);
 
@@ -313,7 +314,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
 
     const bool bucket = use_bucket();
     AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
-    AGSX_CUDA(cudaMemsetAsync(ctr, 0, bucket ? tile_cnt_offset() + tiles * 4 : counters_bytes(), st));
+    AGSX_CUDA(cudaMemsetAsync(ctr, 0, bucket ? tile_cnt_offset() + tiles * 4 * kTileSlices : counters_bytes(), st));
     // the other frame-scoped buffers (ranges, chunk sums, per-tile P_it words)
     // are zeroed by K1 itself, so the kernels form one PDL chain
     const bool units = raster_uses_units(p, maxt);
@@ -338,6 +339,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     AGSX_CUDA(cudaEventRecord(ctx->ev_zeroed, st));
     const SplatPlanes pl = planes_of(ctx);
     if (n > 0) {
+        NvtxRange r("agsx.preprocess");
         const int grid = static_cast<int>((n + 255) / 256);
         launch_pdl(k_preprocess, dim3(grid), dim3(256), 0, st, p, sc->view(), pl, ptr<uint32_t>(ctx->status),
                    ptr<uint32_t>(ctx->dkeys), ctr, dump, fz, bk);
@@ -345,13 +347,17 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     }
     AGSX_CUDA(cudaEventRecord(ctx->ev[1], st));
     ctx->f_bucket = bucket;
-    if (bucket) {
-        enqueue_bucket_sort(ctx, p, bk);
-    } else {
-        enqueue_depth_sort(ctx, n, tiles, p, pl);
+    {
+        NvtxRange r("agsx.pair_gen+sort");
+        if (bucket) {
+            enqueue_bucket_sort(ctx, n, p, bk);
+        } else {
+            enqueue_depth_sort(ctx, n, tiles, p, pl);
+        }
     }
     uint32_t* vals = ptr<uint32_t>(ctx->pvals);
     if (!bucket) vals = ctx->f_pvals;
+    NvtxRange r("agsx.raster");
     enqueue_raster(ctx, p, maxt, vals);
 }
 
@@ -359,17 +365,19 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
 // per-tile sort.  Events: ev[2] after the scan, ev[3] after the scatter,
 // ev[4] after the per-tile sort (stage "pair_gen" = the scatter, "sort" =
 // scan + per-tile sort).
-void enqueue_bucket_sort(agsx_ctx* ctx, const FrameParams& p, const BucketOut& bk) {
+void enqueue_bucket_sort(agsx_ctx* ctx, uint64_t n, const FrameParams& p, const BucketOut& bk) {
     cudaStream_t st = ctx->stream;
     Counters* ctr = ptr<Counters>(ctx->ctr);
     const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
     const uint32_t T = static_cast<uint32_t>(tiles);
     const int scan_grid = static_cast<int>((tiles + kTileScanPer - 1) / kTileScanPer);
-    launch_pdl(k_tile_scan, dim3(scan_grid), dim3(1024), 0, st, bk.tile_cnt, ptr<uint2>(ctx->ranges), T, ctr,
+    launch_pdl(k_tile_scan, dim3(scan_grid), dim3(kTileScanThreads), 0, st, bk.tile_cnt, ptr<uint2>(ctx->ranges), T,
+               ctr,
                ctx->pair_capacity, ptr<uint64_t>(ctx->lb), ctx->epoch++, ptr<uint32_t>(ctx->big_list));
     check_launch(ctx);
     AGSX_CUDA(cudaEventRecord(ctx->ev[2], st));
-    launch_pdl(k_bucket_scatter, dim3(ctx->num_sms * 8), dim3(256), 0, st, p, planes_of(ctx), bk,
+    const int scatter_grid = static_cast<int>(std::max<uint64_t>((n + 255) / 256, 1));  // one splat per thread
+    launch_pdl(k_bucket_scatter, dim3(scatter_grid), dim3(256), 0, st, p, planes_of(ctx), bk,
                static_cast<const Counters*>(ctr), ptr<uint64_t>(ctx->ekeys));
     check_launch(ctx);
     AGSX_CUDA(cudaEventRecord(ctx->ev[3], st));
@@ -571,6 +579,7 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     if (!sc) return fail(ctx, AGSX_EINVAL, "render: null scene");
     if (sc->device != ctx->device) return fail(ctx, AGSX_EINVAL, "scene lives on another device");
     if (const int rc = refuse_if_host_frame(ctx, "render")) return rc;
+    NvtxRange nv("agsx.render");
     FrameParams p;
     const int rc = prepare(ctx, cam, cfg, lut, p);
     if (rc) return rc;
@@ -650,6 +659,7 @@ int refuse_if_host_frame(agsx_ctx* ctx, const char* what) {
 // re-run: if one of them overflowed, the wait fails with AGSX_EFRAME_LOST.
 int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
     if (!ctx->have_frame || !ctx->pending) return fail(ctx, AGSX_EINVAL, "no frame in flight");
+    NvtxRange nv("agsx.wait");
     for (int attempt = 0; attempt < 4; ++attempt) {
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         const Counters c = *ctx->h_ctr;
@@ -689,6 +699,7 @@ int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
             continue;
         }
         ctx->pending = false;
+        ctx->last_m = c.m;
         ctx->pairs_per_splat = c.m ? static_cast<double>(c.p) / c.m : 0.0;
         if (out) {
             out->pair_count = c.p;

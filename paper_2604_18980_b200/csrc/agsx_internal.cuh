@@ -579,6 +579,26 @@ struct Counters {
     uint32_t band_done[32];  // units finished per egress row slot (banded host egress)
 };
 
+// Tile ids of a mask record's hit tiles in row-major order (up to 8).
+__device__ __forceinline__ void tiles_of_mask(uint4 r, int tiles_x, uint32_t (&tl)[8]) {
+    unsigned long long mask = static_cast<unsigned long long>(r.x) | (static_cast<unsigned long long>(r.y) << 32);
+    const uint32_t tx0 = r.z & 0xffffu, ty0 = r.z >> 16, sw = r.w;
+    uint32_t row_base = ty0 * static_cast<uint32_t>(tiles_x) + tx0, row_start = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        tl[u] = 0u;
+        if (mask) {
+            const uint32_t b = static_cast<uint32_t>(__ffsll(static_cast<long long>(mask)) - 1);
+            mask &= mask - 1;
+            while (b >= row_start + sw) {
+                row_start += sw;
+                row_base += static_cast<uint32_t>(tiles_x);
+            }
+            tl[u] = row_base + (b - row_start);
+        }
+    }
+}
+
 // Per-context words that survive the per-frame counter memset: how many of the
 // frames enqueued since the last wait overflowed the pair arena (their pairs
 // were not emitted, so their images are not the frame's), and how many frames

@@ -256,6 +256,60 @@ __device__ __noinline__ void warp_sort_tile(const uint64_t* __restrict__ ekeys, 
     }
 }
 
+// One tile of 1 < n <= 32 E pairs by one warp: a bitonic sort of the full
+// 64-bit keys (depth bits << 32 | Gaussian id -- unique, so the order is the
+// reference's (depth, Gaussian id) order with no tie handling), in registers.
+// Lane l holds elements l E .. l E + E - 1, so strides below E are register
+// exchanges and the others one shuffle per element; padding keys are
+// ~0ull and sort last.  Writes the Gaussian ids in order.
+template <int E>
+__device__ __forceinline__ void warp_bitonic_tile(const uint64_t* __restrict__ ekeys, uint32_t* __restrict__ vals,
+                                                  uint32_t off, int n) {
+    const int lane = threadIdx.x & 31;
+    constexpr int N = 32 * E;
+    uint64_t v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        v[e] = i < n ? ekeys[off + i] : ~0ull;
+    }
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < E) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if (e & j) continue;
+                    const int e2 = e | j;
+                    // ascending block: bit k of the element index lane E + e
+                    const bool asc = k < E ? (e & k) == 0 : (lane & (k / E)) == 0;
+                    const uint64_t a = v[e], b = v[e2];
+                    const bool sw = asc ? (b < a) : (a < b);
+                    v[e] = sw ? b : a;
+                    v[e2] = sw ? a : b;
+                }
+            } else {
+                const int lj = j / E;
+                const bool lower = (lane & lj) == 0;
+                const bool asc = (lane & (k / E)) == 0;
+                const bool take_min = lower == asc;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const uint64_t o = __shfl_xor_sync(0xffffffffu, v[e], lj);
+                    const bool lt = o < v[e];
+                    v[e] = (lt == take_min) ? o : v[e];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        if (i < n) vals[off + i] = static_cast<uint32_t>(v[e]);
+    }
+}
+
 // One large tile (n > kWarpSortMax) by the whole CTA.  n <= kCtaSortMax: each
 // warp holds a 256-key segment in registers and keys move through the shared
 // buffer `sbuf` (2048 keys); larger tiles stream segments of 2048 keys
@@ -443,53 +497,56 @@ __device__ __noinline__ void cta_sort_tile(uint64_t* __restrict__ src, uint64_t*
 }  // namespace
 
 // ---- K2: tile scan --------------------------------------------------------
-__global__ void __launch_bounds__(1024)
+// The histogram has kTileSlices counters per tile (K1 counts a pair into
+// slice gid % kTileSlices), so the scatter's returning atomics spread over
+// kTileSlices addresses per tile instead of queueing on one.  One thread per
+// tile: the tile's slices are scanned in place into their end offsets (the
+// scatter counts down), the tile total gives the range.
+__global__ void __launch_bounds__(kTileScanThreads)
 k_tile_scan(uint32_t* __restrict__ cnt, uint2* __restrict__ ranges, uint32_t T, Counters* ctr, uint64_t capacity,
             uint64_t* lb, uint32_t epoch, uint32_t* __restrict__ big_list) {
     griddep_wait();
-    constexpr int kItems = kTileScanPer / 1024;  // 8 consecutive tiles per thread
+    static_assert(kTileSlices == 8, "two uint4 loads per tile");
+    constexpr int kWarps = kTileScanThreads / 32;
     __shared__ uint32_t s_warp[32];
     __shared__ uint32_t s_tile, s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(&ctr->tile_ctr[4], 1u);
     __syncthreads();
-    const uint32_t tile = s_tile;
-    const uint64_t t0 = static_cast<uint64_t>(tile) * kTileScanPer + static_cast<uint64_t>(tid) * kItems;
-    uint32_t c[kItems];
-    if (t0 + kItems <= T) {
-        const uint4 a = *reinterpret_cast<const uint4*>(cnt + t0);
-        const uint4 b = *reinterpret_cast<const uint4*>(cnt + t0 + 4);
-        c[0] = a.x, c[1] = a.y, c[2] = a.z, c[3] = a.w, c[4] = b.x, c[5] = b.y, c[6] = b.z, c[7] = b.w;
-    } else {
-#pragma unroll
-        for (int i = 0; i < kItems; ++i) c[i] = t0 + i < T ? cnt[t0 + i] : 0u;
+    const uint32_t blk = s_tile;
+    const uint64_t t = static_cast<uint64_t>(blk) * kTileScanThreads + tid;
+    uint32_t c[kTileSlices] = {};
+    if (t < T) {
+        const uint4 a0 = *reinterpret_cast<const uint4*>(cnt + t * kTileSlices);
+        const uint4 a1 = *reinterpret_cast<const uint4*>(cnt + t * kTileSlices + 4);
+        c[0] = a0.x, c[1] = a0.y, c[2] = a0.z, c[3] = a0.w, c[4] = a1.x, c[5] = a1.y, c[6] = a1.z, c[7] = a1.w;
     }
     uint32_t sum = 0;
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) sum = sat_add(sum, c[i]);
+    for (int i = 0; i < kTileSlices; ++i) sum = sat_add(sum, c[i]);
     uint32_t incl = sum;
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl = sat_add(incl, t);
+        const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = sat_add(incl, x);
     }
     uint32_t excl = __shfl_up_sync(0xffffffffu, incl, 1);
     if (lane == 0) excl = 0;
     if (lane == 31) s_warp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-        const uint32_t v = s_warp[lane];
+        const uint32_t v = lane < kWarps ? s_warp[lane] : 0u;
         uint32_t vi = v;
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, vi, o);
-            if (lane >= o) vi = sat_add(vi, t);
+            const uint32_t x = __shfl_up_sync(0xffffffffu, vi, o);
+            if (lane >= o) vi = sat_add(vi, x);
         }
         uint32_t ve = __shfl_up_sync(0xffffffffu, vi, 1);
         if (lane == 0) ve = 0;
         const uint32_t agg = __shfl_sync(0xffffffffu, vi, 31);
-        const uint32_t prefix = lookback_warp(lb, tile, agg, epoch);
+        const uint32_t prefix = lookback_warp(lb, blk, agg, epoch);
         s_warp[lane] = ve;
         if (lane == 0) s_prefix = prefix;
-        if (lane == 0 && tile == gridDim.x - 1) {
+        if (lane == 0 && blk == gridDim.x - 1) {
             const uint32_t total = sat_add(prefix, agg);
             ctr->p = total;
             const bool fits = total != 0xffffffffu && total <= capacity;
@@ -498,105 +555,88 @@ k_tile_scan(uint32_t* __restrict__ cnt, uint2* __restrict__ ranges, uint32_t T, 
         }
     }
     __syncthreads();
-    uint32_t run = sat_add(sat_add(s_prefix, s_warp[warp]), excl);
+    const uint32_t start = sat_add(sat_add(s_prefix, s_warp[warp]), excl);
+    if (t < T) {
+        // slice i: [base_i, base_i + c_i); the scatter claims slots upward from base_i
+        uint32_t run = start;
+        uint32_t e[kTileSlices];
 #pragma unroll
-    for (int i = 0; i < kItems; ++i) {
-        const uint64_t t = t0 + i;
-        if (t < T) {
-            const uint32_t end = sat_add(run, c[i]);
-            ranges[t] = c[i] ? make_uint2(run, end) : make_uint2(0u, 0u);  // empty tiles: {0, 0} (pair_sort.cpp:30-42)
-            cnt[t] = end;  // the scatter counts down from the end
-            run = end;
+        for (int i = 0; i < kTileSlices; ++i) {
+            e[i] = run;
+            run = sat_add(run, c[i]);
         }
+        *reinterpret_cast<uint4*>(cnt + t * kTileSlices) = make_uint4(e[0], e[1], e[2], e[3]);
+        *reinterpret_cast<uint4*>(cnt + t * kTileSlices + 4) = make_uint4(e[4], e[5], e[6], e[7]);
+        ranges[t] = sum ? make_uint2(start, run) : make_uint2(0u, 0u);  // empty tiles: {0, 0} (pair_sort.cpp:30-42)
     }
     // tiles above kWarpSortMax pairs -> big_list (one atomic per warp)
-    uint32_t nbig = 0;
-#pragma unroll
-    for (int i = 0; i < kItems; ++i) nbig += (t0 + i < T && c[i] > static_cast<uint32_t>(kWarpSortMax)) ? 1u : 0u;
-    const uint32_t any_big = __ballot_sync(0xffffffffu, nbig != 0u);
-    if (any_big) {
-        uint32_t bincl = nbig;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, bincl, o);
-            if (lane >= o) bincl += t;
-        }
+    const bool big = t < T && sum > static_cast<uint32_t>(kWarpSortMax);
+    const uint32_t bb = __ballot_sync(0xffffffffu, big);
+    if (bb) {
         uint32_t bbase = 0;
-        if (lane == 31) bbase = atomicAdd(&ctr->tile_ctr[5], bincl);
-        bbase = __shfl_sync(0xffffffffu, bbase, 31) + bincl - nbig;
-#pragma unroll
-        for (int i = 0; i < kItems; ++i)
-            if (t0 + i < T && c[i] > static_cast<uint32_t>(kWarpSortMax)) big_list[bbase++] = static_cast<uint32_t>(t0 + i);
+        if (lane == 0) bbase = atomicAdd(&ctr->tile_ctr[5], static_cast<uint32_t>(__popc(bb)));
+        bbase = __shfl_sync(0xffffffffu, bbase, 0);
+        if (big) big_list[bbase + __popc(bb & ((1u << lane) - 1u))] = static_cast<uint32_t>(t);
     }
 }
 
 // ---- K3: scatter ------------------------------------------------------------
+// Every listed splat writes its (depth bits << 32 | gid) key into each hit
+// tile's segment at a slot claimed from its slice counter (one thread per
+// splat; the hit mask in groups of 8: a group's atomics are issued back to
+// back, then its stores).
 __global__ void __launch_bounds__(256)
 k_bucket_scatter(FrameParams p, SplatPlanes pl, BucketOut bk, const Counters* ctr, uint64_t* __restrict__ ekeys) {
     griddep_wait();
     if (ctr->p_eff == 0u) return;  // overflow (the host grows the arena and re-runs) or no pairs
     const uint32_t m = ctr->m;
-    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t stride = gridDim.x * blockDim.x;  // the grid covers the scene: one splat per thread
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += stride) {
         const uint4 r = bk.hits[j];
         const uint2 e = bk.gd[j];
         const uint64_t key = (static_cast<uint64_t>(e.y) << 32) | e.x;
-        TileTest t{};
-        if (r.w == kHitsRecompute) {  // span over 64 tiles: re-run the test
-            const float4 a = pl.p0[e.x];
-            t.mode = p.mode;
-            t.cx = a.x;
-            t.cy = a.y;
-            t.ixx = a.z;
-            t.ixy = 0.5f * a.w;
-            t.iyy = pl.p1[e.x].x;
-            t.rx = __uint_as_float(r.x);
-            t.ry = __uint_as_float(r.y);
-            t.r2 = __uint_as_float(r.z);
-            t.v1x = t.v1y = t.a = t.b = 0.0f;
-            if (p.mode == AGSX_MODE_OBB) {
-                const float4 o = pl.p4[e.x];
-                t.v1x = o.x;
-                t.v1y = o.y;
-                t.a = o.z;
-                t.b = o.w;
-            }
-        }
+        const uint32_t slice = e.x % kTileSlices;  // K1 counted this splat's pairs in that slice
         if (r.w != kHitsRecompute) {
-            // the hit mask in groups of 8: the group's atomics are issued back
-            // to back (independent), then its stores
             unsigned long long mask = static_cast<unsigned long long>(r.x) | (static_cast<unsigned long long>(r.y) << 32);
-            const uint32_t tx0 = r.z & 0xffffu, ty0 = r.z >> 16, sw = r.w;
-            uint32_t row_base = ty0 * static_cast<uint32_t>(p.tiles_x) + tx0;  // tile id of bit row_start
-            uint32_t row_start = 0;
+            uint4 rr = r;
             while (mask) {
-                uint32_t tile[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    tile[u] = 0xffffffffu;
-                    if (mask) {
-                        const uint32_t b = static_cast<uint32_t>(__ffsll(static_cast<long long>(mask)) - 1);
-                        mask &= mask - 1;
-                        while (b >= row_start + sw) {
-                            row_start += sw;
-                            row_base += static_cast<uint32_t>(p.tiles_x);
-                        }
-                        tile[u] = row_base + (b - row_start);
-                    }
-                }
-                uint32_t pos[8];
+                rr.x = static_cast<uint32_t>(mask);
+                rr.y = static_cast<uint32_t>(mask >> 32);
+                uint32_t tl[8], pos[8];
+                tiles_of_mask(rr, p.tiles_x, tl);
+                const int cnt = min(__popcll(static_cast<long long>(mask)), 8);
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (tile[u] != 0xffffffffu) pos[u] = atomicSub(&bk.tile_cnt[tile[u]], 1u) - 1u;
+                    if (u < cnt) pos[u] = atomicAdd(&bk.tile_cnt[tl[u] * kTileSlices + slice], 1u);
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (tile[u] != 0xffffffffu) ekeys[pos[u]] = key;
+                    if (u < cnt) ekeys[pos[u]] = key;
+                for (int u = 0; u < cnt; ++u) mask &= mask - 1;  // the group's bits
             }
             continue;
         }
+        TileTest t{};  // span over 64 tiles: re-run the test
+        const float4 a = pl.p0[e.x];
+        t.mode = p.mode;
+        t.cx = a.x;
+        t.cy = a.y;
+        t.ixx = a.z;
+        t.ixy = 0.5f * a.w;
+        t.iyy = pl.p1[e.x].x;
+        t.rx = __uint_as_float(r.x);
+        t.ry = __uint_as_float(r.y);
+        t.r2 = __uint_as_float(r.z);
+        t.v1x = t.v1y = t.a = t.b = 0.0f;
+        if (p.mode == AGSX_MODE_OBB) {
+            const float4 o = pl.p4[e.x];
+            t.v1x = o.x;
+            t.v1y = o.y;
+            t.a = o.z;
+            t.b = o.w;
+        }
         hit_tiles(t, p, r, [&](int tx, int ty) {
             const uint32_t tile = static_cast<uint32_t>(ty * p.tiles_x + tx);
-            const uint32_t pos = atomicSub(&bk.tile_cnt[tile], 1u) - 1u;
-            ekeys[pos] = key;
+            ekeys[atomicAdd(&bk.tile_cnt[tile * kTileSlices + slice], 1u)] = key;
         });
     }
 }
@@ -648,6 +688,7 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
             }
             if (n > static_cast<uint32_t>(kWarpSortMax)) continue;  // a CTA sorted it
             const int ni = static_cast<int>(n);
+#ifdef AGSX_TS_RADIX
             if (ni <= 32)
                 warp_sort_tile<1>(ekeys, vals, lo, ni, buf, hist);
             else if (ni <= 64)
@@ -656,6 +697,18 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
                 warp_sort_tile<4>(ekeys, vals, lo, ni, buf, hist);
             else
                 warp_sort_tile<8>(ekeys, vals, lo, ni, buf, hist);
+#else
+            (void)buf;
+            (void)hist;
+            if (ni <= 32)
+                warp_bitonic_tile<1>(ekeys, vals, lo, ni);
+            else if (ni <= 64)
+                warp_bitonic_tile<2>(ekeys, vals, lo, ni);
+            else if (ni <= 128)
+                warp_bitonic_tile<4>(ekeys, vals, lo, ni);
+            else
+                warp_bitonic_tile<8>(ekeys, vals, lo, ni);
+#endif
         }
     }
 }

@@ -318,9 +318,11 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
             pl.p2[gi] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(pack_extent(ex, ey)));
             if (p.mode == AGSX_MODE_OBB) pl.p4[gi] = make_float4(tt.v1x, tt.v1y, tt.a, tt.b);
             if (bk.tile_cnt) {
-                // tile histogram of the bucketed sort: one reduction per hit tile
+                // tile histogram of the bucketed sort, counted in slice gid %
+                // kTileSlices of each hit tile (fire-and-forget reductions)
+                const uint32_t slice = gi % kTileSlices;
                 hit_tiles(tt, p, hits, [&](int tx, int ty) {
-                    atomicAdd(&bk.tile_cnt[static_cast<uint32_t>(ty * p.tiles_x + tx)], 1u);
+                    atomicAdd(&bk.tile_cnt[static_cast<uint32_t>(ty * p.tiles_x + tx) * kTileSlices + slice], 1u);
                 });
             } else {
                 reinterpret_cast<uint4*>(pl.p3)[gi] = hits;

@@ -46,7 +46,7 @@ struct FrameZero {
 // id, depth bits}), in no particular order -- the per-tile sort makes the
 // final order deterministic.
 struct BucketOut {
-    uint32_t* tile_cnt = nullptr;  // tiles; zeroed before K1
+    uint32_t* tile_cnt = nullptr;  // tiles x kTileSlices pair counts (slice = gid % kTileSlices); zeroed before K1
     uint4* hits = nullptr;         // P3 hit record per listed splat
     uint2* gd = nullptr;           // {gid, depth bits} per listed splat
 };
@@ -59,9 +59,11 @@ __global__ void k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_
 // counts), P / capacity, and the list of tiles above kWarpSortMax pairs.
 constexpr int kWarpSortMax = 256;   // pairs per tile sorted by one warp (keys in registers)
 constexpr int kCtaSortMax = 2048;  // ... by one CTA with the keys in registers / shared memory
-constexpr int kTileScanPer = 8192;  // tiles per scan CTA
-__global__ void k_tile_scan(uint32_t* cnt, uint2* ranges, uint32_t T, Counters* ctr, uint64_t capacity,
-                            uint64_t* lb, uint32_t epoch, uint32_t* big_list);
+constexpr int kTileSlices = 8;  // histogram counters per tile (bucketed sort)
+constexpr int kTileScanThreads = 256;
+constexpr int kTileScanPer = kTileScanThreads;  // tiles per scan CTA (one per thread)
+__global__ void k_tile_scan(uint32_t* cnt, uint2* ranges, uint32_t T, Counters* ctr, uint64_t capacity, uint64_t* lb,
+                            uint32_t epoch, uint32_t* big_list);
 // K3: scatter of (depth bits << 32 | gid) into each tile's segment (one
 // returning atomic per pair on the tile's end offset).
 __global__ void k_bucket_scatter(FrameParams p, SplatPlanes pl, BucketOut bk, const Counters* ctr,

@@ -110,3 +110,12 @@ def test_render_without_gpu_fails_loudly():
         P.render(s, view=0)
     with pytest.raises(capi.AgsxError):
         capi.Context(0)
+
+
+def test_stage_nvtx_ranges_compiled_in():
+    """SURVEY.md §5 (stage tracing): the frame path pushes NVTX ranges named
+    after the reference's stage_times keys; an nsys/ncu NVTX capture shows
+    them on the host thread. Without a tool attached they cost a few ns."""
+    data = open(capi.LIB_PATH, "rb").read()
+    for name in (b"agsx.render", b"agsx.preprocess", b"agsx.pair_gen+sort", b"agsx.raster", b"agsx.wait"):
+        assert name + b"\0" in data, name
