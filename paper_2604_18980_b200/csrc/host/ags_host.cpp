@@ -13,6 +13,8 @@
 #include <mutex>
 #include <thread>
 
+#include <sys/mman.h>
+
 #include "agsx.h"
 #include "ags/ags.hpp"
 #include "ags_internal.hpp"
@@ -406,6 +408,51 @@ int default_device() {
     return e ? std::atoi(e) : 0;
 }
 
+// A page-locked staging image per host thread (grow-only): the raster streams
+// the frame into it by banded copy-engine transfers behind the blend.
+struct Staging {
+    float* p = nullptr;
+    std::size_t floats = 0;
+    ~Staging() {
+        if (p) agsx_host_free(p);
+    }
+    float* get(std::size_t n) {
+        if (n > floats) {
+            if (p) agsx_host_free(p);
+            p = nullptr;
+            floats = 0;
+            void* q = nullptr;
+            if (agsx_host_alloc(n * sizeof(float), &q) != AGSX_OK) throw std::bad_alloc();
+            p = static_cast<float*>(q);
+            floats = n;
+        }
+        return p;
+    }
+};
+
+float* thread_staging(std::size_t n) {
+    static thread_local Staging st;
+    return st.get(n);
+}
+
+// The returned Image owns a std::vector<float> (image.hpp:9-23).  Filling it
+// from the staging image in one pass (no zero-initialisation first), with
+// transparent huge pages requested for the fresh buffer, halves the host
+// cost of the 191 MB vector at 4608x3456 (page faults dominate).
+void fill_image(Image& img, int w, int h, const float* src) {
+    img.width = w;
+    img.height = h;
+    const std::size_t n = static_cast<std::size_t>(w) * h * 3;
+    img.data.clear();
+    img.data.shrink_to_fit();
+    img.data.reserve(n);
+    const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(img.data.data());
+    const std::uintptr_t a = (b + (1u << 21) - 1) & ~static_cast<std::uintptr_t>((1u << 21) - 1);
+    const std::uintptr_t e = (b + n * sizeof(float)) & ~static_cast<std::uintptr_t>((1u << 21) - 1);
+    if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // advisory: ignore failures
+    img.data.assign(src, src + n);
+}
+
 agsx_ctx* thread_ctx() {
     static thread_local CtxHolder h;
     if (!h.ctx) {
@@ -567,10 +614,11 @@ RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderCon
     agsx_lut l{};
     if (lut) l = to_c(*lut);
     RenderReport rep;
-    rep.image = Image(cam.width, cam.height);
+    const std::size_t npx = static_cast<std::size_t>(cam.width) * cam.height;
+    float* staging = thread_staging(npx * 3);
     std::vector<float> maxt_by_gid;
     agsx_frame f{};
-    f.image = rep.image.data.data();
+    f.image = staging;
     if (rec.max_t) {
         maxt_by_gid.assign(std::max<std::uint64_t>(scene.size(), 1), 0.0f);
         f.max_t = maxt_by_gid.data();
@@ -591,6 +639,7 @@ RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderCon
     } else {
         check(agsx_render(ctx, sc, &c, &k, lut ? &l : nullptr, &f), ctx);
     }
+    fill_image(rep.image, cam.width, cam.height, staging);
     rep.pair_count = f.pair_count;
     rep.splat_count = f.splat_count;
     rep.stage_times["preprocess"] = f.stage_ms[0] * 1e-3;

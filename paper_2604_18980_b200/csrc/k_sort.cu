@@ -13,6 +13,10 @@
 // means value = input index.  The element count may live on the device.
 #include "kernels.cuh"
 
+#ifndef AGSX_DS_MINB
+#define AGSX_DS_MINB 5  // downsweep CTAs per SM (register cap): 3 -> 5 measured sort 0.216 -> 0.205 ms
+#endif
+
 namespace agsx {
 
 namespace {
@@ -146,7 +150,7 @@ k_scan_counts(uint32_t* __restrict__ counts, int G, uint32_t* __restrict__ total
 // contiguous per-digit runs to global memory at base[d] = (digits below d)
 // + (earlier chunks' digit-d keys) + (earlier tiles of this chunk).
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads, 3)
+__global__ void __launch_bounds__(kSortThreads, AGSX_DS_MINB)
 k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
             uint32_t* __restrict__ vout, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
             K sentinel, const uint32_t* __restrict__ counts_excl, const uint32_t* __restrict__ totals,
