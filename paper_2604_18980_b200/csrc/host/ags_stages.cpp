@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 #include "agsx.h"
 #include "ags/ags.hpp"
@@ -161,25 +162,55 @@ void raster_tile(std::span<const GaussianTilePair> tile_pairs, std::span<const S
 // --------------------------------------------------- device-scene cache
 namespace {
 
-// FNV-1a over the bytes of up to 1024 evenly spaced Gaussians (every field,
-// SH included) and the count.
+// Fingerprint of the WHOLE scene (every field of every Gaussian, SH
+// included, and the count), so a caller that edits the span between calls --
+// which the reference's render(span) simply re-reads -- never gets a stale
+// device copy.  64-bit words mixed per thread over contiguous blocks of
+// Gaussians (hardware threads, up to 32), the block hashes combined in order.
 std::uint64_t scene_fingerprint(std::span<const Gaussian3D> scene) {
-    std::uint64_t h = 1469598103934665603ull;
-    auto mix = [&](const void* p, std::size_t n) {
-        const auto* b = static_cast<const unsigned char*>(p);
-        for (std::size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 1099511628211ull;
-    };
     const std::size_t n = scene.size();
-    mix(&n, sizeof(n));
-    const std::size_t samples = std::min<std::size_t>(n, 1024);
-    for (std::size_t s = 0; s < samples; ++s) {
-        const Gaussian3D& g = scene[samples == n ? s : (s * (n - 1)) / (samples - 1)];
-        mix(&g.mean, sizeof(g.mean));
-        mix(&g.scale, sizeof(g.scale));
-        mix(&g.rotation, sizeof(g.rotation));
-        mix(&g.opacity, sizeof(g.opacity));
-        mix(g.sh.data(), g.sh.size() * sizeof(float));
-    }
+    auto hash_range = [&](std::size_t lo, std::size_t hi) {
+        std::uint64_t h = 0x9e3779b97f4a7c15ull ^ lo;
+        auto mix = [&h](std::uint64_t v) {
+            h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+            h *= 0xff51afd7ed558ccdull;
+        };
+        for (std::size_t i = lo; i < hi; ++i) {
+            const Gaussian3D& g = scene[i];
+            std::uint64_t w[6];
+            static_assert(sizeof(g.mean) + sizeof(g.scale) + sizeof(g.rotation) + sizeof(g.opacity) == 44,
+                          "Gaussian3D fields");
+            std::memcpy(w, &g.mean, 12);
+            std::memcpy(reinterpret_cast<char*>(w) + 12, &g.scale, 12);
+            std::memcpy(reinterpret_cast<char*>(w) + 24, &g.rotation, 16);
+            std::memcpy(reinterpret_cast<char*>(w) + 40, &g.opacity, 4);
+            reinterpret_cast<std::uint32_t*>(w)[11] = static_cast<std::uint32_t>(g.sh.size());
+            for (std::uint64_t v : w) mix(v);
+            const float* sh = g.sh.data();
+            std::size_t k = 0;
+            for (; k + 2 <= g.sh.size(); k += 2) {
+                std::uint64_t v;
+                std::memcpy(&v, sh + k, 8);
+                mix(v);
+            }
+            if (k < g.sh.size()) {
+                std::uint32_t v;
+                std::memcpy(&v, sh + k, 4);
+                mix(v);
+            }
+        }
+        return h;
+    };
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    const std::size_t parts = n < (1u << 16) ? 1 : hw;
+    std::vector<std::uint64_t> hs(parts);
+    std::vector<std::thread> ts;
+    for (std::size_t t = 1; t < parts; ++t)
+        ts.emplace_back([&, t] { hs[t] = hash_range(n * t / parts, n * (t + 1) / parts); });
+    hs[0] = hash_range(0, n / parts);
+    for (auto& th : ts) th.join();
+    std::uint64_t h = 1469598103934665603ull ^ n;
+    for (std::uint64_t v : hs) h = (h ^ v) * 1099511628211ull;
     return h;
 }
 

@@ -40,6 +40,19 @@ int main(int argc, char** argv) {
     const ags::DeviceScene dev(s.gaussians);
     const ags::RenderReport rep2 = ags::render(dev, cam, cfg, lp);
     const bool same = rep.pair_count == rep2.pair_count && rep.image.data == rep2.image.data;
+    // the span's device copy is cached across calls: an in-place edit of ANY
+    // Gaussian must show in the next render(span) (the reference re-reads the
+    // span every call) -- every Gaussian is hidden here, then restored
+    std::vector<ags::Gaussian3D> edited = s.gaussians;
+    (void)ags::render(edited, cam, cfg, lp);  // cached
+    for (auto& g : edited) g.opacity = 0.0f;  // nothing survives the culls
+    const ags::RenderReport rep_hidden = ags::render(edited, cam, cfg, lp);
+    edited[edited.size() / 2 + 1].opacity = s.gaussians[edited.size() / 2 + 1].opacity;
+    const ags::RenderReport rep_one = ags::render(edited, cam, cfg, lp);  // one Gaussian back
+    edited = s.gaussians;
+    const ags::RenderReport rep_back = ags::render(edited, cam, cfg, lp);
+    const bool cache_ok = rep_hidden.splat_count == 0 && rep_one.splat_count <= 1 &&
+                          rep_back.pair_count == rep.pair_count && rep_back.image.data == rep.image.data;
     std::ofstream(argv[10], std::ios::binary)
         .write(reinterpret_cast<const char*>(rep.image.data.data()),
                static_cast<std::streamsize>(rep.image.data.size() * sizeof(float)));
@@ -80,8 +93,8 @@ int main(int argc, char** argv) {
         ++errors_ok;
     }
     std::printf("{\"pair_count\": %zu, \"splat_count\": %zu, \"device_scene_same\": %s, \"errors_ok\": %d, "
-                "\"stage_keys\": %zu, \"contributions\": %zu}\n",
+                "\"stage_keys\": %zu, \"contributions\": %zu, \"cache_follows_edits\": %s}\n",
                 rep.pair_count, rep.splat_count, same ? "true" : "false", errors_ok, rep.stage_times.size(),
-                rep3.contributions.size());
+                rep3.contributions.size(), cache_ok ? "true" : "false");
     return 0;
 }

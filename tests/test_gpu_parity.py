@@ -791,6 +791,7 @@ def test_cxx_drop_in_caller(tmp_path, port, layout, mode, k, lutbin):
     img = np.fromfile(out, np.float32).reshape(240, 320, 3)
     assert np.max(np.abs(img - want["image"])) <= IMG_MAX_ABS
     assert res["device_scene_same"] and res["errors_ok"] == 3 and res["stage_keys"] == 4
+    assert res["cache_follows_edits"]  # render(span)'s device-scene cache never serves a stale scene
     # RecordOptions{max_t, contributions} (analysis.cpp:171-173): the oracle's stream, record for record
     cfg = port.config(mode, k=k)
     lut = port.lut([lutbin] * 20) if lutbin else None
