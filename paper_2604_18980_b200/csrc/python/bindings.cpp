@@ -15,6 +15,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <limits>
@@ -104,6 +105,10 @@ struct LutHolder {
 // Pool of page-locked image buffers: a returned numpy image owns one block
 // (capsule) and gives it back to the pool when the array is freed, so the
 // device->host image copy runs at full link bandwidth without re-pinning.
+// The page-locked bytes held by live images are capped (AGS_PINNED_POOL_MB,
+// default 2048): a caller that keeps many frames gets ordinary (pageable)
+// arrays past the cap -- one extra host copy each -- instead of pinning
+// unbounded host memory.
 class PinnedPool {
 public:
     static PinnedPool& get() {
@@ -117,20 +122,32 @@ public:
                 if (it->second >= bytes && it->second <= 2 * bytes) {
                     void* p = it->first;
                     sizes_[p] = it->second;
+                    live_ += it->second;
                     free_.erase(it);
                     return p;
                 }
+            if (live_ + bytes > cap()) return nullptr;  // pageable past the cap
         }
         void* p = nullptr;
         if (agsx_host_alloc(bytes, &p) != AGSX_OK) return nullptr;
         std::lock_guard<std::mutex> g(mu_);
         sizes_[p] = bytes;
+        live_ += bytes;
         return p;
+    }
+    static std::size_t cap() {
+        static const std::size_t c = [] {
+            const char* e = std::getenv("AGS_PINNED_POOL_MB");
+            const long long mb = e ? std::atoll(e) : 2048;
+            return static_cast<std::size_t>(mb > 0 ? mb : 0) << 20;
+        }();
+        return c;
     }
     void release(void* p) {
         std::lock_guard<std::mutex> g(mu_);
         auto it = sizes_.find(p);
         if (it == sizes_.end()) return;
+        live_ -= it->second;
         free_.emplace_back(p, it->second);
         sizes_.erase(it);
         while (free_.size() > 4) {  // bound the cached pinned memory
@@ -143,6 +160,7 @@ private:
     std::mutex mu_;
     std::vector<std::pair<void*, std::size_t>> free_;
     std::map<void*, std::size_t> sizes_;
+    std::size_t live_ = 0;  // page-locked bytes owned by live arrays
 };
 
 template <typename T>

@@ -972,3 +972,27 @@ def test_tile_sizes_above_64(ctx, port):
     for ts in (64, 80, 128, 200):
         check_frame(ctx, port, oscene, dev, 0, "ellipse", background=(0.2, 0.2, 0.2), tile_size=ts)
         check_frame(ctx, port, oscene, dev, 0, "aabb", tile_size=ts)
+
+
+def test_kept_frames_past_the_pinned_cap(tmp_path):
+    """a caller that keeps its frames. Page-locked images
+    are capped (AGS_PINNED_POOL_MB); past the cap render() returns ordinary
+    arrays. Every kept frame stays intact and equal to a fresh render."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1])\n"
+        "import paper_2604_18980_b200 as P\n"
+        "s = P.synth_scene(3, 3000, 'veil', cameras=4, width=320, height=240, focal=250.0)\n"
+        "kept = [P.render(s, v % 4, 'ellipse')['image'] for v in range(8)]\n"
+        "pinned = sum(1 for a in kept if not a.flags['OWNDATA'] and a.base is not None)\n"
+        "for v in range(8):\n"
+        "    again = P.render(s, v % 4, 'ellipse')['image']\n"
+        "    assert np.array_equal(kept[v].view(np.uint32), again.view(np.uint32)), v\n"
+        "print('ok', pinned)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, AGS_PINNED_POOL_MB="2")  # two 0.9 MB frames fit
+    out = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().startswith("ok")
