@@ -171,13 +171,14 @@ def moved_bytes(n, m, p, p_it, tiles, px, depth_passes, bucketed):
     Tile-bucketed path (AGSX_SORT=bucket): K1 adds a 4 B reduction per pair
     and writes a 24 B list entry per splat instead of P3 + depth key; the
     scatter reads the list and does a 4 B atomic + 8 B write per pair; the
-    sort reads 8 B and writes 4 B per pair plus the 12 B-per-tile scan."""
+    sort reads 8 B and writes 4 B per pair plus the scan (8 histogram slices
+    per tile read and written, 8 B range: 72 B per tile)."""
     raster = 52 * p_it + 16 * tiles + 12 * px
     if bucketed:
         return {
             "preprocess": 56 * n + 4 * n + 48 * m + 24 * m + 8 * p + 16 * tiles,
             "pair_gen": 24 * m + 8 * p + 8 * p,
-            "sort": 12 * tiles + 8 * p + 4 * p,
+            "sort": 72 * tiles + 8 * p + 4 * p,
             "raster": raster,
         }
     return {
