@@ -260,6 +260,37 @@ __device__ __forceinline__ void for_each_tile_hit(const TileTest& t, const Frame
     const float cx = t.cx, cy = t.cy;
     float y0 = static_cast<float>(s.ty0) * ts;  // tile coordinates advance by exact float adds
     const float x0_first = static_cast<float>(s.tx0) * ts;
+#ifdef AGSX_K1_BRANCHFREE
+    // Variant (measured slower: preprocess 0.185 vs 0.177 ms):
+    // branch-free per tile, all four edge minima evaluated and OR-ed, one
+    // exact division per tile (a column's right-edge minimiser is the next
+    // column's left one).  The default below exits at the first edge that
+    // hits, which on K1's packed survivor warps is usually the first one.
+    for (int ty = s.ty0; ty <= s.ty1; ++ty, y0 += ts) {
+        const float y1 = smin(y0 + ts, H);
+        const float dy0 = y0 - cy, dy1 = y1 - cy;
+        const float xh0 = cx - t.ixy * dy0 / t.ixx;
+        const float xh1 = cx - t.ixy * dy1 / t.ixx;
+        const bool row_in = cy >= y0 && cy <= y1;
+        const bool row_box = y0 <= cy + t.ry && cy - t.ry <= y1;
+        float x0 = x0_first;
+        float yv0 = cy - t.ixy * (x0 - cx) / t.iyy;
+        for (int tx = s.tx0; tx <= s.tx1; ++tx, x0 += ts) {
+            const float x1 = smin(x0 + ts, W);
+            const float dxl = x0 - cx, dxr = x1 - cx;
+            const float yv1 = cy - t.ixy * dxr / t.iyy;
+            const bool box = row_box && x0 <= cx + t.rx && cx - t.rx <= x1;
+            const bool in = row_in && cx >= x0 && cx <= x1;  // centre inside: min = 0 <= r2
+            const bool h0 = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh0, x0, x1) - cx, dy0) <= t.r2;
+            const bool h1 = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh1, x0, x1) - cx, dy1) <= t.r2;
+            const bool v0 = quad_form(t.ixx, t.ixy, t.iyy, dxl, sclamp(yv0, y0, y1) - cy) <= t.r2;
+            const bool v1 = quad_form(t.ixx, t.ixy, t.iyy, dxr, sclamp(yv1, y0, y1) - cy) <= t.r2;
+            if (box && (in || h0 || h1 || v0 || v1)) f(tx, ty);
+            yv0 = yv1;
+        }
+    }
+    return;
+#endif
     for (int ty = s.ty0; ty <= s.ty1; ++ty, y0 += ts) {
         const float y1 = smin(y0 + ts, H);
         const float dy0 = y0 - cy, dy1 = y1 - cy;
