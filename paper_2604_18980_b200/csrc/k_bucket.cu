@@ -12,25 +12,31 @@
 // id).  Here:
 //   K1 (k_preprocess) counts the pairs of every tile (one reduction per hit
 //      tile) and lists the splats with tiles;
-//   K2 (k_tile_scan) scans the tile counts: the ranges, each tile's end
+//   K2 (k_tile_scan) scans the tile counts: the ranges, each slice's base
 //      offset, P and the capacity check -- the tile offsets ARE the ranges;
 //   K3 (k_bucket_scatter) writes every pair's (depth bits << 32 | gid) into
-//      its tile's segment through a returning atomic on the end offset (the
+//      its tile's segment through a returning atomic on its slice cursor (the
 //      slot order within a segment is arbitrary);
 //   K4 (k_tile_sort) sorts each segment by that 64-bit key, which restores
 //      the reference's (depth, Gaussian id) order bit for bit, and writes
 //      the Gaussian ids for the rasterizer.
 // Nothing global is sorted: P pairs are written once and read once, and the
-// depth sort of the splats is gone.
+// depth sort of the splats is gone.  K1's histogram is spread over
+// kTileSlices counters per tile (slice = gid % kTileSlices).
 //
-// Per-tile sort: an LSD radix sort on 8-bit digits of (depth - min depth of
-// the tile) -- usually 3 digits -- ranked by warp multisplit (8 ballots per
-// digit).  Equal depths within a tile (a few hundred tiles per frame) are
-// detected afterwards; such a tile is re-sorted with the Gaussian-id digits
-// first, so every order is exact.  A tile of <= 256 pairs is one warp's work
-// with the keys in registers; up to 2048 pairs one CTA's (keys in registers,
-// exchanged through shared memory); larger tiles stream through a global
-// ping-pong buffer, one CTA each.
+// Per-tile sort: a tile of <= 256 pairs is one warp's register bitonic sort
+// of the full 64-bit keys (unique: no tie handling).  Larger tiles are one
+// CTA's LSD radix sort on 8-bit digits of (depth - min depth of the tile),
+// ranked by warp multisplit (8 ballots per digit), with the keys in
+// registers / shared memory up to 2048 pairs and streamed through a global
+// ping-pong buffer above; equal depths within such a tile are detected
+// afterwards and ordered by Gaussian id (a re-sort with the gid digits first
+// when a run is long), so every order is exact.
+//
+// Measured at config 3: bit-exact, but not faster than the
+// depth-then-tile path (the scatter is latency-bound on its scattered
+// accesses, the per-tile sort ALU-bound), so it is selected with
+// AGSX_SORT=bucket only.
 #include "kernels.cuh"
 
 namespace agsx {
@@ -80,16 +86,12 @@ __device__ __forceinline__ void warp_rank(const uint64_t (&k)[NC], int nvalid, P
         if (c * 32 >= nvalid) break;  // warp-uniform
         const bool ok = c * 32 + lane < nvalid;
         const uint32_t d = dg(k[c]);
-#ifdef AGSX_TS_MATCH
-        const uint32_t pm = __match_any_sync(0xffffffffu, ok ? d : 0x100u + lane) & __ballot_sync(0xffffffffu, ok);
-#else
         uint32_t pm = __ballot_sync(0xffffffffu, ok);
 #pragma unroll
         for (int b = 0; b < 8; ++b) {
             const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
             pm &= ((d >> b) & 1u) ? bal : ~bal;
         }
-#endif
         const uint32_t lt = pm & lt_mask;
         const uint32_t before = hist[d];
         rank[c] = before + __popc(lt);
@@ -99,67 +101,12 @@ __device__ __forceinline__ void warp_rank(const uint64_t (&k)[NC], int nvalid, P
     }
 }
 
-// Exclusive scan of a warp's 256-bin histogram in place (lane l owns bins
-// 8l .. 8l+7); returns nothing, hist[d] = keys of digits below d.
-__device__ __forceinline__ void warp_scan256(uint32_t* hist) {
-    const int lane = threadIdx.x & 31;
-    uint4* h4 = reinterpret_cast<uint4*>(hist) + 2 * lane;
-    const uint4 a = h4[0], b = h4[1];
-    const uint32_t s = a.x + a.y + a.z + a.w + b.x + b.y + b.z + b.w;
-    uint32_t incl = s;
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-    }
-    uint32_t r = incl - s;
-    uint4 oa, ob;
-    oa.x = r;
-    r += a.x;
-    oa.y = r;
-    r += a.y;
-    oa.z = r;
-    r += a.z;
-    oa.w = r;
-    r += a.w;
-    ob.x = r;
-    r += b.x;
-    ob.y = r;
-    r += b.y;
-    ob.z = r;
-    r += b.z;
-    ob.w = r;
-    __syncwarp();
-    h4[0] = oa;
-    h4[1] = ob;
-    __syncwarp();
-}
-
 __device__ __forceinline__ void warp_zero256(uint32_t* hist) {
     const int lane = threadIdx.x & 31;
     uint4* h4 = reinterpret_cast<uint4*>(hist) + 2 * lane;
     h4[0] = make_uint4(0u, 0u, 0u, 0u);
     h4[1] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
-}
-
-// Adjacent equal depths in the sorted keys held lane-strided in k[].
-template <int NC>
-__device__ __forceinline__ bool warp_has_tie(const uint64_t (&k)[NC], int n) {
-    const int lane = threadIdx.x & 31;
-    bool tie = false;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (c * 32 >= n) break;
-        const uint32_t hi = static_cast<uint32_t>(k[c] >> 32);
-        uint32_t nx = __shfl_down_sync(0xffffffffu, hi, 1);
-        if (c + 1 < NC) {
-            const uint32_t first_next = __shfl_sync(0xffffffffu, static_cast<uint32_t>(k[c + 1] >> 32), 0);
-            if (lane == 31) nx = first_next;
-        }
-        const int i = c * 32 + lane;
-        tie |= i + 1 < n && hi == nx;
-    }
-    return __any_sync(0xffffffffu, tie);
 }
 
 // New position of the key at sorted index i when its depth ties a
@@ -177,83 +124,6 @@ __device__ __forceinline__ int tie_position(const uint64_t* buf, int n, int i, u
     int r = 0;
     for (int j = s; j < e; ++j) r += buf[j] < key ? 1 : 0;
     return s + r;
-}
-
-// One tile of n <= NC*32 pairs by one warp.  buf: the warp's 256-key shared
-// buffer; hist: its 256 counters.  LSD passes over the depth digits; equal
-// depths (rare) are then ordered by Gaussian id within their run.
-template <int NC>
-__device__ __noinline__ void warp_sort_tile(const uint64_t* __restrict__ ekeys, uint32_t* __restrict__ vals,
-                                            uint32_t off, int n, uint64_t* buf, uint32_t* hist) {
-    const int lane = threadIdx.x & 31;
-    uint64_t k[NC];
-    uint32_t rank[NC];
-    uint32_t dmin = 0xffffffffu, dmax = 0u, gmax = 0u;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const int i = c * 32 + lane;
-        k[c] = i < n ? ekeys[off + i] : 0ull;
-        if (i < n) {
-            const uint32_t hi = static_cast<uint32_t>(k[c] >> 32);
-            dmin = min(dmin, hi);
-            dmax = max(dmax, hi);
-            gmax = max(gmax, static_cast<uint32_t>(k[c]));
-        }
-    }
-    dmin = __reduce_min_sync(0xffffffffu, dmin);
-    dmax = __reduce_max_sync(0xffffffffu, dmax);
-    gmax = __reduce_max_sync(0xffffffffu, gmax);
-    const int nd = digits_for(dmax - dmin);
-    int ng = 0;  // gid digits: only when a run of equal depths is too long for the fix-up
-    int pos[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) pos[c] = c * 32 + lane;
-    for (int attempt = 0; attempt < 2; ++attempt) {
-        const int np = ng + nd;
-        for (int ps = 0; ps < np; ++ps) {
-            const PassDigit dg = pass_digit(ps, ng, dmin);
-            warp_zero256(hist);
-            warp_rank<NC>(k, n, dg, hist, rank);
-            warp_scan256(hist);
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const int i = c * 32 + lane;
-                if (c * 32 >= n) break;
-                if (i < n) buf[hist[dg(k[c])] + rank[c]] = k[c];
-            }
-            __syncwarp();
-#pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                const int i = c * 32 + lane;
-                if (c * 32 >= n) break;
-                if (i < n) k[c] = buf[i];
-            }
-            __syncwarp();
-        }
-        if (ng > 0 || !warp_has_tie<NC>(k, n)) break;
-        if (np == 0) {  // all depths equal: stage the keys for the run scan
-#pragma unroll
-            for (int c = 0; c < NC; ++c)
-                if (c * 32 + lane < n) buf[c * 32 + lane] = k[c];
-            __syncwarp();
-        }
-        bool long_run = false;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const int i = c * 32 + lane;
-            if (c * 32 >= n) break;
-            if (i < n) pos[c] = tie_position(buf, n, i, k[c], long_run);
-        }
-        if (!__any_sync(0xffffffffu, long_run)) break;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) pos[c] = c * 32 + lane;
-        ng = digits_for(gmax);  // a long run: the gid digits first, then depth again
-        if (ng == 0) break;
-    }
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (c * 32 + lane < n) vals[off + pos[c]] = static_cast<uint32_t>(k[c]);
-    }
 }
 
 // One tile of 1 < n <= 32 E pairs by one warp: a bitonic sort of the full
@@ -650,7 +520,7 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
     __shared__ __align__(16) uint32_t s_hist[kTSWarps][256];            // 8 KB
     __shared__ uint32_t s_base[256], s_red[32];
     __shared__ uint32_t s_claim;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     if (ctr->p_eff == 0u) {
         // overflow: the scan's offsets are not valid; empty ranges for the raster
         for (uint32_t t = blockIdx.x * blockDim.x + tid; t < T; t += gridDim.x * blockDim.x)
@@ -669,8 +539,6 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
         cta_sort_tile(ekeys + r.x, ekeys2 + r.x, vals + r.x, r.y - r.x, s_keys, s_hist, s_base, s_red);
     }
     // then one warp per tile, tiles claimed four at a time
-    uint64_t* buf = s_keys + warp * kWarpSortMax;
-    uint32_t* hist = s_hist[warp];
     while (true) {
         uint32_t t0 = 0;
         if (lane == 0) t0 = atomicAdd(&ctr->tile_ctr[7], 4u);
@@ -688,18 +556,6 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
             }
             if (n > static_cast<uint32_t>(kWarpSortMax)) continue;  // a CTA sorted it
             const int ni = static_cast<int>(n);
-#ifdef AGSX_TS_RADIX
-            if (ni <= 32)
-                warp_sort_tile<1>(ekeys, vals, lo, ni, buf, hist);
-            else if (ni <= 64)
-                warp_sort_tile<2>(ekeys, vals, lo, ni, buf, hist);
-            else if (ni <= 128)
-                warp_sort_tile<4>(ekeys, vals, lo, ni, buf, hist);
-            else
-                warp_sort_tile<8>(ekeys, vals, lo, ni, buf, hist);
-#else
-            (void)buf;
-            (void)hist;
             if (ni <= 32)
                 warp_bitonic_tile<1>(ekeys, vals, lo, ni);
             else if (ni <= 64)
@@ -708,7 +564,6 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
                 warp_bitonic_tile<4>(ekeys, vals, lo, ni);
             else
                 warp_bitonic_tile<8>(ekeys, vals, lo, ni);
-#endif
         }
     }
 }

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of the sort paths on one box: parity subset, then bench lines per variant.
-#   VARIANTS="bucket depth match" bash scripts/ab_sort.sh
+#   VARIANTS="bucket depth" bash scripts/ab_sort.sh
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
@@ -19,10 +19,6 @@ PY
 for v in ${VARIANTS:-bucket depth}; do
   case $v in
     depth) AGSX_SORT=depth timeout 300 python bench.py --steps 20 --no-cpu --no-e2e --no-inflight > $OUT/b_$v.json 2> $OUT/b_$v.err ;;
-    match) make -s EXTRA_NVCC=-DAGSX_TS_MATCH -j16 > /dev/null 2>&1 || make EXTRA_NVCC=-DAGSX_TS_MATCH -B -j16 > /dev/null 2>&1
-           touch paper_2604_18980_b200/csrc/k_bucket.cu; make -s EXTRA_NVCC=-DAGSX_TS_MATCH -j16 > $OUT/make_match.log 2>&1
-           timeout 300 python bench.py --steps 20 --no-cpu --no-e2e --no-inflight > $OUT/b_$v.json 2> $OUT/b_$v.err
-           touch paper_2604_18980_b200/csrc/k_bucket.cu; make -s -j16 > /dev/null 2>&1 ;;
     bucket) AGSX_SORT=bucket timeout 300 python bench.py --steps 20 --no-cpu --no-e2e --no-inflight > $OUT/b_$v.json 2> $OUT/b_$v.err ;;
     *) timeout 300 python bench.py --steps 20 --no-cpu --no-e2e --no-inflight > $OUT/b_$v.json 2> $OUT/b_$v.err ;;
   esac
