@@ -996,3 +996,42 @@ def test_kept_frames_past_the_pinned_cap(tmp_path):
     out = subprocess.run([sys.executable, "-c", code, root], env=env, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert out.stdout.strip().startswith("ok")
+
+
+@pytest.mark.parametrize("mode", ["adagscale", "ellipse", "obb"])
+def test_bucketed_sort_path_matches_default(tmp_path, mode):
+    """The tile-bucketed pair-gen + sort (AGSX_SORT=bucket)
+    is selected per process: run it in a subprocess and compare its sorted
+    keys, Gaussian ids, ranges and image with the default depth-then-tile
+    path in this process (both bit-exact against the oracle elsewhere)."""
+    import subprocess
+    import sys
+
+    import paper_2604_18980_b200 as P
+
+    spec = dict(seed=9, count=20000, layout="veil", cameras=3, width=640, height=480, focal=500.0)
+    kw = dict(mode=mode, k=0.3 if mode == "adagscale" else 0.0, lut_bins=[0.6] * 20 if mode == "adagscale" else [])
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1])\n"
+        "import paper_2604_18980_b200 as P\n"
+        f"s = P.synth_scene(**{spec!r})\n"
+        "r = P.Renderer(0)\n"
+        f"out = r.render(s, 2, **{kw!r})\n"
+        "keys, gids = r.dump_sorted_pairs()\n"
+        "assert r.frame_stats()['bucketed_sort'] == 1\n"
+        "np.savez(sys.argv[2], keys=keys, gids=gids, ranges=r.dump_ranges(r.frame_stats()['tiles']),"
+        " image=out['image'])\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dst = str(tmp_path / "bucket.npz")
+    env = dict(os.environ, AGSX_SORT="bucket")
+    res = subprocess.run([sys.executable, "-c", code, root, dst], env=env, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = np.load(dst)
+    s = P.synth_scene(**spec)
+    r = P.Renderer(0)
+    out = r.render(s, 2, **kw)
+    keys, gids = r.dump_sorted_pairs()
+    assert r.frame_stats()["bucketed_sort"] == 0
+    assert np.array_equal(got["keys"], keys) and np.array_equal(got["gids"], gids)
+    assert np.array_equal(got["ranges"], r.dump_ranges(r.frame_stats()["tiles"]))
+    assert np.array_equal(got["image"].view(np.uint32), out["image"].view(np.uint32))
