@@ -6,6 +6,8 @@
 //              validate(cfg/cam) scene.cpp:41-59, 113-123
 #include "agsx_ctx.cuh"
 
+#include <cmath>
+
 extern "C" {
 
 int agsx_abi_version(void) { return AGSX_ABI_VERSION; }
@@ -23,6 +25,48 @@ void agsx_host_free(void* p) {
 }
 
 }  // extern "C"
+
+namespace agsx::host {
+// Host copy of a scene's slot -> id (orig) or id -> slot (inv) map; empty when
+// the scene keeps the caller's order.  For the dump and host-side paths.
+std::vector<uint32_t> scene_map_host(const Buf& b, uint64_t n) {
+    std::vector<uint32_t> v;
+    if (!b.p || n == 0) return v;
+    v.resize(n);
+    AGSX_CUDA(cudaMemcpy(v.data(), b.p, n * 4, cudaMemcpyDeviceToHost));
+    return v;
+}
+
+// A slot-ordered per-Gaussian array (status, max_t) copied to the host in
+// Gaussian-id order.
+void slots_to_ids_host(const agsx_scene* sc, const void* dev, uint32_t* host_out, cudaStream_t st) {
+    const uint64_t n = sc->n;
+    if (!n) return;
+    if (!sc->inv.p) {
+        AGSX_CUDA(cudaMemcpyAsync(host_out, dev, n * 4, cudaMemcpyDeviceToHost, st));
+        AGSX_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    std::vector<uint32_t> by_slot(n);
+    AGSX_CUDA(cudaMemcpyAsync(by_slot.data(), dev, n * 4, cudaMemcpyDeviceToHost, st));
+    AGSX_CUDA(cudaStreamSynchronize(st));
+    const std::vector<uint32_t> inv = scene_map_host(sc->inv, n);
+    for (uint64_t g = 0; g < n; ++g) host_out[g] = by_slot[inv[g]];
+}
+
+}  // namespace agsx::host
+
+namespace {
+// Scene storage order: AGSX_SCENE_ORDER=input keeps the caller's order
+// (A/B runs); the default is the 3D Morton order (DevScene).
+bool scene_order_morton() {
+    static const bool morton = [] {
+        const char* e = std::getenv("AGSX_SCENE_ORDER");
+        return !(e && std::strcmp(e, "input") == 0);
+    }();
+    return morton;
+}
+}  // namespace
 
 extern "C" {
 
@@ -141,8 +185,63 @@ int agsx_scene_upload(agsx_ctx* ctx, const agsx_scene_desc* d, agsx_scene** out)
                 ptr<float>(sc->sh_rest) + b * (3 * D - 3));
             check_launch(ctx);
         }
-        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         release(stage);
+        if (scene_order_morton() && n > 1) {
+            // storage order: 3D Morton order of the means (DevScene).  Spatial
+            // neighbours share K1's warps (similar footprints: less divergence in
+            // the tile test) and the bucketed scatter's tiles.
+            float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+            for (uint64_t i = 0; i < n; ++i)
+                for (int a = 0; a < 3; ++a) {
+                    const float v = d->mean[3 * i + a];
+                    if (v < lo[a]) lo[a] = v;  // NaN never compares: skipped
+                    if (v > hi[a]) hi[a] = v;
+                }
+            float3 l, sc3;
+            float* lp[3] = {&l.x, &l.y, &l.z};
+            float* sp[3] = {&sc3.x, &sc3.y, &sc3.z};
+            for (int a = 0; a < 3; ++a) {
+                const bool ok = std::isfinite(lo[a]) && std::isfinite(hi[a]) && hi[a] > lo[a];
+                *lp[a] = ok ? lo[a] : 0.0f;
+                *sp[a] = ok ? 1023.0f / (hi[a] - lo[a]) : 0.0f;
+            }
+            Buf codes, codes2, ord, ord2;
+            ensure(codes, n * 4);
+            ensure(codes2, n * 4);
+            ensure(ord, n * 4);
+            ensure(ord2, n * 4);
+            const int grid = static_cast<int>((n + 255) / 256);
+            k_morton_codes<<<grid, 256, 0, ctx->stream>>>(n, ptr<float4>(sc->pos_op), l, sc3, ptr<uint32_t>(codes));
+            check_launch(ctx);
+            // stable LSD sort of the 30-bit codes, values = Gaussian ids
+            uint32_t* ck[2] = {ptr<uint32_t>(codes), ptr<uint32_t>(codes2)};
+            uint32_t* cv[2] = {ptr<uint32_t>(ord), ptr<uint32_t>(ord2)};
+            for (int ps = 0; ps < 4; ++ps)
+                sort_pass<uint32_t>(ctx, ck[ps & 1], ps ? cv[ps & 1] : nullptr, ck[(ps + 1) & 1], cv[(ps + 1) & 1],
+                                    nullptr, n, 8 * ps, false, nullptr);
+            // after 4 passes the order is in cv[0]
+            Buf pos2, rot2, scale2, gb2, rest2;
+            ensure(pos2, n * 16);
+            ensure(rot2, n * 16);
+            ensure(scale2, n * 16);
+            ensure(gb2, n * 8);
+            ensure(rest2, std::max<uint64_t>(n * (3 * D - 3), 1) * 4);
+            ensure(sc->inv, n * 4);
+            k_permute_scene<<<grid, 256, 0, ctx->stream>>>(
+                n, D, cv[0], ptr<float4>(sc->pos_op), ptr<float4>(sc->rot), ptr<float4>(sc->scale_r),
+                ptr<float2>(sc->sh_gb), ptr<float>(sc->sh_rest), ptr<float4>(pos2), ptr<float4>(rot2),
+                ptr<float4>(scale2), ptr<float2>(gb2), ptr<float>(rest2), ptr<uint32_t>(sc->inv));
+            check_launch(ctx);
+            AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+            std::swap(sc->pos_op, pos2);
+            std::swap(sc->rot, rot2);
+            std::swap(sc->scale_r, scale2);
+            std::swap(sc->sh_gb, gb2);
+            std::swap(sc->sh_rest, rest2);
+            std::swap(sc->orig, ord);  // cv[0] is ord: the order after four passes
+            for (Buf* b : {&pos2, &rot2, &scale2, &gb2, &rest2, &codes, &codes2, &ord, &ord2}) release(*b);
+        }
+        AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         return AGSX_OK;
     });
     if (rc != AGSX_OK) {
@@ -156,7 +255,7 @@ int agsx_scene_upload(agsx_ctx* ctx, const agsx_scene_desc* d, agsx_scene** out)
 void agsx_scene_free(agsx_scene* sc) {
     if (!sc) return;
     cudaSetDevice(sc->device);
-    for (Buf* b : {&sc->pos_op, &sc->rot, &sc->scale_r, &sc->sh_gb, &sc->sh_rest}) release(*b);
+    for (Buf* b : {&sc->pos_op, &sc->rot, &sc->scale_r, &sc->sh_gb, &sc->sh_rest, &sc->orig, &sc->inv}) release(*b);
     delete sc;
 }
 
@@ -218,11 +317,9 @@ int agsx_render(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* cam,
                                       static_cast<size_t>(cam->width) * cam->height * 12,
                                       cudaMemcpyDeviceToHost, ctx->stream));
         }
-        if (maxt && scene->n) {
-            AGSX_CUDA(cudaMemcpyAsync(out->max_t, ctx->maxt.p, scene->n * 4, cudaMemcpyDeviceToHost,
-                                      ctx->stream));
-        }
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (maxt && scene->n)  // per Gaussian id (the device array is per storage slot)
+            slots_to_ids_host(scene, ctx->maxt.p, reinterpret_cast<uint32_t*>(out->max_t), ctx->stream);
         return AGSX_OK;
     });
 }
@@ -273,8 +370,7 @@ int agsx_render_contributions(agsx_ctx* ctx, const agsx_scene* scene, const agsx
         if (out && out->image && !ctx->f_image_on_host)
             AGSX_CUDA(cudaMemcpyAsync(out->image, ctx->image.p, static_cast<size_t>(cam->width) * cam->height * 12,
                                       cudaMemcpyDeviceToHost, ctx->stream));
-        if (maxt && n)
-            AGSX_CUDA(cudaMemcpyAsync(out->max_t, ctx->maxt.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        if (maxt && n) slots_to_ids_host(scene, ctx->maxt.p, reinterpret_cast<uint32_t*>(out->max_t), ctx->stream);
         // pass 1: events per tile; host scan -> per-tile offsets in tile order
         ensure(ctx->tmp1, std::max<uint64_t>(tiles, 1) * 4);
         ensure(ctx->tmp2, std::max<uint64_t>(tiles, 1) * 8);
@@ -305,13 +401,14 @@ int agsx_render_contributions(agsx_ctx* ctx, const agsx_scene* scene, const agsx
         ++ctx->launches;
         AGSX_CUDA(cudaMemcpyAsync(records, ctx->tmp3.p, total * sizeof(agsx_blend_record), cudaMemcpyDeviceToHost,
                                   ctx->stream));
-        std::vector<uint32_t> st(n);
-        if (n) AGSX_CUDA(cudaMemcpyAsync(st.data(), ctx->status.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+        std::vector<uint32_t> st(n);  // per Gaussian id
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
-        std::vector<uint32_t> view_index(n);
+        slots_to_ids_host(scene, ctx->status.p, st.data(), ctx->stream);
+        const std::vector<uint32_t> inv = scene_map_host(scene->inv, n);
+        std::vector<uint32_t> view_index(n);  // per storage slot (the records carry slots)
         uint32_t k = 0;
         for (uint64_t i = 0; i < n; ++i) {  // survivors in Gaussian order (preprocess.cpp:158-162)
-            view_index[i] = k;
+            view_index[inv.empty() ? i : inv[i]] = k;
             k += (st[i] & kAliveBit) ? 1u : 0u;
         }
         for (uint64_t i = 0; i < total; ++i) records[i].splat = view_index[records[i].splat];
@@ -381,7 +478,7 @@ int agsx_dump_tile_counts(agsx_ctx* ctx, uint32_t* counts, uint8_t* alive, uint6
         if (n != ctx->f_scene->n) return fail(ctx, AGSX_EINVAL, "count mismatch");
         std::vector<uint32_t> st(n);
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
-        if (n) AGSX_CUDA(cudaMemcpy(st.data(), ctx->status.p, n * 4, cudaMemcpyDeviceToHost));
+        slots_to_ids_host(ctx->f_scene, ctx->status.p, st.data(), ctx->stream);
         for (uint64_t i = 0; i < n; ++i) {
             if (counts) counts[i] = st[i] & kCountMask;
             if (alive) alive[i] = (st[i] & kAliveBit) ? 1 : 0;
@@ -410,12 +507,13 @@ int agsx_dump_sorted_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* gids, uint64
             if (T) AGSX_CUDA(cudaMemcpy(rg.data(), ctx->ranges.p, T * 8, cudaMemcpyDeviceToHost));
             if (c.m) AGSX_CUDA(cudaMemcpy(gd.data(), ctx->bk_gd.p, c.m * 8, cudaMemcpyDeviceToHost));
             if (P) AGSX_CUDA(cudaMemcpy(pv.data(), ctx->f_pvals, P * 4, cudaMemcpyDeviceToHost));
-            std::vector<uint32_t> depth_by_gid(n, 0);
-            for (const uint2& e : gd) depth_by_gid[e.x] = e.y;
+            const std::vector<uint32_t> orig = scene_map_host(ctx->f_scene->orig, n);
+            std::vector<uint32_t> depth_by_slot(n, 0);
+            for (const uint2& e : gd) depth_by_slot[e.x] = e.y;  // the list and the values carry storage slots
             for (uint64_t t = 0; t < T; ++t)
                 for (uint32_t i = rg[t].x; i < rg[t].y && i < P; ++i) {
-                    if (keys) keys[i] = (t << 32) | depth_by_gid[pv[i]];
-                    if (gids) gids[i] = pv[i];
+                    if (keys) keys[i] = (t << 32) | depth_by_slot[pv[i]];
+                    if (gids) gids[i] = orig.empty() ? pv[i] : orig[pv[i]];
                 }
             return AGSX_OK;
         }
@@ -429,11 +527,12 @@ int agsx_dump_sorted_pairs(agsx_ctx* ctx, uint64_t* keys, uint32_t* gids, uint64
             AGSX_CUDA(cudaMemcpy(tk.data(), ctx->f_tkeys, P * 4, cudaMemcpyDeviceToHost));
             AGSX_CUDA(cudaMemcpy(pv.data(), ctx->f_pvals, P * 4, cudaMemcpyDeviceToHost));
         }
-        std::vector<uint32_t> depth_by_gid(n, 0);
-        for (uint32_t j = 0; j < c.m; ++j) depth_by_gid[dv[j]] = dk[j];
+        const std::vector<uint32_t> orig = scene_map_host(ctx->f_scene->orig, n);
+        std::vector<uint32_t> depth_by_slot(n, 0);  // the depth order and pairs carry storage slots
+        for (uint32_t j = 0; j < c.m; ++j) depth_by_slot[dv[j]] = dk[j];
         for (uint64_t i = 0; i < P; ++i) {
-            if (keys) keys[i] = (static_cast<uint64_t>(tk[i]) << 32) | depth_by_gid[pv[i]];
-            if (gids) gids[i] = pv[i];
+            if (keys) keys[i] = (static_cast<uint64_t>(tk[i]) << 32) | depth_by_slot[pv[i]];
+            if (gids) gids[i] = orig.empty() ? pv[i] : orig[pv[i]];
         }
         return AGSX_OK;
     });

@@ -67,6 +67,7 @@ struct agsx_scene {
     uint64_t n = 0;
     int D = 1;
     Buf pos_op, rot, scale_r, sh_gb, sh_rest;
+    Buf orig, inv;  // storage order (DevScene); empty: slot = id
     DevScene view() const {
         DevScene s;
         s.n = n;
@@ -76,6 +77,8 @@ struct agsx_scene {
         s.scale_r = static_cast<const float4*>(scale_r.p);
         s.sh_gb = static_cast<const float2*>(sh_gb.p);
         s.sh_rest = static_cast<const float*>(sh_rest.p);
+        s.orig = static_cast<const uint32_t*>(orig.p);
+        s.inv = static_cast<const uint32_t*>(inv.p);
         return s;
     }
 };
@@ -89,7 +92,8 @@ struct agsx_ctx {
     int num_sms = 148;
     int occ_sort32 = 1, occ_sort64 = 1, occ_emit = 1, occ_emit_big = 1, occ_raster = 1, occ_tile_sort = 1;
     double pairs_per_splat = 0.0;  // previous frame's P / M (picks the emit stage)
-    uint64_t last_m = 0;           // previous frame's splats with tiles (sizes the scatter grid)
+    uint64_t last_m = 0;           // previous frame's splats with tiles
+    double prev_pairs_per_tile = 0.0;  // previous frame's P / T (picks the sort path, agsx_frame.cu)
     Buf sort_counts;  // grid x 256 chunk digit counts + 256 totals (one pass at a time)
 
     // device arenas (grow-only)
@@ -221,6 +225,8 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
                 uint8_t* host_u8 = nullptr);
 int finish_frame(agsx_ctx* ctx, agsx_frame* out);
 int refuse_if_host_frame(agsx_ctx* ctx, const char* what);
+void slots_to_ids_host(const agsx_scene* sc, const void* dev, uint32_t* host_out, cudaStream_t st);
+std::vector<uint32_t> scene_map_host(const Buf& b, uint64_t n);
 int quantize_to_host(agsx_ctx* ctx, uint8_t* image_u8);
 cudaError_t shared_copy_stream(int device, cudaStream_t* out);
 

@@ -148,15 +148,28 @@ uint32_t* tile_cnt_of(agsx_ctx* ctx) {
     return reinterpret_cast<uint32_t*>(static_cast<char*>(ctx->ctr.p) + tile_cnt_offset());
 }
 
-// Sort path of a frame: the depth-then-tile radix path (default), or the
-// tile-bucketed path of k_bucket.cu with AGSX_SORT=bucket (bit-identical
-// output; measured slower at config 3).
-bool use_bucket() {
-    static const bool bucket = [] {
+// Sort path of a frame, both bit-identical: the
+// depth-then-tile radix path (default) or the tile-bucketed path of
+// k_bucket.cu (AGSX_SORT=bucket).  AGSX_SORT=auto picks per frame: the
+// bucketed path when the context's previous frame averaged fewer than
+// kBucketMaxPairsPerTile pairs per tile, else the depth path (measured not
+// faster at config 3 either way, so not the default).
+constexpr double kBucketMaxPairsPerTile = 160.0;
+int sort_mode() {  // 0 depth, 1 bucket, 2 auto
+    static const int mode = [] {
         const char* e = std::getenv("AGSX_SORT");
-        return e && std::strcmp(e, "bucket") == 0;
+        if (e && std::strcmp(e, "bucket") == 0) return 1;
+        if (e && std::strcmp(e, "auto") == 0) return 2;
+        return 0;
     }();
-    return bucket;
+    return mode;
+}
+bool may_bucket() { return sort_mode() != 0; }
+bool may_depth() { return sort_mode() != 1; }
+bool frame_uses_bucket(const agsx_ctx* ctx) {
+    const int m = sort_mode();
+    if (m != 2) return m == 1;
+    return ctx->prev_pairs_per_tile > 0.0 && ctx->prev_pairs_per_tile < kBucketMaxPairsPerTile;
 }
 // 256-splat chunks of the depth order (K3 work units)
 uint64_t chunk_slots(uint64_t n) { return std::max<uint64_t>((n + 255) / 256, 1); }
@@ -187,7 +200,7 @@ void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pi
     ensure(ctx->ranges, std::max<uint64_t>(tiles, 1) * 8);
     ensure(ctx->image, std::max<uint64_t>(pixels, 1) * 12);
     ensure(ctx->ctr, tile_cnt_offset() + std::max<uint64_t>(tiles, 1) * 4 * kTileSlices + 16);
-    if (use_bucket()) {
+    if (may_bucket()) {
         ensure(ctx->bk_hits, std::max<uint64_t>(n, 1) * 16);
         ensure(ctx->bk_gd, std::max<uint64_t>(n, 1) * 8);
         ensure(ctx->big_list, std::max<uint64_t>(tiles, 1) * 4);
@@ -199,11 +212,11 @@ void ensure_frame_buffers(agsx_ctx* ctx, uint64_t n, uint64_t tiles, uint64_t pi
     }
     const uint64_t cap = ctx->pair_capacity;
     ensure(ctx->pvals, cap * 4);
-    if (use_bucket()) {
+    if (may_bucket()) {
         ensure(ctx->ekeys, cap * 8);
         ensure(ctx->ekeys2, cap * 8);
     }
-    if (!use_bucket()) {
+    if (may_depth()) {
         ensure(ctx->tkeys, cap * 4);
         ensure(ctx->tkeys2, cap * 4);
         ensure(ctx->pvals2, cap * 4);
@@ -300,7 +313,8 @@ void launch_quantize(agsx_ctx* ctx, const float* src, uint8_t* dst, uint64_t n, 
 }
 
 void enqueue_bucket_sort(agsx_ctx* ctx, uint64_t n, const FrameParams& p, const BucketOut& bk);
-void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FrameParams& p, const SplatPlanes& pl);
+void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FrameParams& p, const SplatPlanes& pl,
+                        const uint32_t* scene_inv);
 void enqueue_raster(agsx_ctx* ctx, const FrameParams& p, bool maxt, uint32_t* vals);
 
 void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bool maxt,
@@ -312,7 +326,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
     ctx->ev = ctx->ev_ring[ctx->frames % agsx_ctx::kRing];
     ++ctx->frames;
 
-    const bool bucket = use_bucket();
+    const bool bucket = frame_uses_bucket(ctx);
     AGSX_CUDA(cudaEventRecord(ctx->ev[0], st));
     AGSX_CUDA(cudaMemsetAsync(ctr, 0, bucket ? tile_cnt_offset() + tiles * 4 * kTileSlices : counters_bytes(), st));
     // the other frame-scoped buffers (ranges, chunk sums, per-tile P_it words)
@@ -330,6 +344,8 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         bk.tile_cnt = tile_cnt_of(ctx);
         bk.hits = ptr<uint4>(ctx->bk_hits);
         bk.gd = ptr<uint2>(ctx->bk_gd);
+        bk.orig = sc->view().orig;
+        bk.inv = sc->view().inv;
     }
     if (n == 0) {  // no K1: the raster still reads the (empty) ranges
         AGSX_CUDA(cudaMemsetAsync(ctx->ranges.p, 0, tiles * 8, st));
@@ -352,7 +368,7 @@ void enqueue_frame(agsx_ctx* ctx, const agsx_scene* sc, const FrameParams& p, bo
         if (bucket) {
             enqueue_bucket_sort(ctx, n, p, bk);
         } else {
-            enqueue_depth_sort(ctx, n, tiles, p, pl);
+            enqueue_depth_sort(ctx, n, tiles, p, pl, sc->view().inv);
         }
     }
     uint32_t* vals = ptr<uint32_t>(ctx->pvals);
@@ -383,7 +399,7 @@ void enqueue_bucket_sort(agsx_ctx* ctx, uint64_t n, const FrameParams& p, const 
     AGSX_CUDA(cudaEventRecord(ctx->ev[3], st));
     launch_pdl(k_tile_sort, dim3(ctx->num_sms * ctx->occ_tile_sort), dim3(256), 0, st, ptr<uint2>(ctx->ranges), T,
                ptr<uint64_t>(ctx->ekeys), ptr<uint64_t>(ctx->ekeys2), ptr<uint32_t>(ctx->pvals), ctr,
-               static_cast<const uint32_t*>(ptr<uint32_t>(ctx->big_list)));
+               static_cast<const uint32_t*>(ptr<uint32_t>(ctx->big_list)), bk.orig, bk.inv);
     check_launch(ctx);
     AGSX_CUDA(cudaEventRecord(ctx->ev[4], st));
     ctx->f_tkeys = nullptr;
@@ -392,7 +408,8 @@ void enqueue_bucket_sort(agsx_ctx* ctx, uint64_t n, const FrameParams& p, const 
 
 // Depth-then-tile radix path: K4a depth sort of the splats, K3 emission in
 // depth order, K4b stable tile sort, K5 ranges.
-void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FrameParams& p, const SplatPlanes& pl) {
+void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FrameParams& p, const SplatPlanes& pl,
+                        const uint32_t* scene_inv) {
     cudaStream_t st = ctx->stream;
     Counters* ctr = ptr<Counters>(ctx->ctr);
     // K4a: stable sort by depth bits (4 x 8-bit, histograms in one read);
@@ -410,7 +427,15 @@ void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FramePa
         SortBias sb;
         sb.kmin_c = &ctr->kmin_c;
         sb.kmax = &ctr->kmax;
-        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m, {}, sb);
+        // The pass runs in Gaussian-id order (equal depths keep id order)
+        // and carries the storage slots on as values (DevScene)
+#ifdef AGSX_PASS0_GATHER
+        SortBias s0 = sb;  // K1 wrote the keys in slot order: read them through inv
+        s0.gather = scene_inv;
+        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m, {}, s0);
+#else
+        sort_pass<uint32_t>(ctx, dk[0], scene_inv, dk[1], dv[1], nullptr, n, 0, true, &ctr->m, {}, sb);
+#endif
         for (int ps = 1; ps < 4; ++ps) {
             SortCountOut co;
             SortBias sp = sb;
@@ -700,6 +725,8 @@ int finish_frame(agsx_ctx* ctx, agsx_frame* out) {
         }
         ctx->pending = false;
         ctx->last_m = c.m;
+        ctx->prev_pairs_per_tile = static_cast<double>(c.p) /
+                                   std::max(1.0, static_cast<double>(ctx->f_params.tiles_x) * ctx->f_params.tiles_y);
         ctx->pairs_per_splat = c.m ? static_cast<double>(c.p) / c.m : 0.0;
         if (out) {
             out->pair_count = c.p;

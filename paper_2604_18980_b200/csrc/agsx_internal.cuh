@@ -44,6 +44,12 @@ struct FrameParams {
 };
 
 // Device-resident scene (uploaded once; 56 B per Gaussian for SH degree 0).
+// The scene is stored in a spatial (3D Morton) order chosen at upload: slot
+// s holds the Gaussian with id orig[s] (the caller's index, which orders
+// equal depths, preprocess.cpp:158-162) and inv[g] is the slot of Gaussian
+// g.  Every per-splat frame array (status, depth keys, planes) is indexed by
+// slot; ids are translated where the reference's order or an output needs
+// them.  orig = inv = nullptr: slot = id.
 struct DevScene {
     uint64_t n;
     int sh_coeffs;  // D per channel
@@ -52,6 +58,10 @@ struct DevScene {
     const float4* scale_r;  // scale.xyz, sh[0] (red DC)
     const float2* sh_gb;    // sh[1], sh[2] (green/blue DC)
     const float* sh_rest;   // (D-1)*3 floats per Gaussian, coefficient-major
+    const uint32_t* orig;   // slot -> Gaussian id
+    const uint32_t* inv;    // Gaussian id -> slot
+    __host__ __device__ __forceinline__ uint32_t id_of(uint32_t slot) const { return orig ? orig[slot] : slot; }
+    __host__ __device__ __forceinline__ uint32_t slot_of(uint32_t id) const { return inv ? inv[id] : id; }
 };
 
 // Per-splat planes written by preprocess for splats that hit >= 1 tile,

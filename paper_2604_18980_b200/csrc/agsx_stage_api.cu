@@ -61,12 +61,12 @@ int agsx_preprocess_view(agsx_ctx* ctx, const agsx_scene* scene, const agsx_came
                 ptr<agsx_splat_view>(ctx->dump), FrameZero{}, BucketOut{});
             check_launch(ctx);
         }
-        std::vector<uint32_t> st(n);
+        std::vector<uint32_t> st(n);  // per Gaussian id (the device array is per storage slot)
         std::vector<agsx_splat_view> sv(n);
         if (n) {
-            AGSX_CUDA(cudaMemcpyAsync(st.data(), ctx->status.p, n * 4, cudaMemcpyDeviceToHost, ctx->stream));
             AGSX_CUDA(cudaMemcpyAsync(sv.data(), ctx->dump.p, n * sizeof(agsx_splat_view),
                                       cudaMemcpyDeviceToHost, ctx->stream));
+            slots_to_ids_host(scene, ctx->status.p, st.data(), ctx->stream);
         }
         AGSX_CUDA(cudaStreamSynchronize(ctx->stream));
         uint64_t m = 0;
@@ -287,8 +287,9 @@ int agsx_fold_max_t(agsx_ctx* ctx, const agsx_scene* scene, const agsx_camera* c
             const bool wide = depth_keys_wide_host(*ctx->h_ctr);  // finish_frame synchronised
             const uint32_t* gid = ctx->f_bucket ? ptr<uint32_t>(ctx->bk_gd) : ptr<uint32_t>(wide ? ctx->dvals : ctx->dvals2);
             const uint32_t* dep = ctx->f_bucket ? gid + 1 : ptr<uint32_t>(wide ? ctx->dkeys : ctx->dkeys2);
+            // max_t is per storage slot, as are the depth order and the bucketed list
             k_fold_max_t<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(
-                gid, dep, ctx->f_bucket ? 2 : 1, &ptr<Counters>(ctx->ctr)->m,
+                gid, nullptr, dep, ctx->f_bucket ? 2 : 1, &ptr<Counters>(ctx->ctr)->m,
                 ptr<uint32_t>(ctx->maxt), lut_shape->depth_min, lut_shape->depth_max, nb, dfold, dfold + nb);
             check_launch(ctx);
         }

@@ -43,6 +43,19 @@ namespace agsx {
 
 namespace {
 
+// Keys of the bucketed path are (depth bits << 32 | storage slot) (DevScene):
+// the slot is the rasterizer's value.  The reference orders equal depths by
+// Gaussian id, so a tile with equal depths (a few hundred tiles per frame),
+// and every tile of the CTA path, is sorted on (depth, id) keys instead:
+// id_key() swaps the low word to the id, slot_of_key() swaps it back.
+__device__ __forceinline__ uint64_t id_key(uint64_t k, const uint32_t* __restrict__ orig) {
+    return orig ? (k & 0xffffffff00000000ull) | orig[static_cast<uint32_t>(k)] : k;
+}
+__device__ __forceinline__ uint32_t slot_of_key(uint64_t k, const uint32_t* __restrict__ inv) {
+    const uint32_t id = static_cast<uint32_t>(k);
+    return inv ? inv[id] : id;
+}
+
 constexpr int kTSThreads = 256;
 constexpr int kTSWarps = kTSThreads / 32;
 constexpr int kTSChunks = kWarpSortMax / 32;  // 8 register chunks of 32 keys per lane
@@ -133,16 +146,9 @@ __device__ __forceinline__ int tie_position(const uint64_t* buf, int n, int i, u
 // exchanges and the others one shuffle per element; padding keys are
 // ~0ull and sort last.  Writes the Gaussian ids in order.
 template <int E>
-__device__ __forceinline__ void warp_bitonic_tile(const uint64_t* __restrict__ ekeys, uint32_t* __restrict__ vals,
-                                                  uint32_t off, int n) {
+__device__ __forceinline__ void warp_bitonic(uint64_t (&v)[E]) {
     const int lane = threadIdx.x & 31;
     constexpr int N = 32 * E;
-    uint64_t v[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int i = lane * E + e;
-        v[e] = i < n ? ekeys[off + i] : ~0ull;
-    }
 #pragma unroll
     for (int k = 2; k <= N; k <<= 1) {
 #pragma unroll
@@ -173,10 +179,49 @@ __device__ __forceinline__ void warp_bitonic_tile(const uint64_t* __restrict__ e
             }
         }
     }
+}
+
+// Adjacent equal depths among the first n sorted keys (lane-contiguous).
+template <int E>
+__device__ __forceinline__ bool warp_sorted_has_tie(const uint64_t (&v)[E], int n) {
+    const int lane = threadIdx.x & 31;
+    bool tie = false;
+#pragma unroll
+    for (int e = 0; e + 1 < E; ++e)
+        tie |= lane * E + e + 1 < n && (v[e] >> 32) == (v[e + 1] >> 32);
+    const uint64_t next = __shfl_down_sync(0xffffffffu, v[0], 1);  // the next lane's first key
+    tie |= lane < 31 && lane * E + E < n && (v[E - 1] >> 32) == (next >> 32);
+    return __any_sync(0xffffffffu, tie);
+}
+
+template <int E>
+__device__ __forceinline__ void warp_bitonic_tile(const uint64_t* __restrict__ ekeys, uint32_t* __restrict__ vals,
+                                                  uint32_t off, int n, const uint32_t* __restrict__ orig,
+                                                  const uint32_t* __restrict__ inv) {
+    const int lane = threadIdx.x & 31;
+    uint64_t v[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         const int i = lane * E + e;
-        if (i < n) vals[off + i] = static_cast<uint32_t>(v[e]);
+        v[e] = i < n ? ekeys[off + i] : ~0ull;
+    }
+    warp_bitonic<E>(v);
+    if (orig && warp_sorted_has_tie<E>(v, n)) {  // equal depths: order them by Gaussian id
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            if (lane * E + e < n) v[e] = id_key(v[e], orig);
+        warp_bitonic<E>(v);
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const int i = lane * E + e;
+            if (i < n) vals[off + i] = slot_of_key(v[e], inv);
+        }
+        return;
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        if (i < n) vals[off + i] = static_cast<uint32_t>(v[e]);  // the slot
     }
 }
 
@@ -187,13 +232,16 @@ __device__ __forceinline__ void warp_bitonic_tile(const uint64_t* __restrict__ e
 // whole tile per pass.
 __device__ __noinline__ void cta_sort_tile(uint64_t* __restrict__ src, uint64_t* __restrict__ alt,
                                            uint32_t* __restrict__ vals, uint32_t n, uint64_t* sbuf,
-                                           uint32_t (*hist)[256], uint32_t* s_base, uint32_t* s_red) {
+                                           uint32_t (*hist)[256], uint32_t* s_base, uint32_t* s_red,
+                                           const uint32_t* __restrict__ orig, const uint32_t* __restrict__ inv) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool inreg = n <= static_cast<uint32_t>(kCtaSortMax);
-    // depth range and largest gid of the tile
+    // depth range and largest gid of the tile; the keys become (depth, id)
+    // keys (id_key) so the radix passes and the tie fix-up see Gaussian ids
     uint32_t dmin = 0xffffffffu, dmax = 0u, gmax = 0u;
     for (uint32_t i = tid; i < n; i += kTSThreads) {
-        const uint64_t k = src[i];
+        const uint64_t k = id_key(src[i], orig);
+        if (orig) src[i] = k;
         dmin = min(dmin, static_cast<uint32_t>(k >> 32));
         dmax = max(dmax, static_cast<uint32_t>(k >> 32));
         gmax = max(gmax, static_cast<uint32_t>(k));
@@ -356,10 +404,10 @@ __device__ __noinline__ void cta_sort_tile(uint64_t* __restrict__ src, uint64_t*
 #pragma unroll
         for (int c = 0; c < kTSChunks; ++c) {
             const uint32_t i = seg + c * 32 + lane;
-            if (i < n) vals[pos[c]] = static_cast<uint32_t>(k[c]);
+            if (i < n) vals[pos[c]] = slot_of_key(k[c], inv);
         }
     } else {
-        for (uint32_t i = tid; i < n; i += kTSThreads) vals[i] = static_cast<uint32_t>(cur[i]);
+        for (uint32_t i = tid; i < n; i += kTSThreads) vals[i] = slot_of_key(cur[i], inv);
     }
     __syncthreads();
 }
@@ -486,19 +534,20 @@ k_bucket_scatter(FrameParams p, SplatPlanes pl, BucketOut bk, const Counters* ct
             continue;
         }
         TileTest t{};  // span over 64 tiles: re-run the test
-        const float4 a = pl.p0[e.x];
+        const uint32_t es = e.x;  // the list carries storage slots
+        const float4 a = pl.p0[es];
         t.mode = p.mode;
         t.cx = a.x;
         t.cy = a.y;
         t.ixx = a.z;
         t.ixy = 0.5f * a.w;
-        t.iyy = pl.p1[e.x].x;
+        t.iyy = pl.p1[es].x;
         t.rx = __uint_as_float(r.x);
         t.ry = __uint_as_float(r.y);
         t.r2 = __uint_as_float(r.z);
         t.v1x = t.v1y = t.a = t.b = 0.0f;
         if (p.mode == AGSX_MODE_OBB) {
-            const float4 o = pl.p4[e.x];
+            const float4 o = pl.p4[es];
             t.v1x = o.x;
             t.v1y = o.y;
             t.a = o.z;
@@ -514,7 +563,8 @@ k_bucket_scatter(FrameParams p, SplatPlanes pl, BucketOut bk, const Counters* ct
 // ---- K4: per-tile sort -------------------------------------------------------
 __global__ void __launch_bounds__(kTSThreads, 3)
 k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys, uint64_t* __restrict__ ekeys2,
-            uint32_t* __restrict__ vals, Counters* ctr, const uint32_t* __restrict__ big_list) {
+            uint32_t* __restrict__ vals, Counters* ctr, const uint32_t* __restrict__ big_list,
+            const uint32_t* __restrict__ orig, const uint32_t* __restrict__ inv) {
     griddep_wait();
     __shared__ __align__(16) uint64_t s_keys[kTSWarps * kWarpSortMax];  // 32 KB
     __shared__ __align__(16) uint32_t s_hist[kTSWarps][256];            // 8 KB
@@ -536,7 +586,7 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
         __syncthreads();
         if (b >= n_big) break;
         const uint2 r = ranges[big_list[b]];
-        cta_sort_tile(ekeys + r.x, ekeys2 + r.x, vals + r.x, r.y - r.x, s_keys, s_hist, s_base, s_red);
+        cta_sort_tile(ekeys + r.x, ekeys2 + r.x, vals + r.x, r.y - r.x, s_keys, s_hist, s_base, s_red, orig, inv);
     }
     // then one warp per tile, tiles claimed four at a time
     while (true) {
@@ -551,19 +601,19 @@ k_tile_sort(uint2* __restrict__ ranges, uint32_t T, uint64_t* __restrict__ ekeys
             const uint32_t hi = __shfl_sync(0xffffffffu, rr.y, q);
             const uint32_t n = hi - lo;
             if (n <= 1u) {
-                if (n == 1u && lane == 0) vals[lo] = static_cast<uint32_t>(ekeys[lo]);
+                if (n == 1u && lane == 0) vals[lo] = static_cast<uint32_t>(ekeys[lo]);  // the slot
                 continue;
             }
             if (n > static_cast<uint32_t>(kWarpSortMax)) continue;  // a CTA sorted it
             const int ni = static_cast<int>(n);
             if (ni <= 32)
-                warp_bitonic_tile<1>(ekeys, vals, lo, ni);
+                warp_bitonic_tile<1>(ekeys, vals, lo, ni, orig, inv);
             else if (ni <= 64)
-                warp_bitonic_tile<2>(ekeys, vals, lo, ni);
+                warp_bitonic_tile<2>(ekeys, vals, lo, ni, orig, inv);
             else if (ni <= 128)
-                warp_bitonic_tile<4>(ekeys, vals, lo, ni);
+                warp_bitonic_tile<4>(ekeys, vals, lo, ni, orig, inv);
             else
-                warp_bitonic_tile<8>(ekeys, vals, lo, ni);
+                warp_bitonic_tile<8>(ekeys, vals, lo, ni, orig, inv);
         }
     }
 }

@@ -13,13 +13,15 @@ namespace agsx {
 // the unsigned maximum of the bit patterns.
 // (stride: 1 for the depth-sort arrays, 2 for the bucketed path's {gid,
 // depth} list.)
-__global__ void k_fold_max_t(const uint32_t* __restrict__ order, const uint32_t* __restrict__ dkeys, int stride,
+__global__ void k_fold_max_t(const uint32_t* __restrict__ order, const uint32_t* __restrict__ inv,
+                             const uint32_t* __restrict__ dkeys, int stride,
                              const uint32_t* m_dev, const uint32_t* __restrict__ maxt, float dmin, float dmax,
                              int nbins, uint32_t* __restrict__ folded, uint32_t* __restrict__ observed) {
     const uint32_t m = *m_dev;
     const float w = (dmax - dmin) / static_cast<float>(nbins);
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
-        const uint32_t mt = maxt[order[static_cast<uint64_t>(j) * stride]];
+        const uint32_t o = order[static_cast<uint64_t>(j) * stride];
+        const uint32_t mt = maxt[inv ? inv[o] : o];
         if (mt == 0u) continue;  // never blended (max_t <= 0)
         int b = f2i_x86((__uint_as_float(dkeys[static_cast<uint64_t>(j) * stride]) - dmin) / w);
         if (b < 0) b = 0;

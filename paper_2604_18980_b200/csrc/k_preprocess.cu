@@ -240,7 +240,11 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         if (ok && th >= opacity) ok = false;
         if (!ok) {
             status[i] = 0u;
+#ifdef AGSX_PASS0_GATHER
             if (!bk.tile_cnt) dkeys[i] = 0xffffffffu;
+#else
+            if (!bk.tile_cnt) dkeys[sc.id_of(static_cast<uint32_t>(i))] = 0xffffffffu;  // keys in id order
+#endif
         }
     }
     // queue the survivors (converged warp: one shared-memory atomic per warp)
@@ -275,7 +279,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
     bool keep = false;
     float depth = 0.0f;
     uint4 hit_rec = make_uint4(0u, 0u, 0u, 0u);
-    uint32_t gi = 0;
+    uint32_t gi = 0;  // storage slot of the survivor (DevScene); sc.id_of(gi) is its Gaussian id
     if (alive) {
         gi = s_gid[slot];
         const float m2x = s_q[0][slot], m2y = s_q[1][slot];
@@ -344,8 +348,8 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
             v.rgb[2] = rgb[2];
             v.opacity = opacity;
             v.th = th;
-            v.source_id = gi;
-            dump[gi] = v;
+            v.source_id = sc.id_of(gi);  // dumps are in Gaussian-id order
+            dump[v.source_id] = v;
         }
         status[gi] = cnt | kAliveBit;
     }
@@ -359,12 +363,18 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         base = __shfl_sync(0xffffffffu, base, 0);
         if (keep) {
             const uint32_t at = base + __popc(kb & ((1u << lane) - 1u));
-            bk.gd[at] = make_uint2(gi, __float_as_uint(depth));
+            bk.gd[at] = make_uint2(gi, __float_as_uint(depth));  // storage slot (the tile sort orders ties by id)
             bk.hits[at] = hit_rec;
         }
         return;
     }
+#ifdef AGSX_PASS0_GATHER
     if (alive) dkeys[gi] = keep ? __float_as_uint(depth) : 0xffffffffu;
+#else
+    // the depth keys in Gaussian-id order: the first depth pass reads them
+    // in order (equal depths keep id order) with the storage slots as values
+    if (alive) dkeys[sc.id_of(gi)] = keep ? __float_as_uint(depth) : 0xffffffffu;
+#endif
     // range of the depth keys (positive floats: bit order = value order), so
     // the depth sort can skip its top digit when the keys span < 2^24.  Per
     // warp, and an atomic only when it improves on the value last seen (the
@@ -386,12 +396,13 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
 // project (preprocess.cpp:26-66): valid[i] and {mean2d.x, mean2d.y, cov2d.xx,
 // cov2d.xy, cov2d.yy, depth} per Gaussian.
 __global__ void k_project(FrameParams p, DevScene sc, uint8_t* __restrict__ valid, float* __restrict__ out) {
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // Gaussian id
     if (i >= sc.n) return;
-    const float4 po = sc.pos_op[i];
+    const uint32_t si = sc.slot_of(static_cast<uint32_t>(i));
+    const float4 po = sc.pos_op[si];
     const float dx = po.x - p.cam_pos[0], dy = po.y - p.cam_pos[1], dz = po.z - p.cam_pos[2];
     float tz = 0.0f, m2x = 0.0f, m2y = 0.0f, cxx = 0.0f, cxy = 0.0f, cyy = 0.0f;
-    const bool ok = project_dev(p, dx, dy, dz, sc.rot[i], sc.scale_r[i], tz, m2x, m2y, cxx, cxy, cyy);
+    const bool ok = project_dev(p, dx, dy, dz, sc.rot[si], sc.scale_r[si], tz, m2x, m2y, cxx, cxy, cyy);
     valid[i] = ok ? 1u : 0u;
     float* o = out + 6 * i;
     o[0] = m2x;
@@ -404,10 +415,11 @@ __global__ void k_project(FrameParams p, DevScene sc, uint8_t* __restrict__ vali
 
 // eval_color (preprocess.cpp:68-105) for a caller-given unit view direction.
 __global__ void k_eval_color(DevScene sc, const float* __restrict__ dirs, float* __restrict__ rgb) {
-    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // Gaussian id
     if (i >= sc.n) return;
-    const float2 gb = sc.sh_gb[i];
-    eval_color(sc, i, sc.scale_r[i].w, gb.x, gb.y, dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2], rgb + 3 * i);
+    const uint32_t si = sc.slot_of(static_cast<uint32_t>(i));
+    const float2 gb = sc.sh_gb[si];
+    eval_color(sc, si, sc.scale_r[si].w, gb.x, gb.y, dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2], rgb + 3 * i);
 }
 
 // compute_th (preprocess.cpp:107-116) with the frame's LUT, k and tau;
@@ -419,6 +431,47 @@ __global__ void k_compute_th(FrameParams p, const float* __restrict__ cov, const
     const float xx = cov[3 * i], xy = cov[3 * i + 1], yy = cov[3 * i + 2];
     const float det = xx * yy - xy * xy;  // SymMat2::det (math.hpp:83)
     th[i] = det > 0.0f ? compute_th_dev(lut_value(p, depth[i]), det, p.k, p.tau) : __int_as_float(0x7fc00000);
+}
+
+// 30-bit Morton code of each mean quantised to 1024 cells per axis.
+__device__ __forceinline__ uint32_t morton_spread10(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void k_morton_codes(uint64_t n, const float4* __restrict__ pos_op, float3 lo, float3 scale,
+                               uint32_t* __restrict__ codes) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 p = pos_op[i];
+    auto q = [](float v, float l, float s) {
+        const float t = (v - l) * s;  // NaN / inf means land in cell 0 / 1023
+        return static_cast<uint32_t>(t > 0.0f ? (t < 1023.0f ? t : 1023.0f) : 0.0f);
+    };
+    codes[i] = morton_spread10(q(p.x, lo.x, scale.x)) | (morton_spread10(q(p.y, lo.y, scale.y)) << 1) |
+               (morton_spread10(q(p.z, lo.z, scale.z)) << 2);
+}
+
+// Slot s <- Gaussian order[s]; inv[order[s]] = s.
+__global__ void k_permute_scene(uint64_t n, int D, const uint32_t* __restrict__ order,
+                                const float4* __restrict__ pos_op, const float4* __restrict__ rot,
+                                const float4* __restrict__ scale_r, const float2* __restrict__ sh_gb,
+                                const float* __restrict__ sh_rest, float4* pos_op2, float4* rot2, float4* scale_r2,
+                                float2* sh_gb2, float* sh_rest2, uint32_t* inv) {
+    const uint64_t s = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t g = order[s];
+    pos_op2[s] = pos_op[g];
+    rot2[s] = rot[g];
+    scale_r2[s] = scale_r[g];
+    sh_gb2[s] = sh_gb[g];
+    const int r = 3 * D - 3;
+    for (int k = 0; k < r; ++k) sh_rest2[s * r + k] = sh_rest[static_cast<uint64_t>(g) * r + k];
+    inv[g] = static_cast<uint32_t>(s);
 }
 
 // Scene upload: host SoA (agsx_scene_desc) -> device planes.

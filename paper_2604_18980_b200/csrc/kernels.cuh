@@ -48,7 +48,9 @@ struct FrameZero {
 struct BucketOut {
     uint32_t* tile_cnt = nullptr;  // tiles x kTileSlices pair counts (slice = gid % kTileSlices); zeroed before K1
     uint4* hits = nullptr;         // P3 hit record per listed splat
-    uint2* gd = nullptr;           // {gid, depth bits} per listed splat
+    uint2* gd = nullptr;           // {storage slot, depth bits} per listed splat (DevScene)
+    const uint32_t* orig = nullptr;  // storage slot -> Gaussian id, nullptr: identity
+    const uint32_t* inv = nullptr;   // Gaussian id -> storage slot
 };
 __global__ void k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* status,
                              uint32_t* dkeys, Counters* ctr, agsx_splat_view* dump, FrameZero fz, BucketOut bk);
@@ -72,7 +74,13 @@ __global__ void k_bucket_scatter(FrameParams p, SplatPlanes pl, BucketOut bk, co
 // the reference's stable (tile, depth, emission order) order -- and the
 // Gaussian ids of the sorted segment into vals.
 __global__ void k_tile_sort(uint2* ranges, uint32_t T, uint64_t* ekeys, uint64_t* ekeys2, uint32_t* vals,
-                            Counters* ctr, const uint32_t* big_list);
+                            Counters* ctr, const uint32_t* big_list, const uint32_t* orig, const uint32_t* inv);
+// Scene storage order (agsx_scene_upload): 30-bit 3D Morton codes of the
+// means over their bounding box, then the SoA gathered into code order.
+__global__ void k_morton_codes(uint64_t n, const float4* pos_op, float3 lo, float3 scale, uint32_t* codes);
+__global__ void k_permute_scene(uint64_t n, int D, const uint32_t* order, const float4* pos_op, const float4* rot,
+                                const float4* scale_r, const float2* sh_gb, const float* sh_rest, float4* pos_op2,
+                                float4* rot2, float4* scale_r2, float2* sh_gb2, float* sh_rest2, uint32_t* inv);
 __global__ void k_pack_scene(uint64_t n, int D, const float* mean, const float* scale,
                              const float* rot, const float* op, const float* sh, float4* pos_op,
                              float4* rotq, float4* scale_r, float2* sh_gb, float* sh_rest);
@@ -122,6 +130,10 @@ struct SortBias {
     const uint32_t* kmax = nullptr;
     int only_wide = 0;
     int co_if_narrow = 0;
+    // Gathered input (the first depth pass over a scene in storage order,
+    // DevScene): position i of the pass reads key kin[gather[i]] and, with no
+    // value array, value gather[i] -- the pass runs in Gaussian-id order.
+    const uint32_t* gather = nullptr;
 };
 template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
@@ -154,7 +166,7 @@ cudaError_t launch_raster_records(cudaStream_t st, const FrameParams& p, const u
                                   const float4* P0, const float4* P1, const float4* P2, float* image,
                                   uint32_t* counts, const uint64_t* offsets, agsx_blend_record* out);
 
-__global__ void k_fold_max_t(const uint32_t* order, const uint32_t* dkeys, int stride, const uint32_t* m_dev,
+__global__ void k_fold_max_t(const uint32_t* order, const uint32_t* inv, const uint32_t* dkeys, int stride, const uint32_t* m_dev,
                              const uint32_t* maxt, float dmin, float dmax, int nbins, uint32_t* folded,
                              uint32_t* observed);
 __global__ void k_sq_err_partial(const float* a, const float* b, uint64_t n, double* partial);
