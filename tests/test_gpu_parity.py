@@ -1001,8 +1001,9 @@ def test_kept_frames_past_the_pinned_cap(tmp_path):
 @pytest.mark.parametrize("mode", ["adagscale", "ellipse", "obb"])
 def test_sort_paths_agree(tmp_path, mode):
     """The two sort paths (DESIGN.md §4.2 depth-then-tile, §4.2b tile-bucketed)
-    give identical keys, Gaussian ids and images: this process renders with
-    the default path, subprocesses with AGSX_SORT=depth|bucket (process-wide
+    and the two scene storage orders (§3: 3D Morton, the caller's) give
+    identical keys, Gaussian ids and images: this process renders with the
+    defaults, subprocesses with AGSX_SORT / AGSX_SCENE_ORDER (process-wide
     switches)."""
     import subprocess
     import sys
@@ -1029,9 +1030,10 @@ def test_sort_paths_agree(tmp_path, mode):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     if os.environ.get("AGSX_SORT") == "bucket":  # this process already runs the bucketed path
         return
-    for forced, flag in (("depth", 0), ("bucket", 1)):
-        dst = str(tmp_path / f"{forced}.npz")
-        env = dict(os.environ, AGSX_SORT=forced)
+    for forced, flag, order in (("depth", 0, "morton"), ("bucket", 1, "morton"), ("depth", 0, "input")):
+        # AGSX_SCENE_ORDER=input keeps the caller's storage order
+        dst = str(tmp_path / f"{forced}_{order}.npz")
+        env = dict(os.environ, AGSX_SORT=forced, AGSX_SCENE_ORDER=order)
         res = subprocess.run([sys.executable, "-c", code, root, dst], env=env, capture_output=True, text=True,
                              timeout=300)
         assert res.returncode == 0, res.stderr[-2000:]
