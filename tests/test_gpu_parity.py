@@ -1041,3 +1041,28 @@ def test_sort_paths_agree(tmp_path, mode):
         assert int(f["b"]) == flag
         assert np.array_equal(f["keys"], got[0][1]) and np.array_equal(f["gids"], got[0][2])
         assert np.array_equal(f["image"].view(np.uint32), got[0][4].view(np.uint32))
+
+
+def test_storage_order_edge_scenes(ctx, port):
+    """The Morton storage order on degenerate scenes: a single
+    Gaussian, many Gaussians at one position (equal Morton codes, equal depths:
+    every tie must fall back to Gaussian-id order), and non-finite means
+    (culled, and ignored by the bounding box of the codes). Keys, ranges,
+    counts and the exact image equal the oracle's."""
+    o = port.synth_scene(7, 600, "slab", cameras=2, width=160, height=120, focal=120.0)
+    cases = {}
+    one = port.synth_scene(7, 1, "slab", cameras=2, width=160, height=120, focal=120.0)
+    cases["single"] = one
+    same = port.synth_scene(7, 600, "slab", cameras=2, width=160, height=120, focal=120.0)
+    same.mean[:] = same.mean[0]  # one position: identical depth keys, gid order decides
+    cases["coincident"] = same
+    nanm = port.synth_scene(7, 600, "slab", cameras=2, width=160, height=120, focal=120.0)
+    nanm.mean[::7, 0] = np.nan
+    nanm.mean[3::11, 2] = np.inf
+    cases["non_finite"] = nanm
+    for name, sc in cases.items():
+        dev = ctx.upload(sc.mean, sc.scale, sc.rotation, sc.opacity, sc.sh)
+        for mode in ("ellipse", "aabb"):
+            out, _ = check_frame(ctx, port, sc, dev, 0, mode, exact=True)
+            assert out["pair_count"] >= 0, name
+    del o
