@@ -313,37 +313,6 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
     }
 }
 
-// Exact cull of one splat against a warp's pixel-centre rectangle: true when
-// min over the rectangle of Q = d^T inv d exceeds qcut (with margins for the
-// float evaluation of the reference's d and q), so no pixel of the rectangle
-// can reach alpha >= tau.  Evaluated in double by one lane per splat.
-__device__ __forceinline__ bool rect_outside(float4 a, float iyy, float qcut, float x0, float x1, float y0,
-                                             float y1) {
-    const double xx = a.z, xy = 0.5 * static_cast<double>(a.w), yy = iyy;
-    const double cx = a.x, cy = a.y;
-    if (!(qcut < __int_as_float(0x7f800000))) return false;
-    if (cx >= x0 && cx <= x1 && cy >= y0 && cy <= y1) return false;
-    const double det = xx * yy - xy * xy;
-    if (!(xx > 0.0) || !(yy > 0.0) || !(det > 0.0)) return false;
-    auto q = [&](double dx, double dy) { return xx * dx * dx + 2.0 * xy * dx * dy + yy * dy * dy; };
-    double m = 1e300;
-    for (int e = 0; e < 2; ++e) {  // horizontal edges y = y0, y1
-        const double dy = (e ? y1 : y0) - cy;
-        const double x = fmin(fmax(cx - xy * dy / xx, static_cast<double>(x0)), static_cast<double>(x1));
-        m = fmin(m, q(x - cx, dy));
-    }
-    for (int e = 0; e < 2; ++e) {  // vertical edges x = x0, x1
-        const double dx = (e ? x1 : x0) - cx;
-        const double y = fmin(fmax(cy - xy * dx / yy, static_cast<double>(y0)), static_cast<double>(y1));
-        m = fmin(m, q(dx, y - cy));
-    }
-    const double disc = sqrt(0.25 * (xx - yy) * (xx - yy) + xy * xy);
-    const double lmin = 0.5 * (xx + yy) - disc;
-    if (!(lmin > 0.0)) return false;
-    const double kappa = (fmax(fabs(xx), fabs(yy)) + fabs(xy)) / lmin;
-    return m * (1.0 - 1e-5 - 64.0 * 0x1p-24 * kappa) > static_cast<double>(qcut);
-}
-
 // Default (fast-alpha) rasterizer for 16x16 tiles: warp-persistent.  The
 // work unit is half a tile (16 columns x 8 rows); warps pull units from a
 // global counter, so load balances at warp granularity and no CTA waits on
@@ -357,7 +326,7 @@ __device__ __forceinline__ bool rect_outside(float4 a, float iyy, float qcut, fl
 //   expf, reference order) -- every alpha >= tau decision is the reference's.
 // P_it per tile (pairs iterated before saturation, rasterizer.cpp:55-56) is
 // the max over its two units, combined through a per-tile 64-bit word.
-template <bool RECT, bool STATS>
+template <bool STATS>
 __global__ void __launch_bounds__(256, 3)
 k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
@@ -458,7 +427,6 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 ly1 = static_cast<float>(y0 + yhi) + 0.5f;
             }
             bool rel = base + lane < end && meets_box(cA.x, cA.y, unpack_extent(cC.w), lx0, lx1, ly0, ly1);
-            if (RECT && rel) rel = !rect_outside(cA, cB.x, cB.z, cx0, cx1, cy0, cy1);
             uint32_t m = __ballot_sync(0xffffffffu, rel);
             if (!m) continue;
             sS[warp][lane][0] = cA;
@@ -660,23 +628,20 @@ void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const 
                          const float4* P0, const float4* P1, const float4* P2, float* image, uint32_t* unit_ctr,
                          unsigned long long* tile_pit, unsigned long long* pit, unsigned long long* dbg,
                          uint32_t* band_done, int band_rows, uint8_t* img_u8) {
-    static const int mode = [] {
-        const char* e = std::getenv("AGSX_RASTER_RECT");
+    static const bool stats = [] {  // AGSX_RASTER_STATS=1: work counters in frame_stats()
         const char* t = std::getenv("AGSX_RASTER_STATS");
-        return ((e && *e == '1') ? 1 : 0) | ((t && *t == '1') ? 2 : 0);
+        return t && *t == '1';
     }();
 #define AGSX_RU_ARGS st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg, band_done, band_rows, img_u8
-    switch (mode) {
-        case 0: launch_pdl(k_raster_units<false, false>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
-        case 1: launch_pdl(k_raster_units<true, false>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
-        case 2: launch_pdl(k_raster_units<false, true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
-        default: launch_pdl(k_raster_units<true, true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS); break;
-    }
+    if (stats)
+        launch_pdl(k_raster_units<true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS);
+    else
+        launch_pdl(k_raster_units<false>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS);
 #undef AGSX_RU_ARGS
 }
 
 cudaError_t raster_units_occupancy(int* occ) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_raster_units<false, false>, 256, 0);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_raster_units<false>, 256, 0);
 }
 
 // Any tile size in [1, 64]: 256 threads, pixel k of thread t is tile pixel

@@ -627,10 +627,10 @@ def test_contributions_match_oracle(ctx, port, layout, mode, ts):
     assert rc == 5 and count.value == len(want)
 
 
-@pytest.mark.parametrize("env", ["AGSX_RASTER_STATS=1", "AGSX_RASTER_RECT=1"])
+@pytest.mark.parametrize("env", ["AGSX_RASTER_STATS=1"])
 def test_raster_diagnostic_variants(tmp_path, env):
-    """The diagnostic rasterizer variants (work counters; fp64 rectangle cull)
-    render the same frame as the default one (counters: iterations and live
+    """The diagnostic rasterizer variant (work counters, AGSX_RASTER_STATS)
+    renders the same frame as the default one (counters: iterations and live
     evaluations reported, every fast blend counted once)."""
     import subprocess
     import sys
