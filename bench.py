@@ -155,11 +155,13 @@ def moved_bytes(n, m, p, p_it, tiles, px, depth_passes, bucketed):
     n Gaussians, m splats with >= 1 tile, p pairs, tiles, px pixels).
 
     Depth-then-tile path (default):
-      preprocess  K1 reads the 56 B scene SoA, writes status + depth key (8 B)
-                  per Gaussian and the 64 B P0..P3 planes per splat with tiles,
-                  zeroes ranges / P_it words (16 B per tile);
-      sort        depth pass 0 (upsweep + downsweep read 4 B keys of all n,
-                  8 B key+value written per splat), depth passes 1.. (4 B
+      preprocess  K1 reads the 56 B scene SoA and the 4 B slot -> id map
+                  (scene in Morton order), writes status + depth
+                  key (8 B) per Gaussian and the 64 B P0..P3 planes per splat
+                  with tiles, zeroes ranges / P_it words (16 B per tile);
+      sort        depth pass 0 (upsweep + downsweep read 4 B keys of all n, the
+                  downsweep 4 B slot values, 8 B key+value written per splat),
+                  depth passes 1.. (4 B
                   upsweep read + 8 B read + 8 B write per splat), the last
                   pass's tile-count by-product (4 B gather + 4 B write per
                   splat), 2 tile passes over the pairs (4 + 8 + 8 B each),
@@ -182,9 +184,9 @@ def moved_bytes(n, m, p, p_it, tiles, px, depth_passes, bucketed):
             "raster": raster,
         }
     return {
-        "preprocess": 56 * n + 8 * n + 64 * m + 16 * tiles,
+        "preprocess": 56 * n + 4 * n + 8 * n + 64 * m + 16 * tiles,
         "pair_gen": 24 * m + 8 * p,
-        "sort": (8 * n + 8 * m) + max(depth_passes - 1, 0) * 20 * m + 8 * m + 2 * 20 * p + 4 * p + 8 * tiles,
+        "sort": (12 * n + 8 * m) + max(depth_passes - 1, 0) * 20 * m + 8 * m + 2 * 20 * p + 4 * p + 8 * tiles,
         "raster": raster,
     }
 
