@@ -429,13 +429,7 @@ void enqueue_depth_sort(agsx_ctx* ctx, uint64_t n, uint64_t tiles, const FramePa
         sb.kmax = &ctr->kmax;
         // The pass runs in Gaussian-id order (equal depths keep id order)
         // and carries the storage slots on as values (DevScene)
-#ifdef AGSX_PASS0_GATHER
-        SortBias s0 = sb;  // K1 wrote the keys in slot order: read them through inv
-        s0.gather = scene_inv;
-        sort_pass<uint32_t>(ctx, dk[0], nullptr, dk[1], dv[1], nullptr, n, 0, true, &ctr->m, {}, s0);
-#else
         sort_pass<uint32_t>(ctx, dk[0], scene_inv, dk[1], dv[1], nullptr, n, 0, true, &ctr->m, {}, sb);
-#endif
         for (int ps = 1; ps < 4; ++ps) {
             SortCountOut co;
             SortBias sp = sb;

@@ -270,37 +270,6 @@ __device__ __forceinline__ void for_each_tile_hit(const TileTest& t, const Frame
     const float cx = t.cx, cy = t.cy;
     float y0 = static_cast<float>(s.ty0) * ts;  // tile coordinates advance by exact float adds
     const float x0_first = static_cast<float>(s.tx0) * ts;
-#ifdef AGSX_K1_BRANCHFREE
-    // Variant (measured slower: preprocess 0.185 vs 0.177 ms):
-    // branch-free per tile, all four edge minima evaluated and OR-ed, one
-    // exact division per tile (a column's right-edge minimiser is the next
-    // column's left one).  The default below exits at the first edge that
-    // hits, which on K1's packed survivor warps is usually the first one.
-    for (int ty = s.ty0; ty <= s.ty1; ++ty, y0 += ts) {
-        const float y1 = smin(y0 + ts, H);
-        const float dy0 = y0 - cy, dy1 = y1 - cy;
-        const float xh0 = cx - t.ixy * dy0 / t.ixx;
-        const float xh1 = cx - t.ixy * dy1 / t.ixx;
-        const bool row_in = cy >= y0 && cy <= y1;
-        const bool row_box = y0 <= cy + t.ry && cy - t.ry <= y1;
-        float x0 = x0_first;
-        float yv0 = cy - t.ixy * (x0 - cx) / t.iyy;
-        for (int tx = s.tx0; tx <= s.tx1; ++tx, x0 += ts) {
-            const float x1 = smin(x0 + ts, W);
-            const float dxl = x0 - cx, dxr = x1 - cx;
-            const float yv1 = cy - t.ixy * dxr / t.iyy;
-            const bool box = row_box && x0 <= cx + t.rx && cx - t.rx <= x1;
-            const bool in = row_in && cx >= x0 && cx <= x1;  // centre inside: min = 0 <= r2
-            const bool h0 = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh0, x0, x1) - cx, dy0) <= t.r2;
-            const bool h1 = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xh1, x0, x1) - cx, dy1) <= t.r2;
-            const bool v0 = quad_form(t.ixx, t.ixy, t.iyy, dxl, sclamp(yv0, y0, y1) - cy) <= t.r2;
-            const bool v1 = quad_form(t.ixx, t.ixy, t.iyy, dxr, sclamp(yv1, y0, y1) - cy) <= t.r2;
-            if (box && (in || h0 || h1 || v0 || v1)) f(tx, ty);
-            yv0 = yv1;
-        }
-    }
-    return;
-#endif
     for (int ty = s.ty0; ty <= s.ty1; ++ty, y0 += ts) {
         const float y1 = smin(y0 + ts, H);
         const float dy0 = y0 - cy, dy1 = y1 - cy;
@@ -349,80 +318,14 @@ __device__ __forceinline__ uint32_t count_tiles(const TileTest& t, const FramePa
 // spans {rx, ry, r2, kHitsRecompute} and the emitter re-runs the test.
 constexpr uint32_t kHitsRecompute = 0xffffffffu;
 
-// Hit mask of the ellipse / AdaGScale test over a span of sw x sh tiles
-// (sh + 1 <= kMaskRowEdges), with every division hoisted: the horizontal-edge
-// minimisers x(y) = cx - ixy (y - cy) / ixx depend only on the row edge and
-// the vertical-edge minimisers y(x) = cy - ixy (x - cx) / iyy only on the
-// column edge, so a splat needs sh + 1 and sw + 1 exact divisions instead of
-// up to four per tile.  The row-edge values live in the caller's per-thread
-// table xh[k * stride].  Every value is computed by the reference's
-// expression and min_quad_to_rect's decision is "some edge minimum <= r2"
-// (pair_gen.cpp:65-83, 145-158), so the mask is bit-identical to
-// for_each_tile_hit's; only the visiting order differs (column-major here).
-constexpr int kMaskRowEdges = 16;
-__device__ __forceinline__ unsigned long long hit_mask_hoisted(const TileTest& t, const FrameParams& p, const Span& s,
-                                                               float* xh, int stride) {
-    const float ts = static_cast<float>(p.tile_size);
-    const float W = static_cast<float>(p.W), H = static_cast<float>(p.H);
-    const float cx = t.cx, cy = t.cy;
-    const int sw = s.tx1 - s.tx0 + 1, sh = s.ty1 - s.ty0 + 1;
-    {
-        float y = static_cast<float>(s.ty0) * ts;
-        for (int k = 0; k <= sh; ++k, y += ts) {
-            const float ye = k == sh ? smin(y, H) : y;  // the last row's bottom edge is clipped (tile_rect)
-            xh[k * stride] = cx - t.ixy * (ye - cy) / t.ixx;
-        }
-    }
-    unsigned long long mask = 0;
-    float x0 = static_cast<float>(s.tx0) * ts;
-    float yv0 = cy - t.ixy * (x0 - cx) / t.iyy;
-    for (int c = 0; c < sw; ++c, x0 += ts) {
-        const float x1 = smin(x0 + ts, W);
-        const float yv1 = cy - t.ixy * (x1 - cx) / t.iyy;
-        const float dxl = x0 - cx, dxr = x1 - cx;
-        const bool col_in = cx >= x0 && cx <= x1;
-        const bool v0_first = fabsf(dxl) <= fabsf(dxr);
-        const float dxa = v0_first ? dxl : dxr, yva = v0_first ? yv0 : yv1;
-        const float dxb = v0_first ? dxr : dxl, yvb = v0_first ? yv1 : yv0;
-        const bool col_box = x0 <= cx + t.rx && cx - t.rx <= x1;
-        float y0 = static_cast<float>(s.ty0) * ts;
-        for (int r = 0; r < sh; ++r, y0 += ts) {
-            const float y1 = smin(y0 + ts, H);
-            if (!(col_box && y0 <= cy + t.ry && cy - t.ry <= y1)) continue;  // box_overlap
-            bool hit = col_in && cy >= y0 && cy <= y1;  // centre inside: min = 0 <= r2
-            const float dy0 = y0 - cy, dy1 = y1 - cy;
-            const bool h0_first = fabsf(dy0) <= fabsf(dy1);
-            if (!hit) {
-                const float xa = xh[(h0_first ? r : r + 1) * stride];
-                hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xa, x0, x1) - cx, h0_first ? dy0 : dy1) <= t.r2;
-            }
-            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, dxa, sclamp(yva, y0, y1) - cy) <= t.r2;
-            if (!hit) {
-                const float xb = xh[(h0_first ? r + 1 : r) * stride];
-                hit = quad_form(t.ixx, t.ixy, t.iyy, sclamp(xb, x0, x1) - cx, h0_first ? dy1 : dy0) <= t.r2;
-            }
-            if (!hit) hit = quad_form(t.ixx, t.ixy, t.iyy, dxb, sclamp(yvb, y0, y1) - cy) <= t.r2;
-            if (hit) mask |= 1ull << (r * sw + c);
-        }
-        yv0 = yv1;
-    }
-    return mask;
-}
-
-// xh: optional per-thread table of kMaskRowEdges floats (stride apart) for
-// hit_mask_hoisted.
-__device__ __forceinline__ uint4 hit_record(const TileTest& t, const FrameParams& p, uint32_t& count,
-                                            float* xh = nullptr, int stride = 1) {
+__device__ __forceinline__ uint4 hit_record(const TileTest& t, const FrameParams& p, uint32_t& count) {
     count = 0;
     const Span s = tile_span(t, p);
     if (s.empty) return make_uint4(0u, 0u, 0u, 0u);
     const int sw = s.tx1 - s.tx0 + 1, sh = s.ty1 - s.ty0 + 1;
     if (sw * sh <= 64) {
         unsigned long long mask = 0;
-        if (xh && sh < kMaskRowEdges && t.mode != AGSX_MODE_AABB && t.mode != AGSX_MODE_OBB)
-            mask = hit_mask_hoisted(t, p, s, xh, stride);
-        else
-            for_each_tile_hit(t, p, [&](int tx, int ty) { mask |= 1ull << ((ty - s.ty0) * sw + (tx - s.tx0)); });
+        for_each_tile_hit(t, p, [&](int tx, int ty) { mask |= 1ull << ((ty - s.ty0) * sw + (tx - s.tx0)); });
         count = static_cast<uint32_t>(__popcll(mask));
         return make_uint4(static_cast<uint32_t>(mask), static_cast<uint32_t>(mask >> 32),
                           static_cast<uint32_t>(s.tx0) | (static_cast<uint32_t>(s.ty0) << 16),

@@ -14,7 +14,7 @@
 #include "agsx_internal.cuh"
 #include "kernels.cuh"
 
-constexpr int kPreQ = 16;  // words per survivor slot: the queue between K1's phases, then the row-edge table
+constexpr int kPreQ = 12;  // words queued per survivor between K1's phases
 
 #ifndef AGSX_PRE_MINB
 #define AGSX_PRE_MINB 4
@@ -213,7 +213,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
     // the stores -- runs on packed warps instead of on the survivors' lanes of
     // every warp.
     __shared__ float s_q[kPreQ][256];  // per survivor slot (structure of arrays)
-    __shared__ uint32_t s_gid[256];
+    __shared__ uint32_t s_slot[256];  // storage slot of each queued survivor
     __shared__ uint32_t s_n;
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
@@ -240,11 +240,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         if (ok && th >= opacity) ok = false;
         if (!ok) {
             status[i] = 0u;
-#ifdef AGSX_PASS0_GATHER
-            if (!bk.tile_cnt) dkeys[i] = 0xffffffffu;
-#else
             if (!bk.tile_cnt) dkeys[sc.id_of(static_cast<uint32_t>(i))] = 0xffffffffu;  // keys in id order
-#endif
         }
     }
     // queue the survivors (converged warp: one shared-memory atomic per warp)
@@ -254,7 +250,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
     qbase = __shfl_sync(0xffffffffu, qbase, 0);
     if (ok) {
         const uint32_t at = qbase + __popc(okb & ((1u << lane) - 1u));
-        s_gid[at] = static_cast<uint32_t>(i);
+        s_slot[at] = static_cast<uint32_t>(i);
         s_q[0][at] = m2x;
         s_q[1][at] = m2y;
         s_q[2][at] = cxx;
@@ -281,7 +277,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
     uint4 hit_rec = make_uint4(0u, 0u, 0u, 0u);
     uint32_t gi = 0;  // storage slot of the survivor (DevScene); sc.id_of(gi) is its Gaussian id
     if (alive) {
-        gi = s_gid[slot];
+        gi = s_slot[slot];
         const float m2x = s_q[0][slot], m2y = s_q[1][slot];
         const float cxx = s_q[2][slot], cxy = s_q[3][slot], cyy = s_q[4][slot], det = s_q[5][slot];
         const float opacity = s_q[6][slot], th = s_q[7][slot], tz = s_q[8][slot];
@@ -291,13 +287,7 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         const float inv_det = 1.0f / det;  // SymMat2::inverse (math.hpp:85-88)
         const float ixx = cyy * inv_det, ixy = -cxy * inv_det, iyy = cxx * inv_det;
         const TileTest tt = make_tile_test(m2x, m2y, cxx, cxy, cyy, ixx, ixy, iyy, opacity, th, p);
-        // the slot's queued words are in registers now: its column of s_q
-        // becomes this thread's row-edge table (hit_mask_hoisted)
-#ifdef AGSX_K1_HOIST
-        const uint4 hits = hit_record(tt, p, cnt, &s_q[0][slot], 256);
-#else
         const uint4 hits = hit_record(tt, p, cnt);
-#endif
         hit_rec = hits;
         keep = cnt > 0;
         float rgb[3] = {0.5f, 0.5f, 0.5f};
@@ -368,13 +358,9 @@ k_preprocess(FrameParams p, DevScene sc, SplatPlanes pl, uint32_t* __restrict__ 
         }
         return;
     }
-#ifdef AGSX_PASS0_GATHER
-    if (alive) dkeys[gi] = keep ? __float_as_uint(depth) : 0xffffffffu;
-#else
     // the depth keys in Gaussian-id order: the first depth pass reads them
     // in order (equal depths keep id order) with the storage slots as values
     if (alive) dkeys[sc.id_of(gi)] = keep ? __float_as_uint(depth) : 0xffffffffu;
-#endif
     // range of the depth keys (positive floats: bit order = value order), so
     // the depth sort can skip its top digit when the keys span < 2^24.  Per
     // warp, and an atomic only when it improves on the value last seen (the

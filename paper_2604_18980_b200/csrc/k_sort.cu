@@ -89,7 +89,7 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint64_t i = base + u * kSortThreads + tid;
-            k[u] = i < hi ? keys[sb.gather ? sb.gather[i] : i] : K(0);
+            k[u] = i < hi ? keys[i] : K(0);
             ok[u] = i < hi && !(use_sentinel && k[u] == sentinel);
         }
 #pragma unroll
@@ -194,10 +194,8 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         if (full) {
 #pragma unroll
             for (int it = 0; it < kSortItems; ++it) {
-                const uint32_t pos = wbase + it * 32;
-                const uint32_t src = sb.gather ? sb.gather[pos] : pos;
-                k[it] = kin[src];
-                v[it] = vin ? vin[pos] : src;
+                k[it] = kin[wbase + it * 32];
+                v[it] = vin ? vin[wbase + it * 32] : wbase + it * 32;
                 ok[it] = true;
             }
         } else {
@@ -205,9 +203,8 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             for (int it = 0; it < kSortItems; ++it) {
                 const uint32_t idx = wbase + it * 32;
                 ok[it] = idx < hi;
-                const uint32_t src = ok[it] && sb.gather ? sb.gather[idx] : idx;
-                k[it] = ok[it] ? kin[src] : K(0);
-                v[it] = ok[it] ? (vin ? vin[idx] : src) : 0u;
+                k[it] = ok[it] ? kin[idx] : K(0);
+                v[it] = ok[it] ? (vin ? vin[idx] : idx) : 0u;
                 if (use_sentinel && k[it] == sentinel) ok[it] = false;
             }
         }

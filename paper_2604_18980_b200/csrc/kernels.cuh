@@ -130,10 +130,6 @@ struct SortBias {
     const uint32_t* kmax = nullptr;
     int only_wide = 0;
     int co_if_narrow = 0;
-    // Gathered input (the first depth pass over a scene in storage order,
-    // DevScene): position i of the pass reads key kin[gather[i]] and, with no
-    // value array, value gather[i] -- the pass runs in Gaussian-id order.
-    const uint32_t* gather = nullptr;
 };
 template <typename K>
 void launch_sort_pass(int grid, size_t smem, cudaStream_t st, const K* kin, const uint32_t* vin, K* kout,
