@@ -342,6 +342,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
     constexpr int NWB = 8;  // warps per block
     // staged splat j of warp w: sS[w][j][0..2] = P0, P1, {rgb, log2 opacity}
     __shared__ __align__(16) float4 sS[NWB][32][3];
+    __shared__ uint8_t sJ[NWB][32];  // batch index of staged record r
     __shared__ uint64_t sTab[32];
     __shared__ __align__(16) float sOut[NWB][8 * 16 * 3];
 
@@ -427,22 +428,27 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 ly1 = static_cast<float>(y0 + yhi) + 0.5f;
             }
             bool rel = base + lane < end && meets_box(cA.x, cA.y, unpack_extent(cC.w), lx0, lx1, ly0, ly1);
-            uint32_t m = __ballot_sync(0xffffffffu, rel);
+            const uint32_t m = __ballot_sync(0xffffffffu, rel);
             if (!m) continue;
-            sS[warp][lane][0] = cA;
-            // {iyy, opacity, band width w = qcut - qsafe, qsafe}: a pixel is in
-            // the margin band only if 0 <= q - qsafe <= w (rounding is
-            // monotone, so fl(q - qsafe) <= fl(qcut - qsafe) whenever
-            // q <= qcut; +inf/-inf thresholds give w = +inf)
-            sS[warp][lane][1] = make_float4(cB.x, cB.y, cB.z - cB.w, cB.w);
-            sS[warp][lane][2] = make_float4(cC.x, cC.y, cC.z, fast_log2(cB.y));  // extent no longer needed
+            // the survivors are staged compacted, in pair order: the blend loop
+            // walks consecutive records (no find-first per splat)
+            const uint32_t nrel = static_cast<uint32_t>(__popc(m));
+            if (rel) {
+                const int r = __popc(m & ((1u << lane) - 1u));
+                sS[warp][r][0] = cA;
+                // {iyy, opacity, band width w = qcut - qsafe, qsafe}: a pixel is in
+                // the margin band only if 0 <= q - qsafe <= w (rounding is
+                // monotone, so fl(q - qsafe) <= fl(qcut - qsafe) whenever
+                // q <= qcut; +inf/-inf thresholds give w = +inf)
+                sS[warp][r][1] = make_float4(cB.x, cB.y, cB.z - cB.w, cB.w);
+                sS[warp][r][2] = make_float4(cC.x, cC.y, cC.z, fast_log2(cB.y));  // extent no longer needed
+                sJ[warp][r] = static_cast<uint8_t>(lane);  // its index in the batch (P_it)
+            }
             __syncwarp();
-            while (m) {
-                const int j = __ffs(m) - 1;
-                m &= m - 1;
-                const float4 sa = sS[warp][j][0];  // mx, my, inv.xx, 2*inv.xy
-                const float4 sb = sS[warp][j][1];  // inv.yy, opacity, qcut - qsafe, qsafe
-                const float4 sc = sS[warp][j][2];  // r, g, b, log2 opacity
+            for (uint32_t jj = 0; jj < nrel; ++jj) {
+                const float4 sa = sS[warp][jj][0];  // mx, my, inv.xx, 2*inv.xy
+                const float4 sb = sS[warp][jj][1];  // inv.yy, opacity, qcut - qsafe, qsafe
+                const float4 sc = sS[warp][jj][2];  // r, g, b, log2 opacity
                 const float dx = px - sa.x;
                 const float t1 = sa.z * dx * dx;
                 const float t2 = sa.w * dx;
@@ -530,7 +536,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 }
                 const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
                 if (!__any_sync(0xffffffffu, tmax >= tfloor)) {
-                    death = base - start + j + 1;
+                    death = base - start + sJ[warp][jj] + 1;
                     all_done = true;
                     break;
                 }
