@@ -186,6 +186,12 @@ int agsx_scene_upload(agsx_ctx* ctx, const agsx_scene_desc* d, agsx_scene** out)
             check_launch(ctx);
         }
         release(stage);
+        float mo = -INFINITY;  // NaN opacities count as +inf (the clamp variant handles them)
+        for (uint64_t i = 0; i < n; ++i) {
+            const float o = d->opacity[i];
+            mo = o > mo ? o : (o == o ? mo : INFINITY);
+        }
+        sc->max_opacity = mo;
         if (scene_order_morton() && n > 1) {
             // storage order: 3D Morton order of the means (DevScene).  Spatial
             // neighbours share K1's warps (similar footprints: less divergence in

@@ -68,6 +68,7 @@ struct agsx_scene {
     int D = 1;
     Buf pos_op, rot, scale_r, sh_gb, sh_rest;
     Buf orig, inv;  // storage order (DevScene); empty: slot = id
+    float max_opacity = INFINITY;  // over the scene (NaN counts as +inf): picks the clamp-free raster
     DevScene view() const {
         DevScene s;
         s.n = n;

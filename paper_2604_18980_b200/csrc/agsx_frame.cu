@@ -602,6 +602,7 @@ int start_frame(agsx_ctx* ctx, const agsx_scene* sc, const agsx_camera* cam, con
     FrameParams p;
     const int rc = prepare(ctx, cam, cfg, lut, p);
     if (rc) return rc;
+    p.clamp_free = sc->max_opacity < p.aclamp;  // alpha <= opacity < aclamp everywhere
     const uint64_t tiles = static_cast<uint64_t>(p.tiles_x) * p.tiles_y;
     ensure_frame_buffers(ctx, sc->n, tiles, static_cast<uint64_t>(cam->width) * cam->height,
                          cfg->mode == AGSX_MODE_OBB, cfg->pair_budget);

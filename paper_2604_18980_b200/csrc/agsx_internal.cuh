@@ -35,6 +35,7 @@ struct FrameParams {
     uint32_t flags;
     int raster_ppt;  // pixels per thread of the 16x16 rasterizer (2 or 4)
     uint32_t unit_lo, unit_hi;  // raster work-unit range of this launch (unit_hi = 0: all units)
+    uint32_t clamp_free;        // no splat's opacity reaches aclamp (alpha_at's clamp never binds)
     // T_upper LUT (lut.hpp:11-26)
     int adaptive;
     float lut_dmin, lut_dmax;

@@ -326,7 +326,11 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
 //   expf, reference order) -- every alpha >= tau decision is the reference's.
 // P_it per tile (pairs iterated before saturation, rasterizer.cpp:55-56) is
 // the max over its two units, combined through a per-tile 64-bit word.
-template <bool STATS>
+// CLAMP = false when no splat's opacity reaches the clamp (FrameParams::
+// clamp_free, from the scene's maximum opacity): alpha <= opacity < clamp, so
+// the fast path drops the clamp test (4 predicated FMNMX issue slots per
+// iteration otherwise); the exact path always applies alpha_at's clamp.
+template <bool STATS, bool CLAMP>
 __global__ void __launch_bounds__(256, 3)
 k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __restrict__ vals,
                const float4* __restrict__ P0, const float4* __restrict__ P1, const float4* __restrict__ P2,
@@ -340,8 +344,10 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                        st_dead = 0;
     constexpr int PPT = 4;
     constexpr int NWB = 8;  // warps per block
-    // staged splat j of warp w: sS[w][j][0..2] = P0, P1, {rgb, log2 opacity}
-    __shared__ __align__(16) float4 sS[NWB][32][3];
+    // staged splat j of warp w: sS[w][j][0..2] = the unit-centred form and
+    // blend data read every iteration, sS[w][j][3] = {mean, opacity} for the
+    // exact path only
+    __shared__ __align__(16) float4 sS[NWB][32][4];
     __shared__ uint8_t sJ[NWB][32];  // batch index of staged record r
     __shared__ uint64_t sTab[32];
     __shared__ __align__(16) float sOut[NWB][8 * 16 * 3];
@@ -386,11 +392,14 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
         const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
         const int x0 = tx * 16, y0 = ty * 16 + half * 8;
         const int w = imin(16, p.W - x0), h = imin(8, p.H - y0);  // h may be <= 0 (bottom tile row)
-        const float px = static_cast<float>(x0 + lx) + 0.5f;
-        float py[PPT], T[PPT], Cr[PPT], Cg[PPT], Cb[PPT];
+        // pixel centres relative to the unit's centre (ucx, ucy): lane
+        // offsets in [-7.5, 7.5] x [-3.5, 3.5], all exact in float
+        const float ucx = static_cast<float>(x0 + 8), ucy = static_cast<float>(y0 + 4);
+        const float lxl = static_cast<float>(lx) - 7.5f;
+        float lyl[PPT], T[PPT], Cr[PPT], Cg[PPT], Cb[PPT];
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-            py[k] = static_cast<float>(y0 + 4 * g + k) + 0.5f;
+            lyl[k] = static_cast<float>(4 * g + k) - 3.5f;
             T[k] = (lx < w && 4 * g + k < h) ? 1.0f : 0.0f;  // outside the image: saturated
             Cr[k] = Cg[k] = Cb[k] = 0.0f;
         }
@@ -435,23 +444,48 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             const uint32_t nrel = static_cast<uint32_t>(__popc(m));
             if (rel) {
                 const int r = __popc(m & ((1u << lane) - 1u));
-                sS[warp][r][0] = cA;
-                // {iyy, opacity, band width w = qcut - qsafe, qsafe}: a pixel is in
-                // the margin band only if 0 <= q - qsafe <= w (rounding is
-                // monotone, so fl(q - qsafe) <= fl(qcut - qsafe) whenever
-                // q <= qcut; +inf/-inf thresholds give w = +inf)
-                sS[warp][r][1] = make_float4(cB.x, cB.y, cB.z - cB.w, cB.w);
-                sS[warp][r][2] = make_float4(cC.x, cC.y, cC.z, fast_log2(cB.y));  // extent no longer needed
+                // q in unit-centred coordinates, expanded once per (splat,
+                // unit): with (mlx, mly) = mean - unit centre,
+                //   q(l) = ixx lx^2 + 2ixy lx ly + iyy ly^2 + bx lx + by ly + c0,
+                // so a pixel costs 2 FMA (Horner in ly) and no subtraction.
+                // Every term and partial sum is bounded by S = the absolute
+                // form at (|mlx| + 7.5, |mly| + 3.5); the float evaluation here
+                // and in the loop, the rounded (mlx, mly), and the reference's
+                // own rounding of (px - mx, py - my) and of its q differ from
+                // the reference's q by < 31 u S (u = 2^-24).  The thresholds
+                // widen by E = 2.5e-6 S > 40 u S (directed rounding), so
+                // q < qsafe' still implies alpha >= tau and q > qcut' alpha < tau;
+                // the band between goes to the exact path.
+                const float mlx = cA.x - ucx, mly = cA.y - ucy;
+                const float ixx = cA.z, b2 = cA.w, iyy = cB.x;
+                const float bx = -(2.0f * ixx * mlx + b2 * mly);
+                const float by = -(b2 * mlx + 2.0f * iyy * mly);
+                const float c0 = (ixx * mlx * mlx + b2 * mlx * mly) + iyy * mly * mly;
+                const float X = fabsf(mlx) + 7.5f, Y = fabsf(mly) + 3.5f;
+                const float S = (fabsf(ixx) * X * X + fabsf(b2) * X * Y) + fabsf(iyy) * Y * Y;
+                const float E = S * 2.5e-6f;
+                const float inf = __int_as_float(0x7f800000);
+                float qs = __fsub_rd(cB.w, E), qc = __fadd_ru(cB.z, E);
+                if (!(E < inf)) qs = -inf, qc = inf;  // no bound: every pixel is exact
+                sS[warp][r][0] = make_float4(ixx, b2, iyy, bx);
+                // {by, c0, band width w = qcut' - qsafe' (rounded up), qsafe'}:
+                // a pixel is in the band only if 0 <= q - qsafe' <= w (rounding
+                // is monotone, so fl(q - qsafe') <= w whenever q <= qcut';
+                // +inf/-inf thresholds give w = +inf)
+                sS[warp][r][1] = make_float4(by, c0, __fsub_ru(qc, qs), qs);
+                // red carries the clamp flag in its sign (colours are >= 0):
+                // alpha_at's clamp can bind only for opacity >= clamp
+                sS[warp][r][2] = make_float4(cB.y >= aclamp ? -cC.x : cC.x, cC.y, cC.z, fast_log2(cB.y));
+                sS[warp][r][3] = make_float4(cA.x, cA.y, cB.y, 0.0f);
                 sJ[warp][r] = static_cast<uint8_t>(lane);  // its index in the batch (P_it)
             }
             __syncwarp();
             for (uint32_t jj = 0; jj < nrel; ++jj) {
-                const float4 sa = sS[warp][jj][0];  // mx, my, inv.xx, 2*inv.xy
-                const float4 sb = sS[warp][jj][1];  // inv.yy, opacity, qcut - qsafe, qsafe
-                const float4 sc = sS[warp][jj][2];  // r, g, b, log2 opacity
-                const float dx = px - sa.x;
-                const float t1 = sa.z * dx * dx;
-                const float t2 = sa.w * dx;
+                const float4 sa = sS[warp][jj][0];  // inv.xx, 2*inv.xy, inv.yy, bx
+                const float4 sb = sS[warp][jj][1];  // by, c0, qcut' - qsafe', qsafe'
+                const float4 sc = sS[warp][jj][2];  // +-r, g, b, log2 opacity
+                const float qB = __fmaf_rn(sa.y, lxl, sb.x);                     // 2ixy lx + by
+                const float qC = __fmaf_rn(__fmaf_rn(sa.x, lxl, sa.w), lxl, sb.y);  // (ixx lx + bx) lx + c0
                 const float l2op = sc.w;
                 const float qsafe = sb.w;
                 const uint32_t wbits = __float_as_uint(sb.z);
@@ -477,8 +511,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 float e[PPT], qv[PPT];
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
-                    const float dy = py[k] - sa.y;
-                    const float q = __fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1);
+                    const float q = __fmaf_rn(__fmaf_rn(sa.z, lyl[k], qB), lyl[k], qC);
                     qv[k] = q;
                     const bool fast = q < qsafe;
                     e[k] = fast ? fast_exp2(__fmaf_rn(q, c_ex2, l2op)) : 0.0f;
@@ -492,43 +525,40 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 if (STATS) {  // iterations in which no pixel of the unit is within q <= qcut
                     bool any_in = false;
 #pragma unroll
-                    for (int k = 0; k < PPT; ++k) {
-                        const float dy = py[k] - sa.y;
-                        any_in = any_in || !(__fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1) > qsafe + sb.z);
-                    }
+                    for (int k = 0; k < PPT; ++k) any_in = any_in || !(qv[k] > qsafe + sb.z);
                     st_empty += !__any_sync(0xffffffffu, any_in);
                     bool any_live = false;  // ... or within q <= qcut of no live (T >= floor) pixel
 #pragma unroll
-                    for (int k = 0; k < PPT; ++k) {
-                        const float dy = py[k] - sa.y;
-                        any_live = any_live || (T[k] >= tfloor &&
-                                                !(__fmaf_rn(__fmaf_rn(sb.x, dy, t2), dy, t1) > qsafe + sb.z));
-                    }
+                    for (int k = 0; k < PPT; ++k) any_live = any_live || (T[k] >= tfloor && !(qv[k] > qsafe + sb.z));
                     st_dead += !__any_sync(0xffffffffu, any_live);
                 }
-                if (sb.y >= aclamp) {  // alpha_at's clamp can bind only for opacity >= clamp
+                if (CLAMP && __float_as_int(sc.x) < 0) {  // clamp flag (opacity >= clamp)
 #pragma unroll
                     for (int k = 0; k < PPT; ++k) e[k] = fminf(e[k], aclamp);
                 }
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
                     const float wgt = e[k] * T[k];
-                    Cr[k] = __fmaf_rn(wgt, sc.x, Cr[k]);
+                    Cr[k] = __fmaf_rn(wgt, fabsf(sc.x), Cr[k]);
                     Cg[k] = __fmaf_rn(wgt, sc.y, Cg[k]);
                     Cb[k] = __fmaf_rn(wgt, sc.z, Cb[k]);
                     T[k] = __fmaf_rn(-e[k], T[k], T[k]);
                 }
                 if (__any_sync(0xffffffffu, need_any)) {  // margin band: the reference's alpha_at
+                    const float4 sd = sS[warp][jj][3];  // mx, my, opacity
+                    const float dx = (ucx + lxl) - sd.x;  // px - mx, as the reference rounds it
+                    const float t1 = sa.x * dx * dx;
+                    const float t2 = sa.y * dx;
 #pragma unroll
                     for (int k = 0; k < PPT; ++k) {
                         if (!(__float_as_uint(qv[k] - qsafe) <= wbits)) continue;
-                        const float dy = py[k] - sa.y;
-                        const float qr = (t1 + t2 * dy) + sb.x * dy * dy;  // reference order
-                        const float a = exact_alpha(qr, sb.y, aclamp, sTab);
+                        const float dy = (ucy + lyl[k]) - sd.y;
+                        const float qr = (t1 + t2 * dy) + sa.z * dy * dy;  // reference order
+                        const float a = exact_alpha(qr, sd.z, aclamp, sTab);
                         if (a < tau) continue;
                         const float t_cur = T[k];
                         const float wgt = a * t_cur;
-                        Cr[k] += wgt * sc.x;
+                        Cr[k] += wgt * fabsf(sc.x);
                         Cg[k] += wgt * sc.y;
                         Cb[k] += wgt * sc.z;
                         T[k] = t_cur * (1.0f - a);
@@ -640,14 +670,20 @@ void launch_raster_units(int grid, cudaStream_t st, const FrameParams& p, const 
     }();
 #define AGSX_RU_ARGS st, p, ranges, vals, P0, P1, P2, image, unit_ctr, tile_pit, pit, dbg, band_done, band_rows, img_u8
     if (stats)
-        launch_pdl(k_raster_units<true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS);
+        launch_pdl(k_raster_units<true, true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS);
+    else if (p.clamp_free)
+        launch_pdl(k_raster_units<false, false>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS);
     else
-        launch_pdl(k_raster_units<false>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS);
+        launch_pdl(k_raster_units<false, true>, dim3(grid), dim3(256), 0, AGSX_RU_ARGS);
 #undef AGSX_RU_ARGS
 }
 
 cudaError_t raster_units_occupancy(int* occ) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_raster_units<false>, 256, 0);
+    int a = 0, b = 0;  // both variants run at the occupancy of the smaller
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_raster_units<false, true>, 256, 0);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_raster_units<false, false>, 256, 0);
+    *occ = a < b ? a : b;
+    return e;
 }
 
 // Any tile size in [1, 64]: 256 threads, pixel k of thread t is tile pixel

@@ -125,6 +125,23 @@ def test_render_matches_oracle_small(ctx, port, layout, mode, exact):
                 exact=exact)
 
 
+@pytest.mark.parametrize("exact", [True, False], ids=["exact", "default"])
+@pytest.mark.parametrize("mode", ["ellipse", "adagscale"])
+def test_render_opacities_at_the_clamp(ctx, port, mode, exact):
+    """Opacities at and above alpha_at's clamp (0.99, rasterizer.hpp:44-50):
+    the scene's maximum opacity selects the default rasteriser's clamp variant
+    (a scene below the clamp runs the clamp-free one, as every synthetic
+    layout does); the decisions and the clamped alphas match the oracle."""
+    oscene, _ = scene_pair(port, ctx, 7, 3000, "slab", 2, 320, 240, 250.0)
+    rng = np.random.default_rng(3)
+    sel = rng.random(oscene.count) < 0.3
+    oscene.opacity[sel] = rng.choice(np.float32([0.99, 0.99000007, 0.995, 0.9999999]), int(sel.sum()))
+    dev = ctx.upload(oscene.mean, oscene.scale, oscene.rotation, oscene.opacity, oscene.sh)
+    for view in range(2):
+        check_frame(ctx, port, oscene, dev, view, mode, k=0.3, lut_bins=[0.6] * 20 if mode == "adagscale" else None,
+                    exact=exact)
+
+
 @pytest.mark.parametrize("exact", [True, False])
 def test_render_config1_veil_adagscale(ctx, port, exact):
     """Config 1: veil 100K, 1920x1080, AdaGScale with the calibrated K/LUT."""
