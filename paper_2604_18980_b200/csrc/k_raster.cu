@@ -503,21 +503,24 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 // remaining blend weights sum to less than T <= floor = 1e-4,
                 // which bounds the image difference to the reference by
                 // 1e-4 per channel; the warp stops when all are saturated.
-                // band test as unsigned compares of float bits: q - qsafe < 0
-                // (a fast pixel) has the sign bit set and exceeds any w >= 0.
-                // It admits a superset of the band (pixels just above qcut);
-                // the exact path rejects those by its own alpha >= tau test.
+                // Fast pixels blend under a predicate (no zeroed alphas).  The
+                // band test compares float bits unsigned: q - qsafe' < 0 (a
+                // fast pixel) has the sign bit set and exceeds any w >= 0; NaN
+                // exceeds +inf (never blends, as in the reference).  It admits
+                // a superset of the band (pixels just above qcut'); the exact
+                // path rejects those by its own alpha >= tau test.
                 uint32_t dmin = 0xffffffffu;
+                bool fast[PPT];
                 float e[PPT], qv[PPT];
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
                     const float q = __fmaf_rn(__fmaf_rn(sa.z, lyl[k], qB), lyl[k], qC);
                     qv[k] = q;
-                    const bool fast = q < qsafe;
-                    e[k] = fast ? fast_exp2(__fmaf_rn(q, c_ex2, l2op)) : 0.0f;
+                    fast[k] = q < qsafe;
+                    e[k] = fast_exp2(__fmaf_rn(q, c_ex2, l2op));
                     dmin = umin(dmin, __float_as_uint(q - qsafe));
                     if (STATS) {
-                        st_fast += fast && T[k] >= tfloor;
+                        st_fast += fast[k] && T[k] >= tfloor;
                         st_need += __float_as_uint(q - qsafe) <= wbits;
                     }
                 }
@@ -538,6 +541,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 }
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
+                    if (!fast[k]) continue;
                     const float wgt = e[k] * T[k];
                     Cr[k] = __fmaf_rn(wgt, fabsf(sc.x), Cr[k]);
                     Cg[k] = __fmaf_rn(wgt, sc.y, Cg[k]);
