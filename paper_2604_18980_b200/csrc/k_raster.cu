@@ -318,12 +318,13 @@ k_raster16(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* __re
 // global counter, so load balances at warp granularity and no CTA waits on
 // another warp.  Lane l owns column l%16 and rows 4(l/16)..+3 of its unit.
 // Per 32-record step of the tile's sorted span, each lane tests one splat
-// against the unit's pixel-centre rectangle (extent box, then an exact
-// min-quad test) and the warp blends the survivors in order:
-//   q by FMA (its error is folded into qcut/qsafe), fast pixels (q < qsafe)
-//   blend alpha = min(2^(q c + log2 opacity), clamp) with FMAs; pixels in
-//   the margin band (qsafe <= q <= qcut) are re-evaluated exactly (glibc
-//   expf, reference order) -- every alpha >= tau decision is the reference's.
+// against the box of the unit's live pixel centres (extent box) and the
+// warp blends the survivors in order, staged compacted in shared memory:
+//   the exponent x = c q + log2 opacity of alpha = 2^x in unit-centred form
+//   (2 FMA per pixel; its error bound widens the thresholds), fast pixels
+//   (x > xs) blend alpha = min(2^x, clamp) with FMAs; pixels in the margin
+//   band (xc <= x <= xs) are re-evaluated exactly (glibc expf, reference
+//   order) -- every alpha >= tau decision is the reference's.
 // P_it per tile (pairs iterated before saturation, rasterizer.cpp:55-56) is
 // the max over its two units, combined through a per-tile 64-bit word.
 // CLAMP = false when no splat's opacity reaches the clamp (FrameParams::
@@ -344,10 +345,10 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                        st_dead = 0;
     constexpr int PPT = 4;
     constexpr int NWB = 8;  // warps per block
-    // staged splat j of warp w: sS[w][j][0..2] = the unit-centred form and
-    // blend data read every iteration, sS[w][j][3] = {mean, opacity} for the
-    // exact path only
-    __shared__ __align__(16) float4 sS[NWB][32][4];
+    // staged splat j of warp w: sS[w][j][0..2] = the unit-centred exponent
+    // form and blend data read every iteration, sS[w][j][3..4] = {P0, iyy,
+    // opacity} (unscaled) for the exact path only
+    __shared__ __align__(16) float4 sS[NWB][32][5];
     __shared__ uint8_t sJ[NWB][32];  // batch index of staged record r
     __shared__ uint64_t sTab[32];
     __shared__ __align__(16) float sOut[NWB][8 * 16 * 3];
@@ -358,7 +359,6 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
 
     const uint32_t units = p.unit_hi ? p.unit_hi : 2u * static_cast<uint32_t>(p.tiles_x * p.tiles_y);
     const float tau = p.tau, tfloor = p.tfloor, aclamp = p.aclamp;
-    const float c_ex2 = -0.5f * 1.4426950408889634f;
     const int lx = lane & 15, g = lane >> 4;
 
     // Units are software-pipelined: while unit U renders, the ranges of U+1
@@ -444,50 +444,58 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
             const uint32_t nrel = static_cast<uint32_t>(__popc(m));
             if (rel) {
                 const int r = __popc(m & ((1u << lane) - 1u));
-                // q in unit-centred coordinates, expanded once per (splat,
-                // unit): with (mlx, mly) = mean - unit centre,
+                // The exponent x = c q + L (alpha ~ 2^x, c = -log2(e)/2, L =
+                // log2 opacity) in unit-centred coordinates, expanded once per
+                // (splat, unit): with (mlx, mly) = mean - unit centre,
                 //   q(l) = ixx lx^2 + 2ixy lx ly + iyy ly^2 + bx lx + by ly + c0,
-                // so a pixel costs 2 FMA (Horner in ly) and no subtraction.
-                // Every term and partial sum is bounded by S = the absolute
-                // form at (|mlx| + 7.5, |mly| + 3.5); the float evaluation here
-                // and in the loop, the rounded (mlx, mly), and the reference's
-                // own rounding of (px - mx, py - my) and of its q differ from
-                // the reference's q by < 31 u S (u = 2^-24).  The thresholds
-                // widen by E = 2.5e-6 S > 40 u S (directed rounding), so
-                // q < qsafe' still implies alpha >= tau and q > qcut' alpha < tau;
-                // the band between goes to the exact path.
+                // and every coefficient scaled by c (c0 also carries L), so a
+                // pixel costs 2 FMA (Horner in ly) and feeds EX2 directly.
+                // Every term and partial sum is bounded by S~ = |c| S + |L|,
+                // S = the absolute form at (|mlx| + 7.5, |mly| + 3.5); the float
+                // evaluation here and in the loop, the rounded (mlx, mly) and
+                // scaled coefficients, and the reference's own rounding of
+                // (px - mx, py - my) and of its q keep x within 39 u S~ of
+                // c q_ref + L (u = 2^-24).  With E~ = 4e-6 S~ > 67 u S~ and
+                // directed rounding, x > xs = c qsafe + L + E~ proves q_ref <
+                // qsafe (alpha >= tau) and x < xc = c qcut + L - E~ proves
+                // q_ref > qcut (alpha < tau); the band between goes to the
+                // exact path.
+                constexpr float c_ex2 = -0.5f * 1.4426950408889634f;
                 const float mlx = cA.x - ucx, mly = cA.y - ucy;
                 const float ixx = cA.z, b2 = cA.w, iyy = cB.x;
                 const float bx = -(2.0f * ixx * mlx + b2 * mly);
                 const float by = -(b2 * mlx + 2.0f * iyy * mly);
                 const float c0 = (ixx * mlx * mlx + b2 * mlx * mly) + iyy * mly * mly;
+                const float L = fast_log2(cB.y);
                 const float X = fabsf(mlx) + 7.5f, Y = fabsf(mly) + 3.5f;
                 const float S = (fabsf(ixx) * X * X + fabsf(b2) * X * Y) + fabsf(iyy) * Y * Y;
-                const float E = S * 2.5e-6f;
+                const float E = (-c_ex2 * S + fabsf(L)) * 4e-6f;
                 const float inf = __int_as_float(0x7f800000);
-                float qs = __fsub_rd(cB.w, E), qc = __fadd_ru(cB.z, E);
-                if (!(E < inf)) qs = -inf, qc = inf;  // no bound: every pixel is exact
-                sS[warp][r][0] = make_float4(ixx, b2, iyy, bx);
-                // {by, c0, band width w = qcut' - qsafe' (rounded up), qsafe'}:
-                // a pixel is in the band only if 0 <= q - qsafe' <= w (rounding
-                // is monotone, so fl(q - qsafe') <= w whenever q <= qcut';
-                // +inf/-inf thresholds give w = +inf)
-                sS[warp][r][1] = make_float4(by, c0, __fsub_ru(qc, qs), qs);
+                // qsafe = -inf (never fast) / qcut = +inf (no cut) stay infinite
+                float xs = cB.w == -inf ? inf : __fadd_ru(__fadd_ru(__fmul_ru(c_ex2, cB.w), L), E);
+                float xc = cB.z == inf ? -inf : __fsub_rd(__fadd_rd(__fmul_rd(c_ex2, cB.z), L), E);
+                if (!(E < inf) || xs != xs || xc != xc) xs = inf, xc = -inf;  // no bound: every pixel is exact
+                sS[warp][r][0] = make_float4(c_ex2 * ixx, c_ex2 * b2, c_ex2 * iyy, c_ex2 * bx);
+                // {c by, c c0 + L, band width w = xs - xc (rounded up), xs}: a
+                // pixel is in the band only if 0 <= xs - x <= w (rounding is
+                // monotone, so fl(xs - x) <= w whenever x >= xc; infinite
+                // thresholds give w = +inf); x > xs (fast) has the sign bit set
+                sS[warp][r][1] = make_float4(c_ex2 * by, __fmaf_rn(c_ex2, c0, L), __fsub_ru(xs, xc), xs);
                 // red carries the clamp flag in its sign (colours are >= 0):
                 // alpha_at's clamp can bind only for opacity >= clamp
-                sS[warp][r][2] = make_float4(cB.y >= aclamp ? -cC.x : cC.x, cC.y, cC.z, fast_log2(cB.y));
-                sS[warp][r][3] = make_float4(cA.x, cA.y, cB.y, 0.0f);
+                sS[warp][r][2] = make_float4(cB.y >= aclamp ? -cC.x : cC.x, cC.y, cC.z, 0.0f);
+                sS[warp][r][3] = cA;                                   // mx, my, ixx, 2ixy
+                sS[warp][r][4] = make_float4(cB.x, cB.y, 0.0f, 0.0f);  // iyy, opacity
                 sJ[warp][r] = static_cast<uint8_t>(lane);  // its index in the batch (P_it)
             }
             __syncwarp();
             for (uint32_t jj = 0; jj < nrel; ++jj) {
-                const float4 sa = sS[warp][jj][0];  // inv.xx, 2*inv.xy, inv.yy, bx
-                const float4 sb = sS[warp][jj][1];  // by, c0, qcut' - qsafe', qsafe'
-                const float4 sc = sS[warp][jj][2];  // +-r, g, b, log2 opacity
-                const float qB = __fmaf_rn(sa.y, lxl, sb.x);                     // 2ixy lx + by
-                const float qC = __fmaf_rn(__fmaf_rn(sa.x, lxl, sa.w), lxl, sb.y);  // (ixx lx + bx) lx + c0
-                const float l2op = sc.w;
-                const float qsafe = sb.w;
+                const float4 sa = sS[warp][jj][0];  // c {inv.xx, 2*inv.xy, inv.yy, bx}
+                const float4 sb = sS[warp][jj][1];  // c by, c c0 + L, xs - xc, xs
+                const float4 sc = sS[warp][jj][2];  // +-r, g, b
+                const float qB = __fmaf_rn(sa.y, lxl, sb.x);                     // c (2ixy lx + by)
+                const float qC = __fmaf_rn(__fmaf_rn(sa.x, lxl, sa.w), lxl, sb.y);  // c ((ixx lx + bx) lx + c0) + L
+                const float xs = sb.w;
                 const uint32_t wbits = __float_as_uint(sb.z);
                 if (STATS) {
                     ++st_it;
@@ -504,35 +512,35 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 // which bounds the image difference to the reference by
                 // 1e-4 per channel; the warp stops when all are saturated.
                 // Fast pixels blend under a predicate (no zeroed alphas).  The
-                // band test compares float bits unsigned: q - qsafe' < 0 (a
-                // fast pixel) has the sign bit set and exceeds any w >= 0; NaN
+                // band test compares float bits unsigned: xs - x < 0 (a fast
+                // pixel) has the sign bit set and exceeds any w >= 0; NaN
                 // exceeds +inf (never blends, as in the reference).  It admits
-                // a superset of the band (pixels just above qcut'); the exact
+                // a superset of the band (pixels just below xc); the exact
                 // path rejects those by its own alpha >= tau test.
                 uint32_t dmin = 0xffffffffu;
                 bool fast[PPT];
-                float e[PPT], qv[PPT];
+                float e[PPT], xv[PPT];
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
-                    const float q = __fmaf_rn(__fmaf_rn(sa.z, lyl[k], qB), lyl[k], qC);
-                    qv[k] = q;
-                    fast[k] = q < qsafe;
-                    e[k] = fast_exp2(__fmaf_rn(q, c_ex2, l2op));
-                    dmin = umin(dmin, __float_as_uint(q - qsafe));
+                    const float x = __fmaf_rn(__fmaf_rn(sa.z, lyl[k], qB), lyl[k], qC);
+                    xv[k] = x;
+                    fast[k] = x > xs;
+                    e[k] = fast_exp2(x);
+                    dmin = umin(dmin, __float_as_uint(xs - x));
                     if (STATS) {
                         st_fast += fast[k] && T[k] >= tfloor;
-                        st_need += __float_as_uint(q - qsafe) <= wbits;
+                        st_need += __float_as_uint(xs - x) <= wbits;
                     }
                 }
                 const bool need_any = dmin <= wbits;
-                if (STATS) {  // iterations in which no pixel of the unit is within q <= qcut
+                if (STATS) {  // iterations in which no pixel of the unit is within x >= xc
                     bool any_in = false;
 #pragma unroll
-                    for (int k = 0; k < PPT; ++k) any_in = any_in || !(qv[k] > qsafe + sb.z);
+                    for (int k = 0; k < PPT; ++k) any_in = any_in || !(xv[k] < xs - sb.z);
                     st_empty += !__any_sync(0xffffffffu, any_in);
-                    bool any_live = false;  // ... or within q <= qcut of no live (T >= floor) pixel
+                    bool any_live = false;  // ... or within x >= xc of no live (T >= floor) pixel
 #pragma unroll
-                    for (int k = 0; k < PPT; ++k) any_live = any_live || (T[k] >= tfloor && !(qv[k] > qsafe + sb.z));
+                    for (int k = 0; k < PPT; ++k) any_live = any_live || (T[k] >= tfloor && !(xv[k] < xs - sb.z));
                     st_dead += !__any_sync(0xffffffffu, any_live);
                 }
                 if (CLAMP && __float_as_int(sc.x) < 0) {  // clamp flag (opacity >= clamp)
@@ -549,16 +557,17 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                     T[k] = __fmaf_rn(-e[k], T[k], T[k]);
                 }
                 if (__any_sync(0xffffffffu, need_any)) {  // margin band: the reference's alpha_at
-                    const float4 sd = sS[warp][jj][3];  // mx, my, opacity
+                    const float4 sd = sS[warp][jj][3];  // mx, my, ixx, 2ixy (unscaled)
+                    const float2 se = *reinterpret_cast<const float2*>(&sS[warp][jj][4]);  // iyy, opacity
                     const float dx = (ucx + lxl) - sd.x;  // px - mx, as the reference rounds it
-                    const float t1 = sa.x * dx * dx;
-                    const float t2 = sa.y * dx;
+                    const float t1 = sd.z * dx * dx;
+                    const float t2 = sd.w * dx;
 #pragma unroll
                     for (int k = 0; k < PPT; ++k) {
-                        if (!(__float_as_uint(qv[k] - qsafe) <= wbits)) continue;
+                        if (!(__float_as_uint(xs - xv[k]) <= wbits)) continue;
                         const float dy = (ucy + lyl[k]) - sd.y;
-                        const float qr = (t1 + t2 * dy) + sa.z * dy * dy;  // reference order
-                        const float a = exact_alpha(qr, sd.z, aclamp, sTab);
+                        const float qr = (t1 + t2 * dy) + se.x * dy * dy;  // reference order
+                        const float a = exact_alpha(qr, se.y, aclamp, sTab);
                         if (a < tau) continue;
                         const float t_cur = T[k];
                         const float wgt = a * t_cur;
