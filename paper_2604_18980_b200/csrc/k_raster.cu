@@ -349,7 +349,6 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
     // form and blend data read every iteration, sS[w][j][3..4] = {P0, iyy,
     // opacity} (unscaled) for the exact path only
     __shared__ __align__(16) float4 sS[NWB][32][5];
-    __shared__ uint8_t sJ[NWB][32];  // batch index of staged record r
     __shared__ uint64_t sTab[32];
     __shared__ __align__(16) float sOut[NWB][8 * 16 * 3];
 
@@ -483,16 +482,16 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 sS[warp][r][1] = make_float4(c_ex2 * by, __fmaf_rn(c_ex2, c0, L), __fsub_ru(xs, xc), xs);
                 // red carries the clamp flag in its sign (colours are >= 0):
                 // alpha_at's clamp can bind only for opacity >= clamp
-                sS[warp][r][2] = make_float4(cB.y >= aclamp ? -cC.x : cC.x, cC.y, cC.z, 0.0f);
+                // .w: the record's index in the batch (P_it)
+                sS[warp][r][2] = make_float4(cB.y >= aclamp ? -cC.x : cC.x, cC.y, cC.z, __int_as_float(lane));
                 sS[warp][r][3] = cA;                                   // mx, my, ixx, 2ixy
                 sS[warp][r][4] = make_float4(cB.x, cB.y, 0.0f, 0.0f);  // iyy, opacity
-                sJ[warp][r] = static_cast<uint8_t>(lane);  // its index in the batch (P_it)
             }
             __syncwarp();
             for (uint32_t jj = 0; jj < nrel; ++jj) {
                 const float4 sa = sS[warp][jj][0];  // c {inv.xx, 2*inv.xy, inv.yy, bx}
                 const float4 sb = sS[warp][jj][1];  // c by, c c0 + L, xs - xc, xs
-                const float4 sc = sS[warp][jj][2];  // +-r, g, b
+                const float4 sc = sS[warp][jj][2];  // +-r, g, b, batch index
                 const float qB = __fmaf_rn(sa.y, lxl, sb.x);                     // c (2ixy lx + by)
                 const float qC = __fmaf_rn(__fmaf_rn(sa.x, lxl, sa.w), lxl, sb.y);  // c ((ixx lx + bx) lx + c0) + L
                 const float xs = sb.w;
@@ -579,7 +578,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 }
                 const float tmax = fmaxf(fmaxf(T[0], T[1]), fmaxf(T[2], T[3]));
                 if (!__any_sync(0xffffffffu, tmax >= tfloor)) {
-                    death = base - start + sJ[warp][jj] + 1;
+                    death = base - start + static_cast<uint32_t>(__float_as_int(sc.w)) + 1;
                     all_done = true;
                     break;
                 }
