@@ -82,6 +82,44 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
     const uint64_t n = n_dev ? *n_dev : n_host;
     uint64_t lo, hi;
     chunk_of(n, gridDim.x, blockIdx.x, lo, hi);
+    auto count_key = [&](K key, bool ok) {
+        const uint32_t vmask = __ballot_sync(0xffffffffu, ok);
+        if (!vmask) return;
+        const uint32_t d = digit_of(static_cast<K>(key - static_cast<K>(bias)), shift);
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(vmask) - 1);
+        if (__all_sync(0xffffffffu, !ok || d == d0)) {
+            if (lane == 0) sh[warp][d0] += __popc(vmask);
+        } else if (ok) {
+            atomicAdd(&sh[warp][d], 1u);
+        }
+    };
+    if constexpr (sizeof(K) == 4) {
+        // 32-bit keys: 16-byte loads (4 keys), four in flight per thread
+        // (chunks start on whole tiles, so the vectors are aligned)
+        const uint64_t hv = lo + ((hi - lo) & ~uint64_t(3));
+        constexpr int U = 4;
+        for (uint64_t base = lo; base < hv; base += 4 * U * kSortThreads) {
+            uint4 q[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t i = base + 4 * (static_cast<uint64_t>(u) * kSortThreads + tid);
+                q[u] = i < hv ? *reinterpret_cast<const uint4*>(keys + i) : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const bool in = base + 4 * (static_cast<uint64_t>(u) * kSortThreads + tid) < hv;
+                const uint32_t e[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    count_key(static_cast<K>(e[j]), in && !(use_sentinel && static_cast<K>(e[j]) == sentinel));
+            }
+        }
+        for (uint64_t base = hv; base < hi; base += kSortThreads) {  // at most 3 keys
+            const uint64_t i = base + tid;
+            const K key = i < hi ? keys[i] : K(0);
+            count_key(key, i < hi && !(use_sentinel && key == sentinel));
+        }
+    } else {
     constexpr int U = 8;  // keys in flight per thread
     for (uint64_t base = lo; base < hi; base += U * kSortThreads) {
         K k[U];
@@ -104,6 +142,7 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
                 atomicAdd(&sh[warp][d], 1u);
             }
         }
+    }
     }
     __syncthreads();
     uint32_t c = 0;
