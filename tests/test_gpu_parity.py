@@ -433,6 +433,53 @@ def test_raster_known_answers(ctx, port):
     assert img[8, 8, 0] == np.float32(0.25) and img[8, 8, 1] == np.float32(0.5) and img[8, 8, 2] == np.float32(0.75)
 
 
+def test_raster_extreme_splats_default_vs_oracle(ctx, port):
+    """The default rasteriser's unit-centred exponent and its widened
+    thresholds on splats far from the synthetic scenes: condition
+    numbers up to 1e5 (the fp64 blend-cull data and the all-exact fallback),
+    sub-pixel and 300-pixel footprints, centres far outside the image,
+    opacities from tau to 1 (the clamp variant of the stage path), every
+    alpha >= tau decision the reference's: max abs <= 1e-3, PSNR >= 50 dB."""
+    rng = np.random.default_rng(77)
+    n, w, h = 4000, 333, 250
+    theta = rng.uniform(0, np.pi, n)
+    major = np.exp(rng.uniform(np.log(0.3), np.log(300.0), n))
+    kappa = np.exp(rng.uniform(0, np.log(1e5), n))
+    minor = np.maximum(major / np.sqrt(kappa), 0.05)
+    c, sn = np.cos(theta), np.sin(theta)
+    cxx = major**2 * c * c + minor**2 * sn * sn
+    cyy = major**2 * sn * sn + minor**2 * c * c
+    cxy = (major**2 - minor**2) * c * sn
+    cov = np.stack([cxx, cxy, cyy], 1).astype(np.float32)
+    det = cov[:, 0] * cov[:, 2] - cov[:, 1] * cov[:, 1]
+    keep = det > 0
+    cov, det = cov[keep], det[keep]
+    m = len(cov)
+    s = np.zeros(m, capi.SPLAT_DTYPE)
+    inv = np.float32(1) / det
+    s["cov2d"] = cov
+    s["inv_cov"] = np.stack([cov[:, 2] * inv, -cov[:, 1] * inv, cov[:, 0] * inv], 1)
+    s["mean2d"] = np.stack([rng.uniform(-400, w + 400, m), rng.uniform(-400, h + 400, m)], 1)
+    op = rng.choice(np.float32([1 / 255 + 1e-6, 0.02, 0.3, 0.7, 0.98, 0.99, 0.999, 1.0]), m)
+    s["opacity"] = op
+    s["th"] = np.float32(1 / 255)
+    s["depth"] = rng.uniform(0.3, 90, m)
+    s["rgb"] = rng.uniform(0, 1, (m, 3))
+    tiles = ((w + 15) // 16) * ((h + 15) // 16)
+    ocfg = port.config("ellipse")
+    okeys, oidx, _ = port.generate_pairs(s, w, h, "ellipse", ocfg)
+    osk, osi, org = port.sort_pairs(okeys, oidx, tiles)
+    want = port.raster(s, osk, osi, org, w, h, ocfg)
+    keys, idx, _ = ctx.generate_pairs(s, w, h, "ellipse", gpu_cfg("ellipse"))
+    sk, si, rg = ctx.sort_pairs(keys, idx, tiles)
+    assert np.array_equal(sk, osk) and np.array_equal(si, osi)
+    exact = ctx.raster(s, si, rg, w, h, gpu_cfg("ellipse", exact=True))
+    assert np.array_equal(exact.view(np.uint32), want.view(np.uint32))
+    got = ctx.raster(s, si, rg, w, h, gpu_cfg("ellipse"))
+    assert np.max(np.abs(got - want)) <= IMG_MAX_ABS
+    assert psnr(got, want) >= IMG_MIN_PSNR
+
+
 def test_stage_preprocess_matches_oracle(ctx, port):
     oscene, dev = scene_pair(port, ctx, 2, 3000, "ramp", 2, 640, 480, 500.0)
     for mode, k, bins in (("ellipse", 0.0, None), ("adagscale", 0.5, [0.7] * 20)):
