@@ -260,8 +260,17 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             uint32_t pm = full ? 0xffffffffu : __ballot_sync(0xffffffffu, ok[it]);
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-                pm &= ((d >> b) & 1u) ? bal : ~bal;
+                // one predicate per bit: the ballot, then keep the lanes whose
+                // bit agrees (pm &= bal ^ flip, flip = ~0 where the bit is clear)
+                uint32_t bal;
+                asm("{\n\t.reg .pred p;\n\t"
+                    "setp.ne.u32 p, %2, 0;\n\t"
+                    "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+                    "@!p not.b32 %0, %0;\n\t"
+                    "and.b32 %0, %0, %1;\n\t}"
+                    : "=r"(bal)
+                    : "r"(pm), "r"(d & (1u << b)));
+                pm = bal;
             }
             peers[it] = pm;
         }
