@@ -101,10 +101,7 @@ __device__ __forceinline__ void warp_rank(const uint64_t (&k)[NC], int nvalid, P
         const uint32_t d = dg(k[c]);
         uint32_t pm = __ballot_sync(0xffffffffu, ok);
 #pragma unroll
-        for (int b = 0; b < 8; ++b) {
-            const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            pm &= ((d >> b) & 1u) ? bal : ~bal;
-        }
+        for (int b = 0; b < 8; ++b) pm = ballot_agree(pm, d & (1u << b));
         const uint32_t lt = pm & lt_mask;
         const uint32_t before = hist[d];
         rank[c] = before + __popc(lt);

@@ -65,7 +65,7 @@ __device__ __forceinline__ void chunk_of(uint64_t n, int G, int c, uint64_t& lo,
 }
 
 // Upsweep: per-chunk 256-bin digit counts -> counts[d][c] (warp-private
-// shared histograms; a warp whose 32 digits agree adds once).
+// shared histograms).
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads)
 k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, int shift, int use_sentinel,
@@ -76,22 +76,17 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
     if (!bias_of(sb, bias, wide)) return;
     constexpr int W = kSortThreads / 32;
     __shared__ uint32_t sh[W][256];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5;
     for (int i = tid; i < W * 256; i += kSortThreads) (&sh[0][0])[i] = 0;
     __syncthreads();
     const uint64_t n = n_dev ? *n_dev : n_host;
     uint64_t lo, hi;
     chunk_of(n, gridDim.x, blockIdx.x, lo, hi);
+    // a shared-memory atomic per key into the warp's histogram (warp
+    // aggregation of equal digits measured slower: its vote/shuffle/vote per
+    // key costs more than the rare conflicts it avoids)
     auto count_key = [&](K key, bool ok) {
-        const uint32_t vmask = __ballot_sync(0xffffffffu, ok);
-        if (!vmask) return;
-        const uint32_t d = digit_of(static_cast<K>(key - static_cast<K>(bias)), shift);
-        const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(vmask) - 1);
-        if (__all_sync(0xffffffffu, !ok || d == d0)) {
-            if (lane == 0) sh[warp][d0] += __popc(vmask);
-        } else if (ok) {
-            atomicAdd(&sh[warp][d], 1u);
-        }
+        if (ok) atomicAdd(&sh[warp][digit_of(static_cast<K>(key - static_cast<K>(bias)), shift)], 1u);
     };
     if constexpr (sizeof(K) == 4) {
         // 32-bit keys: 16-byte loads (4 keys), four in flight per thread
@@ -131,17 +126,7 @@ k_upsweep(const K* __restrict__ keys, const uint32_t* n_dev, uint64_t n_host, in
             ok[u] = i < hi && !(use_sentinel && k[u] == sentinel);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t vmask = __ballot_sync(0xffffffffu, ok[u]);
-            if (!vmask) continue;
-            const uint32_t d = digit_of(static_cast<K>(k[u] - static_cast<K>(bias)), shift);
-            const uint32_t d0 = __shfl_sync(0xffffffffu, d, __ffs(vmask) - 1);
-            if (__all_sync(0xffffffffu, !ok[u] || d == d0)) {
-                if (lane == 0) sh[warp][d0] += __popc(vmask);
-            } else if (ok[u]) {
-                atomicAdd(&sh[warp][d], 1u);
-            }
-        }
+        for (int u = 0; u < U; ++u) count_key(k[u], ok[u]);
     }
     }
     __syncthreads();
@@ -259,19 +244,7 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
             const uint32_t d = digit_of(static_cast<K>(k[it] - static_cast<K>(bias)), shift);
             uint32_t pm = full ? 0xffffffffu : __ballot_sync(0xffffffffu, ok[it]);
 #pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                // one predicate per bit: the ballot, then keep the lanes whose
-                // bit agrees (pm &= bal ^ flip, flip = ~0 where the bit is clear)
-                uint32_t bal;
-                asm("{\n\t.reg .pred p;\n\t"
-                    "setp.ne.u32 p, %2, 0;\n\t"
-                    "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
-                    "@!p not.b32 %0, %0;\n\t"
-                    "and.b32 %0, %0, %1;\n\t}"
-                    : "=r"(bal)
-                    : "r"(pm), "r"(d & (1u << b)));
-                pm = bal;
-            }
+            for (int b = 0; b < 8; ++b) pm = ballot_agree(pm, d & (1u << b));
             peers[it] = pm;
         }
 #pragma unroll
