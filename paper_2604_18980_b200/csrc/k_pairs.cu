@@ -51,6 +51,18 @@ __device__ __forceinline__ void emit_hits_rec(const FrameParams& p, const SplatP
         unsigned long long mask = static_cast<unsigned long long>(r.x) | (static_cast<unsigned long long>(r.y) << 32);
         const int tx0 = static_cast<int>(r.z & 0xffffu), ty0 = static_cast<int>(r.z >> 16);
         const int sw = static_cast<int>(r.w);
+        if (sw <= 32) {  // row by row: 32-bit bit scans, no row tracking per pair
+            const uint32_t rm = sw == 32 ? 0xffffffffu : ((1u << sw) - 1u);
+            for (int row = 0; mask; ++row, mask >>= sw) {
+                uint32_t bits = static_cast<uint32_t>(mask) & rm;
+                while (bits) {
+                    const int b = __ffs(bits) - 1;
+                    bits &= bits - 1u;
+                    f(tx0 + b, ty0 + row);
+                }
+            }
+            return;
+        }
         int row = 0, row_end = sw;  // bits arrive in increasing order: track the row, no division
         while (mask) {
             const int b = __ffsll(static_cast<long long>(mask)) - 1;
