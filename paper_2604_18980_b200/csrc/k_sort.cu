@@ -281,6 +281,19 @@ k_downsweep(const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __re
         }
         __syncthreads();
         const uint32_t tn = s_tile_n;
+        if (!co.src && tn == static_cast<uint32_t>(kSortTile)) {  // a full tile: unrolled, no bounds
+#pragma unroll
+            for (int j = 0; j < kSortItems; ++j) {
+                const uint32_t i = static_cast<uint32_t>(tid + j * kSortThreads);
+                const K key = s_keys[i];
+                const uint32_t pos = s_pos[digit_of(static_cast<K>(key - static_cast<K>(bias)), shift)] + i;
+                kout[pos] = key;
+                vout[pos] = s_vals[i];
+            }
+            s_base[tid] += count;
+            __syncthreads();
+            continue;
+        }
         const uint32_t tn_round = (tn + 31u) & ~31u;  // whole warps for the aggregated atomics
         for (uint32_t i = tid; i < tn_round; i += kSortThreads) {
             const bool act = i < tn;
