@@ -101,6 +101,9 @@ FrameParams make_params(const agsx_camera& cam, const agsx_config& cfg, const ag
             p.lut_ext = lut_ext_dev;
         }
     }
+    // TUpperLUT::value_at's bin width (lut.hpp:16-25), one IEEE division here
+    // instead of one per Gaussian (the host and device quotients are equal)
+    p.lut_w = (p.lut_dmax - p.lut_dmin) / static_cast<float>(p.lut_n);
     return p;
 }
 

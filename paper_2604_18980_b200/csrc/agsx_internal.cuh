@@ -40,6 +40,7 @@ struct FrameParams {
     int adaptive;
     float lut_dmin, lut_dmax;
     int lut_n;
+    float lut_w;  // (lut_dmax - lut_dmin) / lut_n, IEEE on the host (the same float as per thread)
     float lut[kLutInline];
     const float* lut_ext;  // device copy when lut_n > kLutInline
 };

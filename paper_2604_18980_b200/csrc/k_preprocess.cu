@@ -36,8 +36,7 @@ __device__ __constant__ float kShC3[7] = {-0.5900435899266435f, 2.89061144264055
 
 // TUpperLUT::value_at (lut.hpp:16-25) with x86 float->int semantics.
 __device__ __forceinline__ float lut_value(const FrameParams& p, float depth) {
-    const float w = (p.lut_dmax - p.lut_dmin) / static_cast<float>(p.lut_n);
-    int b = f2i_x86((depth - p.lut_dmin) / w);
+    int b = f2i_x86((depth - p.lut_dmin) / p.lut_w);
     if (b < 0) b = 0;
     if (b >= p.lut_n) b = p.lut_n - 1;
     return p.lut_ext ? p.lut_ext[b] : p.lut[b];
