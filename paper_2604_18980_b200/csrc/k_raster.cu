@@ -488,7 +488,8 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                 sS[warp][r][4] = make_float4(cB.x, cB.y, 0.0f, 0.0f);  // iyy, opacity
             }
             __syncwarp();
-            for (uint32_t jj = 0; jj < nrel; ++jj) {
+            uint32_t jj = 0;  // nrel >= 1: the exit test sits at the bottom
+            do {
                 const float4 sa = sS[warp][jj][0];  // c {inv.xx, 2*inv.xy, inv.yy, bx}
                 const float4 sb = sS[warp][jj][1];  // c by, c c0 + L, xs - xc, xs
                 const float4 sc = sS[warp][jj][2];  // +-r, g, b, batch index
@@ -582,7 +583,7 @@ k_raster_units(FrameParams p, const uint2* __restrict__ ranges, const uint32_t* 
                     all_done = true;
                     break;
                 }
-            }
+            } while (++jj < nrel);
             __syncwarp();
         }
 
