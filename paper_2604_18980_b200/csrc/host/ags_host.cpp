@@ -435,23 +435,68 @@ float* thread_staging(std::size_t n) {
     return st.get(n);
 }
 
-// The returned Image owns a std::vector<float> (image.hpp:9-23).  Filling it
-// from the staging image in one pass (no zero-initialisation first), with
-// transparent huge pages requested for the fresh buffer, halves the host
-// cost of the 191 MB vector at 4608x3456 (page faults dominate).
-void fill_image(Image& img, int w, int h, const float* src) {
-    img.width = w;
-    img.height = h;
-    const std::size_t n = static_cast<std::size_t>(w) * h * 3;
-    img.data.clear();
-    img.data.shrink_to_fit();
-    img.data.reserve(n);
-    const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(img.data.data());
-    const std::uintptr_t a = (b + (1u << 21) - 1) & ~static_cast<std::uintptr_t>((1u << 21) - 1);
-    const std::uintptr_t e = (b + n * sizeof(float)) & ~static_cast<std::uintptr_t>((1u << 21) - 1);
-    if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // advisory: ignore failures
-    img.data.assign(src, src + n);
-}
+// The returned Image owns a std::vector<float> (image.hpp:9-23).  A fresh
+// 191 MB vector (4608x3456) costs its page faults, a zero fill and the copy:
+// ~40 ms a call on one thread.  ImageFill splits that around the GPU frame:
+// start() (before the frame) reserves the buffer with transparent huge pages
+// and faults it in on host threads while the GPU renders; finish() (after
+// it) copies the staging image in by slices on host threads, then sizes the
+// vector by assign() over its own storage -- the copy already made the
+// values, the assignment copies each float onto itself (glibc's memmove
+// returns at once when source and destination coincide), so no single-
+// threaded zero fill is paid.  Images under 512 KB take the one-pass assign.
+class ImageFill {
+public:
+    ImageFill(Image& img, int w, int h) : img_(img), n_(static_cast<std::size_t>(w) * h * 3) {
+        img.width = w;
+        img.height = h;
+        // one host thread per 256 KB of image, up to 16 (320x240: 3 slices)
+        const std::size_t by_size = std::max<std::size_t>(1, n_ >> 16);
+        nt_ = static_cast<unsigned>(std::min<std::size_t>({16, by_size, std::max(1u, std::thread::hardware_concurrency())}));
+        per_ = ((n_ + nt_ - 1) / nt_ + 1023) & ~std::size_t{1023};  // 4 KB-aligned slices
+        img.data.clear();
+        img.data.shrink_to_fit();
+        img.data.reserve(n_);
+        if (nt_ == 1) return;
+        const std::uintptr_t b = reinterpret_cast<std::uintptr_t>(img.data.data());
+        const std::uintptr_t a = (b + (1u << 21) - 1) & ~static_cast<std::uintptr_t>((1u << 21) - 1);
+        const std::uintptr_t e = (b + n_ * sizeof(float)) & ~static_cast<std::uintptr_t>((1u << 21) - 1);
+        if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);  // advisory: ignore failures
+        // fault the reserved pages in (one byte store per 4 KB page) while the frame renders
+        volatile char* base = reinterpret_cast<volatile char*>(img.data.data());
+        for (unsigned t = 0; t < nt_; ++t)
+            if (t * per_ < n_)
+                faulting_.emplace_back([base, lo = t * per_ * sizeof(float), hi = std::min(n_, (t + 1) * per_) * sizeof(float)] {
+                    for (std::size_t i = lo; i < hi; i += 4096) base[i] = 0;
+                });
+    }
+    ~ImageFill() { join(); }
+    void finish(const float* src) {
+        join();
+        if (nt_ == 1) {
+            img_.data.assign(src, src + n_);
+            return;
+        }
+        float* dst = img_.data.data();  // reserved storage: the copy creates the floats in it
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < nt_; ++t)
+            if (t * per_ < n_)
+                pool.emplace_back([=, this] { std::memcpy(dst + t * per_, src + t * per_, (std::min(n_, (t + 1) * per_) - t * per_) * sizeof(float)); });
+        std::memcpy(dst, src, std::min(n_, per_) * sizeof(float));
+        for (auto& th : pool) th.join();
+        img_.data.assign(dst, dst + n_);  // capacity suffices: no reallocation, a self-copy
+    }
+
+private:
+    void join() {
+        for (auto& th : faulting_) th.join();
+        faulting_.clear();
+    }
+    Image& img_;
+    std::size_t n_, per_ = 0;
+    unsigned nt_ = 1;
+    std::vector<std::thread> faulting_;
+};
 
 agsx_ctx* thread_ctx() {
     static thread_local CtxHolder h;
@@ -619,6 +664,7 @@ RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderCon
     std::vector<float> maxt_by_gid;
     agsx_frame f{};
     f.image = staging;
+    ImageFill fill(rep.image, cam.width, cam.height);
     if (rec.max_t) {
         maxt_by_gid.assign(std::max<std::uint64_t>(scene.size(), 1), 0.0f);
         f.max_t = maxt_by_gid.data();
@@ -639,7 +685,7 @@ RenderReport render(const DeviceScene& scene, const Camera& cam, const RenderCon
     } else {
         check(agsx_render(ctx, sc, &c, &k, lut ? &l : nullptr, &f), ctx);
     }
-    fill_image(rep.image, cam.width, cam.height, staging);
+    fill.finish(staging);
     rep.pair_count = f.pair_count;
     rep.splat_count = f.splat_count;
     rep.stage_times["preprocess"] = f.stage_ms[0] * 1e-3;

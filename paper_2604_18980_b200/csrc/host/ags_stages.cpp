@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <thread>
 
 #include "agsx.h"
@@ -244,6 +245,14 @@ RenderReport render(std::span<const Gaussian3D> scene, const Camera& cam, const 
         return render(dev, cam, cfg, lut, rec);
     }
     SceneCache& c = scene_cache();
+    if (c.dev && c.data == scene.data() && c.size == scene.size()) {
+        // Same span as the cached copy: render from it while host threads
+        // fingerprint the span, and keep the frame only if the span is
+        // unchanged (else upload it and render again below).
+        auto fp_now = std::async(std::launch::async, [scene] { return scene_fingerprint(scene); });
+        RenderReport rep = render(*c.dev, cam, cfg, lut, rec);
+        if (fp_now.get() == c.fp) return rep;
+    }
     const std::uint64_t fp = scene_fingerprint(scene);
     if (!c.dev || c.data != scene.data() || c.size != scene.size() || c.fp != fp) {
         c.dev.reset();  // free the previous copy before uploading the next
