@@ -1041,7 +1041,8 @@ def test_tile_sizes_above_64(ctx, port):
 def test_kept_frames_past_the_pinned_cap(tmp_path):
     """a caller that keeps its frames. Page-locked images
     are capped (AGS_PINNED_POOL_MB); past the cap render() returns ordinary
-    arrays. Every kept frame stays intact and equal to a fresh render."""
+    arrays, filled from the renderer's staging block (f32 and PPM bytes). Every
+    kept frame stays intact and equal to a fresh render."""
     import subprocess
     import sys
 
@@ -1054,6 +1055,10 @@ def test_kept_frames_past_the_pinned_cap(tmp_path):
         "for v in range(8):\n"
         "    again = P.render(s, v % 4, 'ellipse')['image']\n"
         "    assert np.array_equal(kept[v].view(np.uint32), again.view(np.uint32)), v\n"
+        "kept8 = [P.render(s, v % 4, 'ellipse', image_u8=True)['image'] for v in range(8)]\n"
+        "for v in range(8):\n"
+        "    again = P.render(s, v % 4, 'ellipse', image_u8=True)['image']\n"
+        "    assert np.array_equal(kept8[v], again), v\n"
         "print('ok', pinned)\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     env = dict(os.environ, AGS_PINNED_POOL_MB="2")  # two 0.9 MB frames fit
