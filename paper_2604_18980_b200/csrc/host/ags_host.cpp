@@ -573,9 +573,11 @@ agsx_splat_view to_c(const SplatView& s) {
 static_assert(sizeof(SplatView) == sizeof(agsx_splat_view), "SplatView layout");
 
 // Pads SH to the largest degree present (zero coefficients are bit-neutral,
-// preprocess.cpp:71-101) and packs the AoS scene into SoA arrays.
+// preprocess.cpp:71-101) and packs the AoS scene into SoA arrays.  The arrays
+// are allocated uninitialised and written once by host threads (each thread
+// takes its slice's page faults), so no single-threaded zero fill is paid.
 struct PackedScene {
-    std::vector<float> mean, scale, rot, op, sh;
+    std::unique_ptr<float[]> mean, scale, rot, op, sh;
     int D = 1;
 };
 
@@ -587,11 +589,12 @@ PackedScene pack(std::span<const Gaussian3D> scene) {
         throw std::invalid_argument("sh coefficient count must be 3*d^2 for d in {1,2,3,4}");
     p.D = static_cast<int>(maxc / 3);
     const std::size_t n = scene.size();
-    p.mean.resize(3 * n);
-    p.scale.resize(3 * n);
-    p.rot.resize(4 * n);
-    p.op.resize(n);
-    p.sh.assign(maxc * n, 0.0f);
+    const std::size_t m = std::max<std::size_t>(n, 1);
+    p.mean.reset(new float[3 * m]);
+    p.scale.reset(new float[3 * m]);
+    p.rot.reset(new float[4 * m]);
+    p.op.reset(new float[m]);
+    p.sh.reset(new float[maxc * m]);
     auto run = [&](std::size_t lo, std::size_t hi) {
         for (std::size_t i = lo; i < hi; ++i) {
             const Gaussian3D& g = scene[i];
@@ -606,7 +609,9 @@ PackedScene pack(std::span<const Gaussian3D> scene) {
             p.rot[4 * i + 2] = g.rotation.y;
             p.rot[4 * i + 3] = g.rotation.z;
             p.op[i] = g.opacity;
-            std::copy(g.sh.begin(), g.sh.end(), p.sh.begin() + maxc * i);
+            float* sh = p.sh.get() + maxc * i;
+            std::copy(g.sh.begin(), g.sh.end(), sh);
+            std::fill(sh + g.sh.size(), sh + maxc, 0.0f);
         }
     };
     // AoS -> SoA by host threads (the per-Gaussian SH vectors are separate
@@ -629,7 +634,7 @@ using namespace detail;
 
 DeviceScene::DeviceScene(std::span<const Gaussian3D> scene) {
     const PackedScene p = pack(scene);
-    agsx_scene_desc d{scene.size(), p.D, p.mean.data(), p.scale.data(), p.rot.data(), p.op.data(), p.sh.data()};
+    agsx_scene_desc d{scene.size(), p.D, p.mean.get(), p.scale.get(), p.rot.get(), p.op.get(), p.sh.get()};
     agsx_ctx* ctx = thread_ctx();
     agsx_scene* s = nullptr;
     check(agsx_scene_upload(ctx, &d, &s), ctx);
